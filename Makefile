@@ -1,0 +1,30 @@
+# Builds the sm_100a C-ABI library in-tree (it travels to the GPU box with
+# the gpurun snapshot; git ignores *.so/*.o).
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude \
+             -Ipaper_1707_03268_b200/csrc --expt-relaxed-constexpr
+SRC_DIR   := paper_1707_03268_b200/csrc
+OBJ_DIR   := build/obj
+LIB       := paper_1707_03268_b200/lib/libdpm_b200.so
+SRCS      := $(wildcard $(SRC_DIR)/*.cu)
+OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
+HDRS      := include/dpm_b200.h $(wildcard $(SRC_DIR)/*.cuh)
+
+all: $(LIB)
+
+$(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(OBJ_DIR)
+	$(NVCC) $(NVFLAGS) $(EXTRA) -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+
+ptxas: EXTRA := -Xptxas -v
+ptxas: clean all
+
+clean:
+	rm -rf $(OBJ_DIR) $(LIB)
+
+.PHONY: all clean ptxas

@@ -1,0 +1,424 @@
+"""Benchmark of the DPM score path (BASELINE.json metric) on B200.
+
+Workload (config 4): 64 seeded 1280x720 images (HOG pyramids, 49 levels,
+441,041 cells x 32 ch each), the 54-filter model (3 mirrored pairs of a
+6x11 root + 8 parts 6x6 one octave finer) on a shared rank-8 basis from the
+reference's cp_als, unbounded GDT placement, root + parts assembly and tau
+compaction.  A step scores the whole 64-image batch (sharded 64/N over N
+GPUs, one process per GPU; the only collective is the final detection
+gather).  Metric: cell x filter evaluations per second (20,013,786 per
+image); images/s alongside.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W]          # this repo
+  python bench.py --impl reference [--steps K] [--warmup W]    # CPU reference arm
+
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  The device-resident inputs (3.6 GB at N=1) exceed
+the 126 MB L2, so no explicit flush is needed between steps.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CFG = 4
+N_IMAGES = 64
+RANK = 8
+METRIC = "DPM cell*filter evals/s (decomposed conv + GDT + assembly)"
+UNIT = "evals/s"
+
+
+# ---------------------------------------------------------------- CPU leg
+
+def _cpu_task(task):
+    """One (image, root level, component) of config 4 through the oracle:
+    project, correlate root + parts (reference correlate3_full on the
+    projected level), place parts with r* and gather, assemble."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import dpm_oracle as O
+    from paper_1707_03268_b200 import synth
+
+    img, i, ci = task
+    wl = _cpu_task.wl
+    C, cores = _cpu_task.C, _cpu_task.cores
+    pyr, bank = wl.pyramid, wl.bank
+    kr, kp = pyr.root_levels[i], pyr.part_levels[i]
+    lv = [np.zeros((1, 1, 32), np.float32)] * len(pyr.levels)
+    lv = list(lv)
+    lv[kr] = synth.hog_level(CFG, img, kr, *pyr.levels[kr])
+    lv[kp] = synth.hog_level(CFG, img, kp, *pyr.levels[kp])
+    t0 = time.perf_counter()
+    res, maps = O.score_pyramid(lv, bank, C, cores, root_levels=[kr], part_levels=[kp],
+                                components=[bank.components[ci]])
+    dt = time.perf_counter() - t0
+    evals = sum(m.size for m in maps.values())
+    return evals, dt
+
+
+def _cpu_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
+    from paper_1707_03268_b200 import synth
+    from paper_1707_03268_b200.pipeline import cores_from_stacked
+
+    wl = synth.workload(CFG)
+    fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg{CFG}_R{RANK}.npz"))
+    _cpu_task.wl = wl
+    _cpu_task.C = fx["C"]
+    _cpu_task.cores = cores_from_stacked(wl.bank, fx["G"])
+
+
+def _cpu_sample_tasks(image, n_root, stride=4):
+    return [(image, i, c) for i in range(0, n_root, stride) for c in range(6)]
+
+
+def cpu_run(tasks, workers):
+    """Wall time of ``tasks`` on a spawn pool of ``workers`` processes."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers, initializer=_cpu_init) as pool:
+        pool.map(_cpu_task, tasks[:workers], chunksize=1)  # warm the workers
+        t0 = time.perf_counter()
+        out = pool.map(_cpu_task, tasks, chunksize=1)
+        wall = time.perf_counter() - t0
+    return sum(e for e, _ in out), wall
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during a timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = str(device_index)
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.dev, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- helpers
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def _traffic():
+    """K2 dram bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(REPO, "profiles", "k2_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_03268_b200 import synth
+    from paper_1707_03268_b200.dist import gather_detections, shard
+    from paper_1707_03268_b200.pipeline import PyramidScorer
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = synth.workload(CFG)
+    fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg{CFG}_R{RANK}.npz"))
+    mine = list(shard(args.images, world, rank))
+    n = len(mine)
+    sc = PyramidScorer(wl.bank, fx["C"], fx["G"], wl.pyramid, n_images=n,
+                       outputs=("totals",), max_dets=args.max_dets)
+    plan = sc.plan
+    host = sc.host_arena(pinned=True)
+    for j, img in enumerate(mine):
+        sc.fill_host(host, j, synth.hog_pyramid(CFG, img, wl.pyramid))
+    plan.X.copy_(host)
+    stream = torch.cuda.current_stream()
+
+    # tau: keep ~0.1% of roots (calibrated once on this rank's first image)
+    plan.run()
+    torch.cuda.synchronize()
+    tot = np.concatenate([plan.assembly_outputs(0, a)["totals"].cpu().numpy().ravel()
+                          for a in range(len(plan.assemblies))])
+    tau = float(np.quantile(tot, 0.999)) if args.tau is None else args.tau
+    if world > 1:
+        t = torch.tensor([tau], device="cuda", dtype=torch.float64)
+        dist.broadcast(t, 0)
+        tau = float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        plan.run(tau=tau)
+    barrier()
+
+    # ---- device-resident timing (value); K2 share via events on the same stream
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            plan.run(tau=tau, stages=("project",))
+            ev[k][1].record(stream)
+            plan.run(tau=tau, stages=("correlate",))
+            ev[k][2].record(stream)
+            plan.run(tau=tau, stages=("place",))
+            ev[k][3].record(stream)
+        barrier()
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    k2_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    k34_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    total_ms = max_over_ranks(sum(step_ms))
+    ms_per_step = total_ms / args.steps
+
+    evals_img = sc.evals_per_image()
+    evals_step = evals_img * args.images
+    value = evals_step * args.steps / (total_ms / 1e3)
+    images_s = args.images * args.steps / (total_ms / 1e3)
+
+    # ---- end to end through the public API: pinned H2D + run + D2H detections
+    for _ in range(max(1, args.warmup // 2)):
+        sc.score_batch(host, tau)
+    barrier()
+    e2e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ndets = []
+    with ClockSampler(local) as clocks_e2e:
+        barrier()
+        e2e_ev[0].record(stream)
+        for _ in range(args.steps):
+            d = sc.score_batch(host, tau)
+            if world > 1:
+                d = gather_detections(d, device="cuda")
+            ndets.append(len(d))
+        e2e_ev[1].record(stream)
+        barrier()
+    e2e_ms = max_over_ranks(e2e_ev[0].elapsed_time(e2e_ev[1]))
+    e2e_value = evals_step * args.steps / (e2e_ms / 1e3)
+    from paper_1707_03268_b200._lib import DETECTION
+    d2h = 4 + int(statistics.mean(ndets)) * DETECTION.itemsize
+
+    # ---- FFMA peak probe (roofline denominator for K2)
+    from paper_1707_03268_b200 import _lib
+    import ctypes
+
+    sink = torch.zeros(148 * 16, device="cuda")
+    flops = ctypes.c_double(0)
+    lib = _lib.lib()
+    lib.dpm_ffma_probe(sink.data_ptr(), 64, ctypes.byref(flops), stream.cuda_stream)
+    pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    pe[0].record(stream)
+    for _ in range(5):
+        lib.dpm_ffma_probe(sink.data_ptr(), 2048, ctypes.byref(flops), stream.cuda_stream)
+    pe[1].record(stream)
+    torch.cuda.synchronize()
+    probe_tflops = 5 * flops.value / (pe[0].elapsed_time(pe[1]) / 1e3) / 1e12
+
+    peaks = _peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nominal_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    k2_flops = sc.k2_flops_per_image() * n
+    k2_avg_ms = statistics.mean(k2_ms)
+    achieved = k2_flops / (k2_avg_ms / 1e3) / 1e12
+    traffic = _traffic()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tasks = _cpu_sample_tasks(image=0, n_root=len(wl.pyramid.root_levels))
+        workers = os.cpu_count() or 1
+        evals, wall = cpu_run(tasks, workers)
+        cpu = {"value": evals / wall, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"image 0, root levels 0,4,...,36 x 6 components ({len(tasks)} "
+                         f"(level, component) tasks, {evals} evals) on a {workers}-process pool "
+                         f"of the numpy oracle; {wall:.1f} s wall"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp32 (K1/K2 FFMA) + f64 (K3/K4 placement)", "data": "synthetic",
+            "config": {"workload": f"config {CFG}: {args.images} x 1280x720 HOG pyramids "
+                                   "(49 levels, 441,041 cells x 32 ch), 54 filters (3 mirrored "
+                                   "pairs: root 6x11 + 8 parts 6x6 at 2x), shared rank-8 basis, "
+                                   "unbounded GDT (r*) + assembly + tau compaction",
+                       "images": args.images, "evals_per_image": evals_img,
+                       "parallelism": f"image shards x{world}",
+                       "l2": "inputs 3.6 GB per step > 126 MB L2 (no flush needed)"},
+            "images_per_s": images_s,
+            "stage_ms": {"k1_project": statistics.mean(k1_ms), "k2_correlate": k2_avg_ms,
+                         "k3k4_place_assemble": statistics.mean(k34_ms)},
+            "roofline": {"kernel": "K2 shortened correlation (all launch classes)",
+                         "bound": "fp32", "achieved": achieved,
+                         "peak": nominal_tflops, "unit": "TFLOP/s",
+                         "frac": achieved / nominal_tflops,
+                         "peak_source": f"148 SMs x 128 FFMA x 2 x {sm_max:.0f} MHz "
+                                        "(MEASURED_PEAKS.json sm_max_mhz; no FP32 number there)",
+                         "ffma_probe_tflops": probe_tflops,
+                         "frac_of_probe": achieved / probe_tflops,
+                         "algorithmic_flops_per_launch": k2_flops,
+                         "traffic": traffic},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sc.h2d_bytes(),
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+                    "detections_per_step": statistics.mean(ndets), "tau": tau},
+            "gpu_launches": 6 * args.steps,
+            "clocks": clocks.summary(),
+            "clocks_e2e": clocks_e2e.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_1707_03268_b200 import synth
+
+    wl = synth.workload(CFG)
+    workers = os.cpu_count() or 1
+    n_root = len(wl.pyramid.root_levels)
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    times, evals = [], 0
+    with ctx.Pool(workers, initializer=_cpu_init) as pool:
+        for k in range(args.warmup + args.steps):
+            tasks = _cpu_sample_tasks(image=k % N_IMAGES, n_root=n_root, stride=8)
+            t0 = time.perf_counter()
+            out = pool.map(_cpu_task, tasks, chunksize=1)
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                times.append(dt)
+                evals = sum(e for e, _ in out)
+    total = sum(times)
+    value = evals * len(times) / total
+    sample = (f"per step: one image, root levels 0,8,...,32 x 6 components ({len(tasks)} "
+              f"(level, component) tasks, {evals} evals) of config {CFG} on a {workers}-process "
+              "pool of the numpy oracle port (the reference is pure Python and cannot travel "
+              "to the GPU box)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"config {CFG} sample (CPU)", "images": 1,
+                   "evals_per_step": evals},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--images", type=int, default=N_IMAGES)
+    ap.add_argument("--tau", type=float, default=None)
+    ap.add_argument("--max-dets", type=int, default=1 << 20)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * dpm_b200.h -- C ABI of the B200 DPM score path (libdpm_b200.so, sm_100a).
+ *
+ * Drop-in boundary for the reference package's scoring path
+ * (/root/reference/pkg/src/cpdetect).  The reference is pure Python/numpy
+ * and has no FFI of its own; each entry point below names the reference
+ * function it replaces, and INTEGRATION.md shows the ctypes binding a
+ * maintainer adds on the reference side.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every array argument is DEVICE memory
+ *    unless its name ends in `_host`.  Offsets inside descriptor structs are
+ *    element offsets (floats / doubles / bytes as documented) from the base
+ *    pointer passed to the call, so one descriptor table serves any buffer.
+ *  - Every call takes a cudaStream_t as `void* stream` (NULL = legacy
+ *    default stream) and is asynchronous on it; no call synchronises, none
+ *    allocates device memory, none keeps global mutable state.  Results are
+ *    deterministic (fixed reduction order, no atomics on score sums).
+ *  - Return value: DPM_OK (0) or a negative dpm_status; dpm_last_error()
+ *    returns a thread-local message naming the offending field.
+ *
+ * Layouts (HBM)
+ *  - Feature level X: float32 [H][W][L] (channel fastest; reference
+ *    check_feature_map order, validation.py:65-86).
+ *  - Projected level P: float32 planar [R][H][pitch], pitch >= W, pitch % 4 == 0.
+ *  - Core G of a filter group: float32 [h][w][R][nf_pad] (filter fastest).
+ *  - Response maps S: float32 [nf][H-h+1][W-w+1].
+ */
+#ifndef DPM_B200_H
+#define DPM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPM_ABI_VERSION 1
+#define DPM_MAX_PARTS 16
+
+typedef enum {
+  DPM_OK = 0,
+  DPM_ERR_ARG = -1,         /* invalid shape / descriptor -> ValidationError */
+  DPM_ERR_UNSUPPORTED = -2, /* valid but not supported by this build        */
+  DPM_ERR_CUDA = -3,        /* CUDA runtime failure -> DeviceError           */
+  DPM_ERR_NUMERIC = -4      /* non-finite inputs where finiteness is required */
+} dpm_status;
+
+/* ------------------------------------------------------------------ misc */
+int dpm_abi_version(void);
+const char* dpm_last_error(void);
+/* SM count and compute capability of `device` (sizing persistent grids). */
+int dpm_device_query(int device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---------------------------------------------------------- K1: project
+ * P[r][y][x] = sum_l X[y][x][l] * C[l][r]
+ * Replaces the channel contraction of _term_stack (correlation.py:128) and,
+ * with C = identity, the channel layout change feeding correlate3_full
+ * (correlation.py:92-112).  One job per (image, level). */
+typedef struct {
+  int64_t x_off;  /* float offset of the level's X block [H][W][L]          */
+  int64_t p_off;  /* float offset of the level's P block [R][H][pitch]      */
+  int32_t H, W;
+  int32_t pitch;  /* P row pitch in floats, >= W, multiple of 4             */
+  int32_t block0; /* first CTA of this job; set by dpm_project_prepare      */
+} dpm_proj_job;
+
+/* Fills block0 of every job (host table) and returns the CTA count to pass
+ * to dpm_project (negative dpm_status on error). */
+int64_t dpm_project_prepare(dpm_proj_job* jobs_host, int njobs);
+int dpm_project(const float* X, float* P, const float* C, int L, int R,
+                const dpm_proj_job* jobs, int njobs, int64_t nblocks, void* stream);
+
+/* ------------------------------------------- K2: shortened correlation
+ * S_f[y][x] = sum_{i<h, j<w, r<R} G[i][j][r][f] * P[chan_off + r][y+i][x+j]
+ * Implicit GEMM over (position x filter) with K = h*w*R, FP32 FFMA.
+ * Replaces correlate3_cp (correlation.py:155-167; G[i][j][r] = w_r a_ir b_jr
+ * over the filter's own c-projected channels), cp_partial_stack
+ * (correlation.py:170-180; prefix k is a filter whose core keeps ranks <= k,
+ * so prefixes are bit-identical to correlate3_cp(upto = k+1)) and
+ * correlate3_full (correlation.py:92-112; C = identity, G = the filter). */
+typedef struct {
+  int64_t p_off;     /* float offset of the (image, level) P block           */
+  int64_t s_off;     /* float offset of the output maps [nf][Ho][Wo]         */
+  int64_t g_off;     /* float offset of the group's core [h][w][R][nf_pad]   */
+  int32_t H, W, pitch, chan_off;
+  int32_t h, w, R, nf;
+  int32_t nf_pad;    /* filter stride of the core: nf rounded up to 8        */
+  int32_t mode;      /* reserved, 0                                          */
+  int32_t range_idx; /* >= 0: fold per-map max/min into ranges[range_idx+f]  */
+  int32_t pad;
+} dpm_corr_job;
+
+/* One CTA work item: tile (ty, tx) of job `job`. */
+typedef struct {
+  int32_t job, ty, tx, pad;
+} dpm_corr_tile;
+
+/* Tile geometry the planner must use for a launch class (h, nf):
+ * tile_w x tile_h output positions per tile; returns warps per CTA, or a
+ * negative dpm_status if (h, nf) has no specialised kernel (then the
+ * generic kernel is used: tile 32 x 8, 8 warps). */
+int dpm_correlate_tile_shape(int h, int nf, int* tile_w, int* tile_h);
+
+/* All tiles of one call must belong to jobs with the same (h, nf, R) class
+ * and max filter width <= w_max.  `ranges` (uint32 pairs: ordered-key max,
+ * ordered-key min; may be NULL) collects per-map extrema for r*. */
+int dpm_correlate(const float* P, const float* G, float* S, const dpm_corr_job* jobs,
+                  const dpm_corr_tile* tiles, int ntiles, int h, int nf, int R,
+                  int w_max, uint32_t* ranges, void* stream);
+
+/* Initialise `n` range slots to (-inf, +inf). */
+int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
+
+/* ---------------------------------------- K3: part placement (FP64)
+ * Penalised max over a window around centre = scale*root + anchor,
+ * separable: x pass then y pass, strict '>' in ascending offset order
+ * (ties -> smallest (dy, dx)), penalty subtracted in two stages exactly as
+ * _placement_grid (detection.py:320-373).  radius >= 0: reference windowed
+ * semantics; radius < 0: unbounded generalised distance transform, realised
+ * as the window of radius r* computed from the map's range (SURVEY.md
+ * App. A.2 lemma; requires c_dxx, c_dyy > 0). */
+typedef struct {
+  int64_t s_off;     /* float offset of the part response map [Hp][Wp]       */
+  int64_t dx_off;    /* int16 offset of the x-pass argmax table [Hp][wr]     */
+  int32_t Hp, Wp;
+  int32_t ay, ax;
+  int32_t scale;
+  int32_t radius;    /* >= 0 windowed, < 0 GDT via r*                        */
+  int32_t rx0, wr;   /* root columns handled (centres scale*rx + ax)         */
+  int32_t range_idx; /* range slot of the map (GDT mode)                     */
+  int32_t block0;    /* first CTA of the x pass; set by dpm_place_prepare    */
+  double cdx, cdy, cdxx, cdyy;
+} dpm_place_job;
+
+/* ------------------------------------------ K4: root + parts assembly
+ * total[ry][rx] = S_root[ry][rx] + sum_i placed_i(ry, rx) + bias
+ * (detection.py:449, 509-519), with the y pass of every part fused in.
+ * Optional outputs: totals (double), packed part positions (uint32
+ * y << 16 | x), per-part placed values (double), and detections with
+ * total >= tau appended to `dets` (count in *det_count). */
+typedef struct {
+  int64_t root_off;   /* float offset of the root map, < 0: no root term      */
+  int64_t total_off;  /* double offset of totals [hr][wr], < 0: not written   */
+  int64_t pos_off;    /* uint32 offset of positions [nparts][hr][wr], < 0: no */
+  int64_t placed_off; /* double offset of placed [nparts][hr][wr], < 0: no    */
+  int32_t root_pitch; /* row pitch of the root map                            */
+  int32_t ry0, ry1, rx0, rx1;
+  int32_t part_job0;  /* first dpm_place_job of this assembly                 */
+  int32_t nparts;
+  int32_t image, level, component;
+  int32_t block0;     /* first CTA; set by dpm_assemble_prepare               */
+  int32_t pad;
+  double bias;
+} dpm_asm_job;
+
+typedef struct {
+  int32_t image, level, component, ry, rx, nparts;
+  double score;
+  uint32_t parts[DPM_MAX_PARTS]; /* y << 16 | x */
+} dpm_detection;
+
+int64_t dpm_place_prepare(dpm_place_job* jobs_host, int njobs);
+int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs);
+
+/* x pass of every placement job (writes the int16 argmax tables). */
+int dpm_place_xpass(const float* S, int16_t* dx, const dpm_place_job* jobs, int njobs,
+                    int64_t nblocks, const uint32_t* ranges, void* stream);
+
+/* y pass + assembly. */
+int dpm_assemble(const float* S, const int16_t* dx, const dpm_place_job* pjobs,
+                 const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
+                 const uint32_t* ranges, double* total, uint32_t* pos, double* placed,
+                 double tau, dpm_detection* dets, int max_dets, int* det_count,
+                 void* stream);
+
+/* ----------------------------------------------------- micro-benchmark
+ * FP32 FFMA peak probe used by bench.py for the K2 roofline denominator:
+ * `iters` dependent-chain-free FFMA blocks on every SM; returns via
+ * *flops the FLOPs the launch performs. */
+int dpm_ffma_probe(float* sink, int iters, double* flops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPM_B200_H */

@@ -1,0 +1,67 @@
+// Shared helpers of libdpm_b200.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdarg>
+#include <cstdio>
+
+#include "dpm_b200.h"
+
+namespace dpm {
+
+// Thread-local message of the last failing ABI call (dpm_last_error()).
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define DPM_REQUIRE(cond, ...)                  \
+  do {                                          \
+    if (!(cond)) {                              \
+      ::dpm::set_error(__VA_ARGS__);            \
+      return DPM_ERR_ARG;                       \
+    }                                           \
+  } while (0)
+
+#define DPM_CUDA(call)                                                          \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess) {                                                    \
+      ::dpm::set_error("%s failed: %s", #call, cudaGetErrorString(e_));         \
+      return DPM_ERR_CUDA;                                                      \
+    }                                                                           \
+  } while (0)
+
+// Launch-error check after <<<>>>.
+#define DPM_LAUNCHED(name)                                                      \
+  do {                                                                          \
+    cudaError_t e_ = cudaGetLastError();                                        \
+    if (e_ != cudaSuccess) {                                                    \
+      ::dpm::set_error("%s launch failed: %s", name, cudaGetErrorString(e_));   \
+      return DPM_ERR_CUDA;                                                      \
+    }                                                                           \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Order-preserving float <-> uint32 key (max over keys == max over floats).
+__device__ __forceinline__ uint32_t float_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_float(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+// Find the job owning CTA `b` in a table sorted by block0 (binary search).
+template <typename Job>
+__device__ __forceinline__ int find_job(const Job* jobs, int njobs, int64_t b) {
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].block0 <= b) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace dpm

@@ -1,0 +1,328 @@
+// K2: shortened multi-filter cross-correlation (implicit GEMM, FP32 FFMA).
+//
+//   S_f[y][x] = sum_{i<h, j<w, r<R} G[i][j][r][f] * P[chan_off + r][y+i][x+j]
+//
+// GEMM view: M = output positions, N = filters, K = h*w*R.  Reference:
+// _term_stack + cumsum (correlation.py:115-180) for per-filter CP models and
+// correlate3_full (correlation.py:92-112) for dense filters (C = identity).
+//
+// Tiling.  A CTA owns a 32-wide x (nwy*MP)-tall tile of output positions of
+// one (image, level) and all filters of one group.  Warp w takes filter
+// subset w % nwf (NF filters) and row band w / nwf (MP rows); lane = x.
+// The projected tile (+ (h-1, w-1) halo) and the group's core are staged in
+// shared memory channel-chunk by channel-chunk (8 ranks at a time), planar,
+// so a warp's 32 column reads of one (r, row) hit 32 consecutive words.
+// Each thread keeps an (MP + FH - 1)-tall register column of P for a fixed
+// (j, r) and slides it over the FH filter rows: per (j, r) it issues
+// MP + FH - 1 conflict-free LDS.32 plus FH broadcast vector loads of G for
+// FH*MP*NF FFMAs (6*8*8 = 384 FFMAs per 25 loads for 6x6 parts).
+//
+// Persistent CTAs walk the tile list with a grid stride; a group's core is
+// re-staged only when the group changes (all part tiles of a DPM model
+// share one group, so it is staged once per CTA when R <= 8).
+#include "common.cuh"
+
+namespace dpm {
+
+constexpr int K2_MP = 8;       // output rows per thread
+constexpr int K2_RCH = 8;      // ranks staged per chunk
+constexpr int K2_MAX_WARPS = 12;
+
+template <int NF>
+__device__ __forceinline__ void load_g(float (&g)[NF], const float* p) {
+  if constexpr (NF % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < NF / 4; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(p)[q];
+      g[4 * q] = v.x; g[4 * q + 1] = v.y; g[4 * q + 2] = v.z; g[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NF / 2; ++q) {
+      const float2 v = reinterpret_cast<const float2*>(p)[q];
+      g[2 * q] = v.x; g[2 * q + 1] = v.y;
+    }
+  }
+}
+
+struct CorrArgs {
+  const float* P;
+  const float* G;
+  float* S;
+  const dpm_corr_job* jobs;
+  const dpm_corr_tile* tiles;
+  int ntiles;
+  int nwf, nwy;
+  int w_max;
+  uint32_t* ranges;
+};
+
+__device__ __forceinline__ void fold_range(uint32_t* ranges, int slot, float vmax, float vmin) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+  }
+  if ((threadIdx.x & 31) == 0 && vmax >= vmin) {
+    atomicMax(ranges + 2 * slot, float_key(vmax));
+    atomicMin(ranges + 2 * slot + 1, float_key(vmin));
+  }
+}
+
+template <int FH, int NF>
+__global__ void __launch_bounds__(32 * K2_MAX_WARPS)
+corr_kernel(const CorrArgs a) {
+  constexpr int MP = K2_MP;
+  constexpr int COL = MP + FH - 1;
+  extern __shared__ __align__(16) float smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wf = warp % a.nwf, wy = warp / a.nwf;
+  const int TY = a.nwy * MP;
+  const int TROWS = TY + FH - 1;
+  const int TPITCH = 32 + a.w_max - 1;
+  float* sP = smem;                                             // [RCH][TROWS][TPITCH]
+  float* sG = smem + ((K2_RCH * TROWS * TPITCH + 3) & ~3);      // [FH][w][RCH][nf_pad]
+
+  int64_t staged_g = -1;
+  int staged_chunk = -1;
+  for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const dpm_corr_tile tile = a.tiles[t];
+    const dpm_corr_job job = a.jobs[tile.job];
+    const int ho = job.H - FH + 1, wo = job.W - job.w + 1;
+    const int y0 = tile.ty * TY, x0 = tile.tx * 32;
+    const int w = job.w, nfp = job.nf_pad;
+    const int tcols = 32 + w - 1;
+    const int64_t plane = (int64_t)job.H * job.pitch;
+
+    float acc[MP][NF];
+#pragma unroll
+    for (int p = 0; p < MP; ++p)
+#pragma unroll
+      for (int f = 0; f < NF; ++f) acc[p][f] = 0.f;
+
+    for (int rc = 0; rc < job.R; rc += K2_RCH) {
+      const int nr = min(K2_RCH, job.R - rc);
+      __syncthreads();  // previous users of sP / sG are done
+      // stage the core chunk unless it is already resident
+      if (staged_g != job.g_off || staged_chunk != rc) {
+        const int per_ij = nr * nfp;
+        const int total = FH * w * per_ij;
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
+          const int ij = e / per_ij, rem = e - ij * per_ij;
+          sG[ij * per_ij + rem] = __ldg(a.G + job.g_off + ((int64_t)ij * job.R + rc) * nfp + rem);
+        }
+        staged_g = job.g_off;
+        staged_chunk = rc;
+      }
+      // stage the P chunk: nr planes x TROWS x tcols (zero outside the level)
+      {
+        const int per_plane = TROWS * tcols;
+        const float* pbase = a.P + job.p_off + (int64_t)(job.chan_off + rc) * plane;
+        for (int e = threadIdx.x; e < nr * per_plane; e += blockDim.x) {
+          const int r = e / per_plane, rem = e - r * per_plane;
+          const int row = rem / tcols, col = rem - row * tcols;
+          const int gy = y0 + row, gx = x0 + col;
+          float v = 0.f;
+          if (gy < job.H && gx < job.W) v = __ldg(pbase + r * plane + (int64_t)gy * job.pitch + gx);
+          sP[(r * TROWS + row) * TPITCH + col] = v;
+        }
+      }
+      __syncthreads();
+
+      const float* pw = sP + (wy * MP) * TPITCH + lane;
+      const float* gw = sG + wf * NF;
+      const int gstride_i = w * nr * nfp;
+      for (int j = 0; j < w; ++j) {
+        for (int r = 0; r < nr; ++r) {
+          const float* pc = pw + r * TROWS * TPITCH + j;
+          float col[COL];
+#pragma unroll
+          for (int q = 0; q < COL; ++q) col[q] = pc[q * TPITCH];
+          const float* gp = gw + (j * nr + r) * nfp;
+#pragma unroll
+          for (int i = 0; i < FH; ++i) {
+            float g[NF];
+            load_g<NF>(g, gp + i * gstride_i);
+#pragma unroll
+            for (int p = 0; p < MP; ++p)
+#pragma unroll
+              for (int f = 0; f < NF; ++f) acc[p][f] = fmaf(col[p + i], g[f], acc[p][f]);
+          }
+        }
+      }
+    }
+
+    // epilogue: coalesced stores (lane = x), optional per-map range fold
+    const int x = x0 + lane;
+    const int yb = y0 + wy * MP;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int fg = wf * NF + f;
+      float vmax = -INFINITY, vmin = INFINITY;
+      if (fg < job.nf) {
+        float* dst = a.S + job.s_off + (int64_t)fg * ho * wo;
+#pragma unroll
+        for (int p = 0; p < MP; ++p) {
+          const int y = yb + p;
+          if (x < wo && y < ho) {
+            dst[(int64_t)y * wo + x] = acc[p][f];
+            vmax = fmaxf(vmax, acc[p][f]);
+            vmin = fminf(vmin, acc[p][f]);
+          }
+        }
+      }
+      if (a.ranges != nullptr && job.range_idx >= 0 && wf * NF + f < job.nf)
+        fold_range(a.ranges, job.range_idx + fg, vmax, vmin);
+    }
+  }
+}
+
+// Generic fallback: any h, any nf; one thread per (position, filter loop).
+__global__ void __launch_bounds__(256)
+corr_generic_kernel(const CorrArgs a) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const dpm_corr_tile tile = a.tiles[t];
+    const dpm_corr_job job = a.jobs[tile.job];
+    const int ho = job.H - job.h + 1, wo = job.W - job.w + 1;
+    const int x = tile.tx * 32 + tx, y = tile.ty * 8 + ty;
+    if (x >= wo || y >= ho) continue;
+    const int64_t plane = (int64_t)job.H * job.pitch;
+    const float* pb = a.P + job.p_off + (int64_t)job.chan_off * plane + (int64_t)y * job.pitch + x;
+    for (int f = 0; f < job.nf; ++f) {
+      float acc = 0.f;
+      for (int j = 0; j < job.w; ++j)
+        for (int r = 0; r < job.R; ++r)
+          for (int i = 0; i < job.h; ++i)
+            acc = fmaf(__ldg(pb + r * plane + (int64_t)i * job.pitch + j),
+                       __ldg(a.G + job.g_off + (((int64_t)i * job.w + j) * job.R + r) * job.nf_pad + f),
+                       acc);
+      a.S[job.s_off + ((int64_t)f * ho + y) * wo + x] = acc;
+      if (a.ranges != nullptr && job.range_idx >= 0) {
+        atomicMax(a.ranges + 2 * (job.range_idx + f), float_key(acc));
+        atomicMin(a.ranges + 2 * (job.range_idx + f) + 1, float_key(acc));
+      }
+    }
+  }
+}
+
+__global__ void ranges_init_kernel(uint32_t* ranges, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    ranges[2 * i] = 0u;             // key(-inf) > 0, any value beats it
+    ranges[2 * i + 1] = 0xffffffffu;
+  }
+}
+
+// ------------------------------------------------------------ dispatch
+struct Shape {
+  int nf_kernel, nwf, nwy;
+};
+
+static bool pick(int h, int nf, Shape* s) {
+  if (nf < 1) return false;
+  if (nf <= 8) {
+    s->nf_kernel = nf <= 2 ? 2 : nf <= 4 ? 4 : nf <= 6 ? 6 : 8;
+    s->nwf = 1;
+    s->nwy = 4;
+  } else {
+    s->nf_kernel = 8;
+    s->nwf = (nf + 7) / 8;
+    if (s->nwf > 6) return false;
+    s->nwy = s->nwf >= 3 ? 1 : 2;
+  }
+  switch (h) {
+    case 2: case 3: case 4: case 5: case 6: case 7: case 8: case 11: case 15: return true;
+    default: return false;
+  }
+}
+
+typedef void (*corr_fn)(const CorrArgs);
+
+template <int FH>
+static corr_fn by_nf(int nfk) {
+  switch (nfk) {
+    case 2: return corr_kernel<FH, 2>;
+    case 4: return corr_kernel<FH, 4>;
+    case 6: return corr_kernel<FH, 6>;
+    default: return corr_kernel<FH, 8>;
+  }
+}
+
+static corr_fn kernel_for(int h, int nfk) {
+  switch (h) {
+    case 2: return by_nf<2>(nfk);
+    case 3: return by_nf<3>(nfk);
+    case 4: return by_nf<4>(nfk);
+    case 5: return by_nf<5>(nfk);
+    case 6: return by_nf<6>(nfk);
+    case 7: return by_nf<7>(nfk);
+    case 8: return by_nf<8>(nfk);
+    case 11: return by_nf<11>(nfk);
+    default: return by_nf<15>(nfk);
+  }
+}
+
+}  // namespace dpm
+
+using namespace dpm;
+
+extern "C" int dpm_correlate_tile_shape(int h, int nf, int* tile_w, int* tile_h) {
+  DPM_REQUIRE(tile_w && tile_h, "dpm_correlate_tile_shape: null output");
+  Shape s;
+  *tile_w = 32;
+  if (pick(h, nf, &s)) {
+    *tile_h = s.nwy * K2_MP;
+    return s.nwf * s.nwy;
+  }
+  *tile_h = 8;
+  return DPM_ERR_UNSUPPORTED;
+}
+
+extern "C" int dpm_ranges_init(uint32_t* ranges, int n, void* stream) {
+  DPM_REQUIRE(ranges && n >= 0, "dpm_ranges_init: bad arguments");
+  if (n == 0) return DPM_OK;
+  ranges_init_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(ranges, n);
+  DPM_LAUNCHED("ranges_init_kernel");
+  return DPM_OK;
+}
+
+extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm_corr_job* jobs,
+                             const dpm_corr_tile* tiles, int ntiles, int h, int nf, int R,
+                             int w_max, uint32_t* ranges, void* stream) {
+  DPM_REQUIRE(P && G && S && jobs && tiles, "dpm_correlate: null pointer");
+  DPM_REQUIRE(ntiles >= 0, "dpm_correlate: ntiles=%d", ntiles);
+  DPM_REQUIRE(h >= 1 && w_max >= 1 && w_max <= 64, "dpm_correlate: h=%d w_max=%d", h, w_max);
+  DPM_REQUIRE(R >= 1 && nf >= 1, "dpm_correlate: R=%d nf=%d", R, nf);
+  if (ntiles == 0) return DPM_OK;
+  int dev = 0, sms = 148;
+  DPM_CUDA(cudaGetDevice(&dev));
+  DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CorrArgs a{P, G, S, jobs, tiles, ntiles, 1, 1, w_max, ranges};
+  Shape s;
+  if (!pick(h, nf, &s)) {
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 8);
+    corr_generic_kernel<<<grid, 256, 0, as_stream(stream)>>>(a);
+    DPM_LAUNCHED("corr_generic_kernel");
+    return DPM_OK;
+  }
+  a.nwf = s.nwf;
+  a.nwy = s.nwy;
+  const int TROWS = s.nwy * K2_MP + h - 1;
+  const int TPITCH = 32 + w_max - 1;
+  const int nfp = (nf + 7) & ~7;  // core filter stride (dpm_corr_job.nf_pad)
+  const size_t smem = sizeof(float) * ((((size_t)K2_RCH * TROWS * TPITCH) + 3 & ~(size_t)3) +
+                                       (size_t)h * w_max * K2_RCH * nfp);
+  DPM_REQUIRE(smem <= 227 * 1024, "dpm_correlate: h=%d w=%d nf=%d needs %zu B shared memory",
+              h, w_max, nf, smem);
+  corr_fn fn = kernel_for(h, s.nf_kernel);
+  DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  const int threads = 32 * s.nwf * s.nwy;
+  DPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+  fn<<<grid, threads, smem, as_stream(stream)>>>(a);
+  DPM_LAUNCHED("corr_kernel");
+  return DPM_OK;
+}

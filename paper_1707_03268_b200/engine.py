@@ -1,0 +1,426 @@
+"""Planner + executor of the B200 score path (K1 -> K2 -> K3 -> K4).
+
+A :class:`Plan` is built once per (geometry, model) on the host: it lays
+out the HBM arenas, groups filters into GEMM launch classes, builds the
+device work-lists, and uploads the model's basis and cores.  ``run()`` then
+issues one launch per kernel (one K2 launch per filter-shape class) on a
+CUDA stream, with no host synchronisation, so a run can be captured into a
+CUDA graph.  PyTorch is only the allocator / stream provider here.
+
+HBM layout (per image, images stacked):
+  X arena : levels back to back, each [H][W][L] float32 (the reference's
+            axis-major feature-map order, validation.py:65-86)
+  P arena : levels back to back, each planar [Rtot][H][pitch] float32
+  S arena : response maps, one block [nf][Ho][Wo] per (level, filter group)
+  DX arena: x-pass argmax tables, [Hp][wr] int16 per placed part
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .device import require_cuda, stream_handle, upload_table
+from .errors import ValidationError
+
+__all__ = ["FilterDef", "PartDef", "AssemblyDef", "Plan", "MAX_GROUP"]
+
+MAX_GROUP = 48  # filters per K2 group (6 warps x 8 filters)
+
+
+@dataclass(frozen=True)
+class FilterDef:
+    """Core of one filter over ``R`` consecutive basis channels from ``chan_off``."""
+
+    core: np.ndarray  # (h, w, R) float32
+    chan_off: int = 0
+
+    @property
+    def h(self):
+        return self.core.shape[0]
+
+    @property
+    def w(self):
+        return self.core.shape[1]
+
+    @property
+    def R(self):
+        return self.core.shape[2]
+
+
+@dataclass(frozen=True)
+class PartDef:
+    level: int
+    filt: int
+    anchor: tuple
+    deformation: tuple
+    radius: int  # >= 0 windowed (reference), < 0 unbounded GDT (r*)
+    scale: int = 1
+
+
+@dataclass(frozen=True)
+class AssemblyDef:
+    root: tuple  # (level, filt) or None
+    rect: tuple  # (ry0, ry1, rx0, rx1) inclusive root positions
+    parts: tuple = ()
+    bias: float = 0.0
+    level_tag: int = 0
+    component: int = 0
+
+
+def _round_up(v, m):
+    return (v + m - 1) // m * m
+
+
+@dataclass
+class _Arena:
+    size: int = 0
+
+    def take(self, n, align=32):
+        off = _round_up(self.size, align)
+        self.size = off + n
+        return off
+
+
+class Plan:
+    """Device plan for ``n_images`` images sharing one pyramid geometry.
+
+    Parameters
+    ----------
+    L : channels of the feature levels.
+    levels : [(H, W)] pyramid level shapes (per image).
+    C : (L, Rtot) float32 basis.
+    filters : [FilterDef].
+    apps : extra (level, filter) maps to compute besides those the
+        assemblies need.
+    assemblies : [AssemblyDef] (root + parts placed and summed).
+    outputs : subset of {"totals", "positions", "placed"}.
+    max_dets : capacity of the on-device detection buffer (0 = none).
+    """
+
+    def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
+                 outputs=("totals", "positions"), max_dets=0, device=None):
+        import torch
+
+        require_cuda()
+        self.torch = torch
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.L = int(L)
+        self.levels = [tuple(int(v) for v in lv) for lv in levels]
+        self.n_images = int(n_images)
+        C = np.ascontiguousarray(C, dtype=np.float32)
+        if C.ndim != 2 or C.shape[0] != self.L:
+            raise ValidationError(f"basis must be ({self.L}, R), got {C.shape}")
+        self.Rtot = C.shape[1]
+        self.filters = list(filters)
+        self.assemblies = list(assemblies)
+        self.outputs = set(outputs)
+        self.max_dets = int(max_dets)
+        for k, f in enumerate(self.filters):
+            if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
+                raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
+                                      f"outside the basis of rank {self.Rtot}")
+        self._layout(apps)
+        self._upload(C)
+
+    # ------------------------------------------------------------ layout
+    def _layout(self, apps):
+        lib = _lib.lib()
+        nimg = self.n_images
+        # which maps are needed
+        needed = set((int(a), int(b)) for a, b in apps)
+        for asm in self.assemblies:
+            if asm.root is not None:
+                needed.add(tuple(asm.root))
+            for p in asm.parts:
+                needed.add((p.level, p.filt))
+        for k, f in needed:
+            H, W = self.levels[k]
+            fd = self.filters[f]
+            if fd.h > H or fd.w > W:
+                raise ValidationError(f"filter extent ({fd.h}, {fd.w}) exceeds image extent "
+                                      f"({H}, {W})")
+        gdt_maps = set((p.level, p.filt) for a in self.assemblies for p in a.parts if p.radius < 0)
+
+        # per-image level offsets
+        xa, pa = _Arena(), _Arena()
+        self.x_level_off, self.p_level_off, self.pitch = [], [], []
+        for H, W in self.levels:
+            pitch = _round_up(W, 4)
+            self.pitch.append(pitch)
+            self.x_level_off.append(xa.take(H * W * self.L, align=4))
+            self.p_level_off.append(pa.take(self.Rtot * H * pitch, align=4))
+        self.x_image_stride = _round_up(xa.size, 32)
+        self.p_image_stride = _round_up(pa.size, 32)
+
+        # filter groups per level (same h, w, R, chan_off; <= MAX_GROUP filters)
+        by_level = {}
+        for k, f in sorted(needed):
+            by_level.setdefault(k, []).append(f)
+        self.groups = []  # (level, (filters...))
+        for k in sorted(by_level):
+            keyed = {}
+            for f in by_level[k]:
+                fd = self.filters[f]
+                keyed.setdefault((fd.h, fd.w, fd.R, fd.chan_off), []).append(f)
+            for key in sorted(keyed):
+                fl = keyed[key]
+                for s in range(0, len(fl), MAX_GROUP):
+                    self.groups.append((k, tuple(fl[s:s + MAX_GROUP])))
+
+        # cores: one block per distinct filter tuple
+        ga = _Arena()
+        self.core_off = {}
+        core_blocks = []
+        for _, fl in self.groups:
+            if fl in self.core_off:
+                continue
+            fd0 = self.filters[fl[0]]
+            nfp = _round_up(len(fl), 8)
+            block = np.zeros((fd0.h, fd0.w, fd0.R, nfp), dtype=np.float32)
+            for i, f in enumerate(fl):
+                block[:, :, :, i] = self.filters[f].core
+            self.core_off[fl] = ga.take(block.size, align=4)
+            core_blocks.append((self.core_off[fl], block))
+        self._core_host = np.zeros(max(ga.size, 4), dtype=np.float32)
+        for off, block in core_blocks:
+            self._core_host[off:off + block.size] = block.ravel()
+
+        # S arena, K2 jobs, tiles, range slots
+        sa = _Arena()
+        self.map_off = {}  # (image, level, filt) -> float offset
+        self.map_shape = {}
+        self.range_slot = {}
+        jobs, classes = [], {}
+        nslots = 0
+        for img in range(nimg):
+            for k, fl in self.groups:
+                H, W = self.levels[k]
+                fd = self.filters[fl[0]]
+                ho, wo = H - fd.h + 1, W - fd.w + 1
+                s_off = sa.take(len(fl) * ho * wo, align=4)
+                rng = -1
+                if any((k, f) in gdt_maps for f in fl):
+                    rng = nslots
+                    nslots += len(fl)
+                for i, f in enumerate(fl):
+                    self.map_off[(img, k, f)] = s_off + i * ho * wo
+                    self.map_shape[(k, f)] = (ho, wo)
+                    if rng >= 0:
+                        self.range_slot[(img, k, f)] = rng + i
+                jid = len(jobs)
+                jobs.append((img * self.p_image_stride + self.p_level_off[k], s_off,
+                             self.core_off[fl], H, W, self.pitch[k], fd.chan_off, fd.h, fd.w,
+                             fd.R, len(fl), _round_up(len(fl), 8), 0, rng, 0))
+                tw, th = self._tile_shape(fd.h, len(fl))
+                cls = classes.setdefault((fd.h, len(fl)), {"tiles": [], "w_max": 1, "R": 1})
+                cls["w_max"] = max(cls["w_max"], fd.w)
+                cls["R"] = max(cls["R"], fd.R)
+                for ty in range((ho + th - 1) // th):
+                    for tx in range((wo + tw - 1) // tw):
+                        cls["tiles"].append((jid, ty, tx, 0))
+        self.s_size = max(sa.size, 4)
+        self.n_ranges = nslots
+        self._corr_jobs = np.array(jobs, dtype=_lib.CORR_JOB) if jobs else np.zeros(0, _lib.CORR_JOB)
+        self._classes = []
+        for (h, nf), cls in sorted(classes.items()):
+            # tiles sorted by core so persistent CTAs keep it resident
+            tl = sorted(cls["tiles"], key=lambda t: (jobs[t[0]][2], t[0], t[1], t[2]))
+            self._classes.append((h, nf, cls["R"], cls["w_max"], np.array(tl, dtype=_lib.CORR_TILE)))
+
+        # K1 jobs
+        pj = [(img * self.x_image_stride + self.x_level_off[k],
+               img * self.p_image_stride + self.p_level_off[k], H, W, self.pitch[k], 0)
+              for img in range(nimg) for k, (H, W) in enumerate(self.levels)]
+        self._proj_jobs = np.array(pj, dtype=_lib.PROJ_JOB)
+        self._proj_blocks = _lib.check(lib.dpm_project_prepare(_lib.table_ptr(self._proj_jobs),
+                                                              len(self._proj_jobs)), "project")
+
+        # placement + assembly jobs
+        da = _Arena()
+        ta, oa, pla = _Arena(), _Arena(), _Arena()
+        place, asm_jobs = [], []
+        self.asm_index = {}  # (image, a) -> (total_off, pos_off, placed_off, hr, wr)
+        for img in range(nimg):
+            for ai, a in enumerate(self.assemblies):
+                ry0, ry1, rx0, rx1 = a.rect
+                hr, wr = ry1 - ry0 + 1, rx1 - rx0 + 1
+                if hr < 1 or wr < 1:
+                    raise ValidationError(f"assembly {ai}: empty root rectangle {a.rect}")
+                if len(a.parts) > _lib.MAX_PARTS:
+                    raise ValidationError(f"assembly {ai}: more than {_lib.MAX_PARTS} parts")
+                first = len(place)
+                for p in a.parts:
+                    hp, wp = self.map_shape[(p.level, p.filt)]
+                    dxo = da.take(hp * wr, align=8)
+                    rslot = self.range_slot.get((img, p.level, p.filt), -1)
+                    place.append((self.map_off[(img, p.level, p.filt)], dxo, hp, wp,
+                                  p.anchor[0], p.anchor[1], p.scale, p.radius, rx0, wr, rslot, 0,
+                                  *[float(v) for v in p.deformation]))
+                root_off, root_pitch = -1, 0
+                if a.root is not None:
+                    root_off = self.map_off[(img, a.root[0], a.root[1])]
+                    root_pitch = self.map_shape[tuple(a.root)][1]
+                    rh, rw = self.map_shape[tuple(a.root)]
+                    if not (0 <= ry0 and ry1 < rh and 0 <= rx0 and rx1 < rw):
+                        raise ValidationError(f"assembly {ai}: rect {a.rect} outside the root "
+                                              f"map {rh}x{rw}")
+                t_off = ta.take(hr * wr, align=4) if "totals" in self.outputs else -1
+                p_off = oa.take(len(a.parts) * hr * wr, align=4) if "positions" in self.outputs else -1
+                pl_off = pla.take(len(a.parts) * hr * wr, align=4) if "placed" in self.outputs else -1
+                self.asm_index[(img, ai)] = (t_off, p_off, pl_off, hr, wr)
+                asm_jobs.append((root_off, t_off, p_off, pl_off, root_pitch, ry0, ry1, rx0, rx1,
+                                 first, len(a.parts), img, a.level_tag, a.component, 0, 0,
+                                 float(a.bias)))
+        self._place_jobs = np.array(place, dtype=_lib.PLACE_JOB) if place else np.zeros(0, _lib.PLACE_JOB)
+        self._asm_jobs = np.array(asm_jobs, dtype=_lib.ASM_JOB) if asm_jobs else np.zeros(0, _lib.ASM_JOB)
+        self._place_blocks = _lib.check(lib.dpm_place_prepare(_lib.table_ptr(self._place_jobs),
+                                                             len(self._place_jobs)), "placement")
+        self._asm_blocks = _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(self._asm_jobs),
+                                                              len(self._asm_jobs)), "assembly")
+        self.dx_size = max(da.size, 8)
+        self.total_size, self.pos_size, self.placed_size = ta.size, oa.size, pla.size
+
+    _tile_cache = {}
+
+    def _tile_shape(self, h, nf):
+        import ctypes
+
+        if (h, nf) not in self._tile_cache:
+            tw, th = ctypes.c_int(0), ctypes.c_int(0)
+            _lib.lib().dpm_correlate_tile_shape(h, nf, ctypes.byref(tw), ctypes.byref(th))
+            self._tile_cache[(h, nf)] = (tw.value, th.value)
+        return self._tile_cache[(h, nf)]
+
+    # ------------------------------------------------------------ buffers
+    def _upload(self, C):
+        t = self.torch
+        dev = self.device
+        self.C = t.from_numpy(C).to(dev)
+        self.G = t.from_numpy(self._core_host).to(dev)
+        self.proj_jobs_d = upload_table(self._proj_jobs, dev)
+        self.corr_jobs_d = upload_table(self._corr_jobs, dev)
+        self.class_tiles_d = [upload_table(c[4], dev) for c in self._classes]
+        self.place_jobs_d = upload_table(self._place_jobs, dev)
+        self.asm_jobs_d = upload_table(self._asm_jobs, dev)
+        self.X = t.empty(self.n_images * self.x_image_stride, dtype=t.float32, device=dev)
+        self.P = t.empty(self.n_images * self.p_image_stride, dtype=t.float32, device=dev)
+        self.S = t.empty(self.s_size, dtype=t.float32, device=dev)
+        self.DX = t.empty(self.dx_size, dtype=t.int16, device=dev)
+        self.ranges = t.empty(max(2 * self.n_ranges, 2), dtype=t.int32, device=dev)
+        self.totals = t.empty(max(self.total_size, 1), dtype=t.float64, device=dev)
+        self.positions = t.empty(max(self.pos_size, 1), dtype=t.int32, device=dev)
+        self.placed = t.empty(max(self.placed_size, 1), dtype=t.float64, device=dev)
+        if self.max_dets > 0:
+            self.dets = t.empty(self.max_dets * _lib.DETECTION.itemsize, dtype=t.uint8, device=dev)
+            self.det_count = t.zeros(1, dtype=t.int32, device=dev)
+        else:
+            self.dets = self.det_count = None
+
+    # ------------------------------------------------------------ inputs
+    def x_view(self, image, level):
+        H, W = self.levels[level]
+        off = image * self.x_image_stride + self.x_level_off[level]
+        return self.X[off:off + H * W * self.L].view(H, W, self.L)
+
+    def load_levels(self, image, levels):
+        """Copy one image's levels (numpy or torch, (H, W, L)) into the X arena."""
+        t = self.torch
+        for k, lv in enumerate(levels):
+            src = lv if isinstance(lv, t.Tensor) else t.from_numpy(np.ascontiguousarray(lv, dtype=np.float32))
+            self.x_view(image, k).copy_(src, non_blocking=True)
+
+    # ------------------------------------------------------------ execute
+    def run(self, tau=float("inf"), stream=None, stages=("project", "correlate", "place")):
+        """Issue K1..K4 on ``stream`` (default: torch's current stream)."""
+        lib = _lib.lib()
+        t = self.torch
+        s = stream_handle(stream)
+        ptr = lambda x: x.data_ptr()  # noqa: E731
+        if "project" in stages:
+            _lib.check(lib.dpm_project(ptr(self.X), ptr(self.P), ptr(self.C), self.L, self.Rtot,
+                                       ptr(self.proj_jobs_d), len(self._proj_jobs),
+                                       self._proj_blocks, s), "project")
+        if "correlate" in stages:
+            if self.n_ranges:
+                _lib.check(lib.dpm_ranges_init(ptr(self.ranges), self.n_ranges, s), "ranges")
+            rng = ptr(self.ranges) if self.n_ranges else None
+            for (h, nf, R, w_max, tiles), tiles_d in zip(self._classes, self.class_tiles_d):
+                _lib.check(lib.dpm_correlate(ptr(self.P), ptr(self.G), ptr(self.S),
+                                             ptr(self.corr_jobs_d), ptr(tiles_d), len(tiles), h,
+                                             nf, R, w_max, rng, s), "correlate")
+        if "place" in stages and len(self._asm_jobs):
+            rng = ptr(self.ranges) if self.n_ranges else None
+            if len(self._place_jobs):
+                _lib.check(lib.dpm_place_xpass(ptr(self.S), ptr(self.DX), ptr(self.place_jobs_d),
+                                               len(self._place_jobs), self._place_blocks, rng, s),
+                           "placement")
+            if self.det_count is not None:
+                with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
+                    self.det_count.zero_()
+            _lib.check(lib.dpm_assemble(
+                ptr(self.S), ptr(self.DX), ptr(self.place_jobs_d), ptr(self.asm_jobs_d),
+                len(self._asm_jobs), self._asm_blocks, rng,
+                ptr(self.totals) if self.total_size else None,
+                ptr(self.positions) if self.pos_size else None,
+                ptr(self.placed) if self.placed_size else None,
+                float(tau),
+                ptr(self.dets) if self.dets is not None else None, self.max_dets,
+                ptr(self.det_count) if self.det_count is not None else None, s), "assemble")
+        return self
+
+    # ------------------------------------------------------------ outputs
+    def map(self, image, level, filt):
+        ho, wo = self.map_shape[(level, filt)]
+        off = self.map_off[(image, level, filt)]
+        return self.S[off:off + ho * wo].view(ho, wo)
+
+    def assembly_outputs(self, image, a):
+        t_off, p_off, pl_off, hr, wr = self.asm_index[(image, a)]
+        n = len(self.assemblies[a].parts)
+        out = {}
+        if t_off >= 0:
+            out["totals"] = self.totals[t_off:t_off + hr * wr].view(hr, wr)
+        if p_off >= 0:
+            out["positions"] = self.positions[p_off:p_off + n * hr * wr].view(n, hr, wr)
+        if pl_off >= 0:
+            out["placed"] = self.placed[pl_off:pl_off + n * hr * wr].view(n, hr, wr)
+        return out
+
+    def detections(self):
+        """Copy the detection records to the host (structured numpy array)."""
+        if self.det_count is None:
+            return np.zeros(0, dtype=_lib.DETECTION)
+        n = int(self.det_count.item())
+        if n > self.max_dets:
+            raise ValidationError(f"{n} detections exceed the buffer of {self.max_dets}; "
+                                  "raise max_dets or tau")
+        raw = self.dets[: n * _lib.DETECTION.itemsize].cpu().numpy()
+        return raw.view(_lib.DETECTION).copy()
+
+    # ------------------------------------------------------------ accounting
+    def evals(self):
+        """cell x filter evaluations per image (BASELINE.md §3 unit of work)."""
+        return sum(self.map_shape[(k, f)][0] * self.map_shape[(k, f)][1]
+                   for k, fl in self.groups for f in fl)
+
+    def k2_flops(self):
+        """Algorithmic K2 FLOPs per image: 2*h*w*R per eval."""
+        tot = 0
+        for k, fl in self.groups:
+            for f in fl:
+                fd = self.filters[f]
+                ho, wo = self.map_shape[(k, f)]
+                tot += 2 * fd.h * fd.w * fd.R * ho * wo
+        return tot
+
+    def k1_bytes(self):
+        return sum(4 * (self.L + self.Rtot) * H * W for H, W in self.levels)
+
+
+def unpack_positions(packed):
+    """uint32 (int16 y << 16 | int16 x) -> (y, x) int arrays."""
+    p = np.asarray(packed).astype(np.uint32)
+    y = (p >> 16).astype(np.uint16).view(np.int16).astype(np.int64)
+    x = (p & 0xFFFF).astype(np.uint16).view(np.int16).astype(np.int64)
+    return y, x

@@ -1,0 +1,154 @@
+"""Batched pyramid scoring: the B200 path for BASELINE.json configs 2-5.
+
+A model bank (many components, each a root + parts, all filters sharing one
+rank-R basis from the reference's ``cp_als`` on the stacked filter tensor,
+SURVEY.md App. A.3) is scored over whole feature pyramids of many images in
+one plan: one K1 launch, one K2 launch per filter-shape class, one K3 and
+one K4 launch -- independent of the number of images, levels and filters.
+
+Root domain / placement:
+  * ``domain="gdt"``: roots whose every part centre ``scale*root + anchor``
+    lies in the part map; ``radius=-1`` is the unbounded generalised
+    distance transform (window of radius r* per map, proven equal);
+  * ``domain="reference"``: the reference's ``_hypothesis_rect`` with each
+    component's windowed ``search_radius`` (scale 1 only).
+"""
+
+import numpy as np
+
+from .engine import AssemblyDef, FilterDef, PartDef, Plan, unpack_positions
+from .errors import ValidationError
+from .geometry import gdt_root_rect, hypothesis_rect
+
+__all__ = ["PyramidScorer", "cores_from_stacked"]
+
+
+def cores_from_stacked(bank, G):
+    """Split the stacked (P, R) core matrix into per-filter (h, w, R) cores."""
+    G = np.asarray(G, dtype=np.float32)
+    out = []
+    for f, off in zip(bank.filters, bank.offsets()):
+        h, w = f.shape[:2]
+        out.append(np.ascontiguousarray(G[off:off + h * w].reshape(h, w, -1)))
+    if sum(c.shape[0] * c.shape[1] for c in out) != G.shape[0]:
+        raise ValidationError("core matrix rows do not match the bank's stacked filters")
+    return out
+
+
+class _PartGeom:
+    def __init__(self, dims, anchor, radius):
+        self.filter = np.empty(dims)
+        self.anchor = anchor
+        self.search_radius = radius
+
+
+class PyramidScorer:
+    """Device plan scoring ``n_images`` pyramids against a filter bank."""
+
+    def __init__(self, bank, C, G, pyramid, n_images=1, radius=-1, domain="gdt",
+                 outputs=("totals", "positions"), max_dets=0, components=None):
+        self.bank, self.pyramid = bank, pyramid
+        self.cores = cores_from_stacked(bank, G)
+        C = np.asarray(C, dtype=np.float32)
+        self.L = C.shape[0]
+        comps = list(bank.components) if components is None else list(components)
+        filters = [FilterDef(c) for c in self.cores]
+        asms = []
+        self.asm_keys = []  # (root level index, component index)
+        for i, (kr, kp) in enumerate(zip(pyramid.root_levels, pyramid.part_levels)):
+            Hr, Wr = pyramid.levels[kr]
+            Hp, Wp = pyramid.levels[kp]
+            for ci, comp in enumerate(comps):
+                rh, rw = bank.filters[comp.root].shape[:2]
+                if rh > Hr or rw > Wr:
+                    continue
+                pdims = [bank.filters[f].shape for f in comp.parts]
+                if any(d[0] > Hp or d[1] > Wp for d in pdims):
+                    continue
+                rad = comp.search_radius if radius is None else radius
+                if domain == "gdt":
+                    rect = gdt_root_rect((Hr - rh + 1, Wr - rw + 1),
+                                         [(Hp - d[0] + 1, Wp - d[1] + 1) for d in pdims],
+                                         comp.anchors, pyramid.scale)
+                elif domain == "reference":
+                    if pyramid.scale != 1 or kr != kp:
+                        raise ValidationError("the reference domain is single-resolution")
+                    rect = hypothesis_rect((Hr, Wr), (rh, rw),
+                                           [_PartGeom(d, a, rad) for d, a in zip(pdims, comp.anchors)])
+                else:
+                    raise ValidationError(f"unknown domain {domain!r}")
+                if rect is None:
+                    continue
+                parts = tuple(PartDef(kp, f, tuple(a), tuple(d), int(rad), pyramid.scale)
+                              for f, a, d in zip(comp.parts, comp.anchors, comp.deformations))
+                asms.append(AssemblyDef((kr, comp.root), rect, parts, comp.bias,
+                                        level_tag=i, component=ci))
+                self.asm_keys.append((i, ci))
+        self.plan = Plan(self.L, pyramid.levels, C, filters, assemblies=asms,
+                         n_images=n_images, outputs=outputs, max_dets=max_dets)
+        self.n_images = n_images
+
+    # inputs
+    def load_image(self, image, levels):
+        self.plan.load_levels(image, levels)
+
+    def host_arena(self, pinned=True):
+        """Host buffer laid out like the device X arena (pinned for async H2D)."""
+        t = self.plan.torch
+        return t.empty(self.plan.X.numel(), dtype=t.float32, pin_memory=pinned)
+
+    def fill_host(self, arena, image, levels):
+        plan = self.plan
+        for k, lv in enumerate(levels):
+            H, W = plan.levels[k]
+            off = image * plan.x_image_stride + plan.x_level_off[k]
+            arena[off:off + H * W * plan.L].numpy()[:] = np.asarray(lv, np.float32).ravel()
+
+    def h2d_bytes(self):
+        """Feature bytes one batch moves host -> device (excluding arena padding)."""
+        return 4 * self.plan.L * self.n_images * sum(h * w for h, w in self.plan.levels)
+
+    def score_batch(self, host_arena, tau, stream=None):
+        """Public end-to-end call: host pyramids (arena layout) in, detections
+        (structured numpy array, DETECTION records with score >= tau) out."""
+        t = self.plan.torch
+        s = t.cuda.current_stream() if stream is None else stream
+        with t.cuda.stream(s):
+            self.plan.X.copy_(host_arena, non_blocking=True)
+            self.plan.run(tau=tau, stream=s)
+            return self.plan.detections()
+
+    @property
+    def X(self):
+        return self.plan.X
+
+    # execution
+    def run(self, tau=float("inf"), stream=None, stages=("project", "correlate", "place")):
+        self.plan.run(tau=tau, stream=stream, stages=stages)
+        return self
+
+    # outputs
+    def results(self, image=0):
+        """[{root_level, component, rect, scores (float64), parts (n, hr, wr, 2)}]"""
+        out = []
+        for ai, (i, ci) in enumerate(self.asm_keys):
+            o = self.plan.assembly_outputs(image, ai)
+            a = self.plan.assemblies[ai]
+            rec = {"root_level": i, "component": ci, "rect": a.rect}
+            if "totals" in o:
+                rec["scores"] = o["totals"].cpu().numpy()
+            if "positions" in o:
+                py, px = unpack_positions(o["positions"].cpu().numpy())
+                rec["parts"] = np.stack([py, px], axis=-1)
+            out.append(rec)
+        return out
+
+    def detections(self):
+        return self.plan.detections()
+
+    # accounting
+    def evals_per_image(self):
+        return self.plan.evals()
+
+    def k2_flops_per_image(self):
+        return self.plan.k2_flops()

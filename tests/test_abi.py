@@ -1,0 +1,94 @@
+"""C ABI: the library loads without a GPU and exports every declared symbol;
+ABI struct layouts match the header; host-side prepare calls validate."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+
+from paper_1707_03268_b200 import _lib
+
+
+def _declared():
+    text = open(os.path.join(REPO, "include", "dpm_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(dpm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    names = _declared()
+    assert len(names) >= 13
+    for n in names:
+        assert hasattr(lib, n), n
+    assert lib.dpm_abi_version() == 1
+
+
+def test_struct_sizes_match_header_comments():
+    # sizes asserted at import against the C layout (int64 first, natural alignment)
+    assert _lib.PROJ_JOB.itemsize == 32
+    assert _lib.CORR_JOB.itemsize == 72
+    assert _lib.PLACE_JOB.itemsize == 88
+    assert _lib.ASM_JOB.itemsize == 88
+    assert _lib.DETECTION.itemsize == 96
+
+
+def test_struct_layout_against_compiled_offsets(tmp_path):
+    """Compile a tiny C program against the header and compare offsetof()."""
+    src = tmp_path / "off.c"
+    fields = {
+        "dpm_proj_job": ("x_off", "p_off", "H", "W", "pitch", "block0"),
+        "dpm_corr_job": ("p_off", "s_off", "g_off", "H", "nf_pad", "range_idx"),
+        "dpm_place_job": ("s_off", "dx_off", "Hp", "block0", "cdx", "cdyy"),
+        "dpm_asm_job": ("root_off", "placed_off", "root_pitch", "block0", "bias"),
+        "dpm_detection": ("image", "score", "parts"),
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dpm_b200.h"', "int main(){"]
+    for st, fs in fields.items():
+        lines.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f in fs:
+            lines.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    lines.append("return 0;}")
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "off"
+    rc = os.system(f"gcc -I{REPO}/include {src} -o {exe}")
+    if rc != 0:
+        pytest.skip("gcc unavailable")
+    out = dict(line.rsplit(" ", 1) for line in os.popen(str(exe)).read().split("\n") if line)
+    dts = {"dpm_proj_job": _lib.PROJ_JOB, "dpm_corr_job": _lib.CORR_JOB,
+           "dpm_place_job": _lib.PLACE_JOB, "dpm_asm_job": _lib.ASM_JOB,
+           "dpm_detection": _lib.DETECTION}
+    for st, fs in fields.items():
+        assert int(out[st]) == dts[st].itemsize, st
+        for f in fs:
+            assert int(out[f"{st}.{f}"]) == dts[st].fields[f][1], (st, f)
+
+
+def test_prepare_validates_and_numbers_blocks():
+    lib = _lib.lib()
+    jobs = np.zeros(2, dtype=_lib.PROJ_JOB)
+    jobs["H"], jobs["W"], jobs["pitch"] = (10, 20), (30, 7), (32, 8)
+    n = lib.dpm_project_prepare(_lib.table_ptr(jobs), 2)
+    assert n == 2 + 1 and list(jobs["block0"]) == [0, 2]
+    jobs["pitch"][1] = 6  # not a multiple of 4
+    with pytest.raises(Exception, match="pitch"):
+        _lib.check(lib.dpm_project_prepare(_lib.table_ptr(jobs), 2))
+    pj = np.zeros(1, dtype=_lib.PLACE_JOB)
+    pj["Hp"], pj["Wp"], pj["wr"], pj["scale"], pj["radius"], pj["range_idx"] = 5, 5, 3, 1, -1, 0
+    with pytest.raises(Exception, match="c_dxx"):
+        _lib.check(lib.dpm_place_prepare(_lib.table_ptr(pj), 1))
+
+
+def test_tile_shapes():
+    lib = _lib.lib()
+    tw, th = ctypes.c_int(), ctypes.c_int()
+    assert lib.dpm_correlate_tile_shape(6, 48, ctypes.byref(tw), ctypes.byref(th)) == 6
+    assert (tw.value, th.value) == (32, 8)
+    assert lib.dpm_correlate_tile_shape(6, 6, ctypes.byref(tw), ctypes.byref(th)) == 4
+    assert th.value == 32
+    assert lib.dpm_correlate_tile_shape(9, 2, ctypes.byref(tw), ctypes.byref(th)) < 0
+    assert th.value == 8  # generic kernel tile

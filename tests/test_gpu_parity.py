@@ -1,0 +1,382 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the reference's golden vectors.  Run on a B200 with ``pytest -m gpu``."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cp, load_golden
+from oracle import dpm_oracle as O
+from parity import assert_map_close, classify_positions, penalised
+
+pytestmark = pytest.mark.gpu
+
+B = pytest.importorskip("paper_1707_03268_b200")
+from paper_1707_03268_b200 import synth  # noqa: E402
+from paper_1707_03268_b200.pipeline import PyramidScorer  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+# ------------------------------------------------------------------ K1 + K2
+
+def test_correlate3_full_matches_reference_golden():
+    g = load_golden("correlation.npz")
+    for k in range(int(g["n_full"])):
+        img, filt = g[f"full{k}_img"], g[f"full{k}_filt"]
+        sm = B.correlate3_full(img, filt)
+        assert_map_close(sm.scores, g[f"full{k}_out"], f"full{k}")
+        assert sm.multiplications == int(g[f"full{k}_mult"])
+        # same fp32-rounded inputs through the oracle: tighter still
+        assert_map_close(sm.scores, O.correlate3_full(f32(img), f32(filt)), f"full{k} f32", 2e-6)
+
+
+def test_cp_engines_match_reference_golden_and_prefix_identity():
+    g = load_golden("correlation.npz")
+    for k in range(int(g["n_cp"])):
+        cp, img = golden_cp(g, f"cp{k}"), g[f"cp{k}_img"]
+        stack = B.cp_partial_stack(img, cp)
+        ref = g[f"cp{k}_stack"]
+        assert stack.shape == ref.shape
+        for r in range(ref.shape[0]):
+            assert_map_close(stack[r], ref[r], f"cp{k} rank {r}")
+        up = int(g[f"cp{k}_upto"])
+        sm = B.correlate3_cp(img, cp, upto_rank=up)
+        assert_map_close(sm.scores, g[f"cp{k}_upto_out"], f"cp{k} upto")
+        assert sm.multiplications == int(g[f"cp{k}_upto_mult"])
+        # reference property (test_correlation.py:158-178): prefixes are bit-identical
+        for r in range(1, cp.rank + 1):
+            assert np.array_equal(B.correlate3_cp(img, cp, upto_rank=r).scores, stack[r - 1])
+
+
+def test_cp_engine_edge_shapes_generic_and_chunked_kernels():
+    rng = np.random.default_rng(77)
+    # (img shape, dims, rank): filter == image (1x1 output), h not specialised,
+    # R > 8 (rank chunking), odd channel counts
+    for ishape, dims, rank in [((6, 11, 32), (6, 11, 32), 8), ((9, 30, 5), (1, 13, 5), 3),
+                               ((17, 19, 32), (9, 4, 32), 12), ((40, 70, 32), (15, 15, 32), 32),
+                               ((33, 65, 7), (6, 6, 7), 20), ((12, 12, 3), (12, 1, 3), 2)]:
+        img = rng.normal(size=ishape).astype(np.float32).astype(np.float64)
+        cp = B.CPModel.from_factors(rng.normal(size=(dims[0], rank)),
+                                    rng.normal(size=(dims[1], rank)),
+                                    rng.normal(size=(dims[2], rank)))
+        ref = O.cp_partial_stack(img, cp)[-1]
+        assert_map_close(B.correlate3_cp(img, cp).scores, ref, f"{ishape}/{dims}/{rank}")
+
+
+def test_dense_many_filters_group_split():
+    """More than 48 same-shape filters on one level: K2 splits the group."""
+    rng = np.random.default_rng(5)
+    level = rng.random((40, 52, 32)).astype(np.float32)
+    cores = [rng.normal(0, 0.05, (6, 6, 8)).astype(np.float32) for _ in range(60)]
+    C = rng.normal(size=(32, 8)).astype(np.float32)
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    plan = Plan(32, [(40, 52)], C, [FilterDef(c) for c in cores], apps=[(0, f) for f in range(60)],
+                outputs=())
+    plan.load_levels(0, [level])
+    plan.run(stages=("project", "correlate"))
+    P = O.project(level, C.astype(np.float64))
+    for f in (0, 47, 48, 59):
+        assert_map_close(plan.map(0, 0, f).double().cpu().numpy(), O.correlate3_full(P, cores[f]),
+                         f"filter {f}")
+
+
+# ----------------------------------------------------------------- K3 + K4
+
+def test_placement_grid_bit_exact_on_fp32_maps_and_golden():
+    g = load_golden("placement.npz")
+    for k in range(int(g["n"])):
+        smap = g[f"p{k}_map"]
+        anc, de, r = tuple(g[f"p{k}_anchor"]), tuple(g[f"p{k}_def"]), int(g[f"p{k}_r"])
+        rect = tuple(int(v) for v in g[f"p{k}_rect"])
+        part = B.PartSpec(np.zeros((1, 1, 1)), anc, de, r)
+        placed, py, px = B._placement_grid(smap, part, rect)
+        # kernel-isolated: identical to the oracle on the same fp32 map
+        o_placed, o_py, o_px = O.placement_grid(f32(smap), anc, de, r, rect)
+        assert np.array_equal(placed, o_placed), k
+        assert np.array_equal(py, o_py) and np.array_equal(px, o_px), k
+        # vs the reference on its float64 map: values to tolerance, argmax to ties
+        ref = g[f"p{k}_placed"]
+        fin = np.isfinite(ref)
+        assert np.array_equal(fin, np.isfinite(placed))
+        assert_map_close(placed[fin], ref[fin], f"placement {k}")
+        S = smap
+        cy = np.arange(rect[0], rect[1] + 1)[:, None] + anc[0] + 0 * px
+        cx = np.arange(rect[2], rect[3] + 1)[None, :] + anc[1] + 0 * py
+        gp = np.stack([py, px], -1).reshape(-1, 2)
+        rp = np.stack([g[f"p{k}_py"], g[f"p{k}_px"]], -1).reshape(-1, 2)
+        cent = np.stack([cy, cx], -1).reshape(-1, 2)
+        _, _, err = classify_positions(gp, rp, lambda i, p: penalised(S, cent[i], p, de),
+                                       ref.reshape(-1), np.abs(S).max())
+        assert err == 0, k
+
+
+def test_best_part_placement_known_answers():
+    part = B.PartSpec(np.zeros((2, 2, 3)), (0, 0), (0.0, 0.0, 0.0, 0.0), 1)
+    assert B.best_part_placement(part, np.zeros((5, 5)), (2, 2)) == ((1, 1), 0.0)
+    rng = np.random.default_rng(7)
+    s = rng.normal(size=(9, 9)).astype(np.float32).astype(np.float64)
+    big = B.PartSpec(np.zeros((2, 2, 3)), (0, 0), (0.0, 0.0, 1e9, 1e9), 3)
+    assert B.best_part_placement(big, s, (4, 4))[0] == (4, 4)
+    zero = B.PartSpec(np.zeros((2, 2, 3)), (0, 0), (0.0, 0.0, 0.0, 0.0), 2)
+    pos, val = B.best_part_placement(zero, s, (4, 4))
+    assert val == s[2:7, 2:7].max() and s[pos] == val
+    far = B.PartSpec(np.zeros((2, 2, 3)), (10, 10), (0.0, 0.0, 0.0, 0.0), 1)
+    with pytest.raises(B.ValidationError, match="empty"):
+        B.best_part_placement(far, np.zeros((5, 5)), (0, 0))
+
+
+def _compact(g, k):
+    pre = f"d{k}"
+    levels = [g[f"{pre}_level{i}"] for i in range(int(g[f"{pre}_nlevels"]))]
+    parts, dparts = [], []
+    for i in range(int(g[f"{pre}_nparts"])):
+        anc = tuple(int(v) for v in g[f"{pre}_part{i}_anchor"])
+        de = tuple(float(v) for v in g[f"{pre}_part{i}_def"])
+        r = int(g[f"{pre}_part{i}_r"])
+        parts.append(B.PartSpec(g[f"{pre}_part{i}"], anc, de, r))
+        dparts.append(B.DecomposedPart(golden_cp(g, f"{pre}_pcp{i}"), anc, de, r))
+    model = B.PartModel(g[f"{pre}_root"], tuple(parts), float(g[f"{pre}_bias"]))
+    dec = B.DecomposedModel(golden_cp(g, f"{pre}_rcp"), tuple(dparts), float(g[f"{pre}_bias"]))
+    return levels, model, dec
+
+
+def _pack(dets):
+    return np.array([[d.hypothesis.level, *d.hypothesis.root,
+                      *[c for pp in d.hypothesis.parts for c in pp], d.score] for d in dets])
+
+
+def _check_dets(got, ref, levels, part_defs, part_maps_fn, what):
+    """Roots identical, scores to 1e-5 of max |score|, part argmaxes up to ties."""
+    assert got.shape == ref.shape, what
+    assert np.array_equal(got[:, :3], ref[:, :3]), what
+    assert_map_close(got[:, -1], ref[:, -1], what)
+    npart = (got.shape[1] - 4) // 2
+    for p in range(npart):
+        gp, rp = got[:, 3 + 2 * p:5 + 2 * p], ref[:, 3 + 2 * p:5 + 2 * p]
+        bad = np.nonzero(np.any(gp != rp, axis=1))[0]
+        errs = 0
+        for i in bad:
+            lvl = int(ref[i, 0])
+            S = part_maps_fn(lvl, p)
+            anc, de = part_defs[p]
+            cent = (int(ref[i, 1]) + anc[0], int(ref[i, 2]) + anc[1])
+            vg = penalised(S, cent, tuple(int(v) for v in gp[i]), de)
+            vr = penalised(S, cent, tuple(int(v) for v in rp[i]), de)
+            if vr - vg > 1e-5 * np.abs(S).max():
+                errs += 1
+        assert errs == 0, f"{what}: part {p} has {errs} argmax errors"
+
+
+def test_detect_and_dense_detect_match_reference_golden():
+    g = load_golden("detect_compact.npz")
+    for k in range(int(g["n"])):
+        levels, model, dec = _compact(g, k)
+        pdefs = [(p.anchor, p.deformation) for p in model.parts]
+        dets, stats = B.detect(dec, levels, -np.inf)
+        _check_dets(_pack(dets), g[f"d{k}_dets"], levels, pdefs,
+                    lambda lvl, p: O.cp_partial_stack(levels[lvl], dec.parts[p].cp)[-1],
+                    f"detect {k}")
+        assert [stats.positions_examined, stats.multiplications] == list(g[f"d{k}_stats"])
+        ddets, dstats = B.dense_detect(model, levels, -np.inf)
+        _check_dets(_pack(ddets), g[f"d{k}_ddets"], levels, pdefs,
+                    lambda lvl, p: O.correlate3_full(levels[lvl], model.parts[p].filter),
+                    f"dense_detect {k}")
+        assert [dstats.positions_examined, dstats.multiplications] == list(g[f"d{k}_dstats"])
+        # threshold: only scores >= tau, same sorted order
+        tau = float(np.median(g[f"d{k}_dets"][:, -1]))
+        some, _ = B.detect(dec, levels, tau)
+        assert all(d.score >= tau for d in some)
+        assert len(some) >= 1
+        h = g[f"d{k}_hyp"]
+        hyp = B.Hypothesis(int(h[0]), (int(h[1]), int(h[2])),
+                           tuple((int(h[3 + 2 * i]), int(h[4 + 2 * i]))
+                                 for i in range(len(model.parts))))
+        lv = levels[hyp.level]
+        assert B.score_hypothesis(model, lv, hyp) == pytest.approx(float(g[f"d{k}_score_hyp"]),
+                                                                   rel=1e-5, abs=1e-5)
+        assert B.cp_score_hypothesis(dec, lv, hyp) == pytest.approx(
+            float(g[f"d{k}_cp_score_hyp"]), rel=1e-5, abs=1e-5)
+
+
+def test_config1_reference_native_detect():
+    """Config 1: 64x48x32 level, root 6x11 + 8 parts 6x6, per-filter CP R=8."""
+    g = load_golden("cfg1.npz")
+    wl = synth.workload(1)
+    comp = wl.bank.components[0]
+    level = synth.hog_level(1, 0, 0, 64, 48).astype(np.float64)
+    parts = tuple(B.DecomposedPart(golden_cp(g, f"part{i}"), a, d, 2)
+                  for i, (a, d) in enumerate(zip(comp.anchors, comp.deformations)))
+    dec = B.DecomposedModel(golden_cp(g, "root"), parts, comp.bias)
+    dets, stats = B.detect(dec, [level], -np.inf)
+    got = _pack(dets)
+    ref = np.concatenate([np.zeros((len(g["dets"]), 1)), g["dets"]], axis=1)
+    pdefs = [(p.anchor, p.deformation) for p in parts]
+    _check_dets(got, ref, [level], pdefs,
+                lambda lvl, p: O.cp_partial_stack(level, parts[p].cp)[-1], "config 1")
+    assert [stats.positions_examined, stats.multiplications] == list(g["stats"])
+    assert_map_close(B.correlate3_cp(level, dec.root_cp).scores, g["root_map"], "cfg1 root map")
+
+
+def test_config1_shared_basis_pyramid_scorer_reference_domain():
+    g = load_golden("cfg1.npz")
+    wl = synth.workload(1)
+    level = synth.hog_level(1, 0, 0, 64, 48)
+    sc = PyramidScorer(wl.bank, g["shared_C"], g["shared_G"], wl.pyramid, radius=None,
+                       domain="reference")
+    sc.load_image(0, [level])
+    sc.run()
+    (res,) = sc.results(0)
+    ry0, ry1, rx0, rx1 = res["rect"]
+    ref = g["shared_dets"]
+    ref_scores = ref[:, -1].reshape(ry1 - ry0 + 1, rx1 - rx0 + 1)
+    assert_map_close(res["scores"], ref_scores, "cfg1 shared totals")
+    ref_parts = ref[:, 2:-1].reshape(ry1 - ry0 + 1, rx1 - rx0 + 1, -1, 2).transpose(2, 0, 1, 3)
+    mismatch = np.any(res["parts"] != ref_parts, axis=-1)
+    assert mismatch.mean() < 1e-3
+
+
+# --------------------------------------------------- batched pyramids (configs)
+
+def _shared(cfg, R):
+    import os
+
+    from conftest import REPO
+    fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg{cfg}_R{R}.npz"))
+    return fx["C"], fx["G"]
+
+
+def _pyramid_parity(cfg, R, sel_levels=None, comps=None, images=(0,), n_images=1):
+    wl = synth.workload(cfg)
+    C, G = _shared(cfg, R)
+    bank, pyr = wl.bank, wl.pyramid
+    comp_list = list(bank.components) if comps is None else [bank.components[c] for c in comps]
+    sc = PyramidScorer(bank, C, G, pyr, n_images=n_images, components=comp_list)
+    levels = {}
+    for img in range(n_images):
+        lv = synth.hog_pyramid(cfg, img, pyr)
+        levels[img] = lv
+        sc.load_image(img, lv)
+    sc.run()
+    cores = sc.cores
+    worst = 0.0
+    for img in images:
+        res = sc.results(img)
+        if sel_levels is not None:
+            res = [r for r in res if r["root_level"] in sel_levels]
+        for rec in res:
+            i, ci = rec["root_level"], rec["component"]
+            kr, kp = pyr.root_levels[i], pyr.part_levels[i]
+            comp = comp_list[ci]
+            lvls = [np.zeros((1, 1, 32), np.float32)] * len(pyr.levels)
+            lvls = list(lvls)
+            lvls[kr], lvls[kp] = levels[img][kr], levels[img][kp]
+            oref, maps = O.score_pyramid(lvls, bank, C, cores, root_levels=[kr],
+                                         part_levels=[kp], components=[comp])
+            (o,) = oref
+            assert tuple(o["rect"]) == tuple(rec["rect"])
+            worst = max(worst, assert_map_close(rec["scores"], o["scores"], f"cfg{cfg} {i}/{ci}"))
+            # response maps (all filters of this component) to 1e-5
+            gpu_maps = {}
+            for f in (comp.root,) + tuple(comp.parts):
+                k = kr if f == comp.root else kp
+                gm = sc.plan.map(img, k, f).double().cpu().numpy()
+                assert_map_close(gm, maps[(k, f)], f"cfg{cfg} map {k}/{f}")
+                gpu_maps[f] = gm
+            # argmaxes: kernel-isolated bit-exactness on the GPU's own maps ...
+            for p, (f, anc, de) in enumerate(zip(comp.parts, comp.anchors, comp.deformations)):
+                gm = gpu_maps[f]
+                r = O.r_star(gm, de)
+                v, py, px = O.place_gathered(gm, anc, de, r, pyr.scale, rec["rect"])
+                assert np.array_equal(rec["parts"][p, ..., 0], py)
+                assert np.array_equal(rec["parts"][p, ..., 1], px)
+            # ... and against the fp64 oracle up to ties
+            ry0, ry1, rx0, rx1 = rec["rect"]
+            for p, (f, anc, de) in enumerate(zip(comp.parts, comp.anchors, comp.deformations)):
+                S = maps[(kp, f)]
+                cy = pyr.scale * np.arange(ry0, ry1 + 1)[:, None] + anc[0]
+                cx = pyr.scale * np.arange(rx0, rx1 + 1)[None, :] + anc[1]
+                cent = np.stack(np.broadcast_arrays(cy, cx), -1).reshape(-1, 2)
+                best = np.array([penalised(S, cent[q], tuple(o["parts"][p].reshape(-1, 2)[q]), de)
+                                 for q in range(cent.shape[0])])
+                _, _, err = classify_positions(rec["parts"][p], o["parts"][p],
+                                               lambda q, pos: penalised(S, cent[q], pos, de),
+                                               best, np.abs(S).max())
+                assert err == 0
+    return worst
+
+
+def test_config2_sample_matches_reference_golden():
+    g = load_golden("cfg2_sample.npz")
+    wl = synth.workload(2)
+    C, G = _shared(2, 8)
+    sc = PyramidScorer(wl.bank, C, G, wl.pyramid)
+    sc.load_image(0, synth.hog_pyramid(2, 0, wl.pyramid))
+    sc.run()
+    res = {(r["root_level"], r["component"]): r for r in sc.results(0)}
+    for k in range(int(g["n"])):
+        i, ci = (int(v) for v in g[f"s{k}_sel"])
+        rec = res[(i, ci)]
+        assert tuple(rec["rect"]) == tuple(int(v) for v in g[f"s{k}_rect"])
+        assert_map_close(rec["scores"], g[f"s{k}_scores"], f"cfg2 golden {k}")
+        mism = np.any(rec["parts"] != g[f"s{k}_parts"], axis=-1)
+        assert mism.mean() < 1e-3
+
+
+@pytest.mark.parametrize("R", [4, 8, 16, 32])
+def test_config2_full_pyramid_rank_sweep(R):
+    _pyramid_parity(2, R, sel_levels=None if R == 8 else {0, 5, 14, 28})
+
+
+def test_config3_sampled_models():
+    _pyramid_parity(3, 16, sel_levels={0, 21, 41}, comps=[0, 1, 17, 59, 60, 119])
+
+
+def test_config4_batch_consistency_and_sample():
+    """Image 2 of a 3-image batch equals the oracle on sampled levels, and
+    batching does not change any bit of any image's results."""
+    _pyramid_parity(4, 8, sel_levels={0, 20, 38}, comps=[0, 3], images=(2,), n_images=3)
+    wl = synth.workload(4)
+    C, G = _shared(4, 8)
+    one = PyramidScorer(wl.bank, C, G, wl.pyramid, n_images=1)
+    one.load_image(0, synth.hog_pyramid(4, 2, wl.pyramid))
+    one.run()
+    three = PyramidScorer(wl.bank, C, G, wl.pyramid, n_images=3)
+    for img in range(3):
+        three.load_image(img, synth.hog_pyramid(4, img, wl.pyramid))
+    three.run()
+    for a, b in zip(one.results(0), three.results(2)):
+        assert np.array_equal(a["scores"], b["scores"])
+        assert np.array_equal(a["parts"], b["parts"])
+
+
+@pytest.mark.parametrize("R", [8, 32])
+def test_config5_large_roots_sample(R):
+    _pyramid_parity(5, R, sel_levels={0, 19, 36})
+
+
+def test_tau_compaction_matches_totals():
+    wl = synth.workload(2)
+    C, G = _shared(2, 8)
+    sc = PyramidScorer(wl.bank, C, G, wl.pyramid, max_dets=200000)
+    sc.load_image(0, synth.hog_pyramid(2, 0, wl.pyramid))
+    allsc = np.concatenate([r["scores"].ravel() for r in sc.run().results(0)])
+    tau = float(np.quantile(allsc, 0.99))
+    sc.run(tau=tau)
+    dets = sc.detections()
+    assert len(dets) == int((allsc >= tau).sum())
+    res = {(r["root_level"], r["component"]): r for r in sc.results(0)}
+    for d in dets[:500]:
+        rec = res[(int(d["level"]), int(d["component"]))]
+        ry0, _, rx0, _ = rec["rect"]
+        assert d["score"] == rec["scores"][d["ry"] - ry0, d["rx"] - rx0]
