@@ -113,33 +113,35 @@ int dpm_correlate(const float* P, const float* G, float* S, const dpm_corr_job* 
 /* Initialise `n` range slots to (-inf, +inf). */
 int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
 
-/* ---------------------------------------- K3: part placement (FP64)
- * Penalised max over a window around centre = scale*root + anchor,
- * separable: x pass then y pass, strict '>' in ascending offset order
- * (ties -> smallest (dy, dx)), penalty subtracted in two stages exactly as
- * _placement_grid (detection.py:320-373).  radius >= 0: reference windowed
- * semantics; radius < 0: unbounded generalised distance transform, realised
- * as the window of radius r* computed from the map's range (SURVEY.md
- * App. A.2 lemma; requires c_dxx, c_dyy > 0). */
+/* ------------------------------- K3 + K4: part placement + assembly
+ * For every root (ry, rx) of an assembly's rectangle:
+ *   placed_i = max over a window around centre (scale*ry + ay_i, scale*rx + ax_i)
+ *              of S_i - penalty, separable: x pass then y pass, strict '>'
+ *              in ascending offset order (ties -> smallest (dy, dx)), the
+ *              penalty subtracted in two stages exactly as _placement_grid
+ *              (detection.py:320-373), in FP64 on the FP32 map;
+ *   total    = S_root[ry][rx] + sum_i placed_i + bias
+ *              (detection.py:449, 509-519; dense_detect 590-598).
+ * radius >= 0: the reference's windowed semantics.  radius < 0: unbounded
+ * generalised distance transform, realised as the window of radius r*
+ * computed from the map's range (SURVEY.md App. A.2 lemma; requires
+ * c_dxx, c_dyy > 0).  Every placed map needs a range slot (filled by
+ * dpm_correlate): it bounds the FP32 screening error and gives r*. */
 typedef struct {
   int64_t s_off;     /* float offset of the part response map [Hp][Wp]       */
-  int64_t dx_off;    /* int16 offset of the x-pass argmax table [Hp][wr]     */
   int32_t Hp, Wp;
   int32_t ay, ax;
   int32_t scale;
   int32_t radius;    /* >= 0 windowed, < 0 GDT via r*                        */
-  int32_t rx0, wr;   /* root columns handled (centres scale*rx + ax)         */
-  int32_t range_idx; /* range slot of the map (GDT mode)                     */
-  int32_t block0;    /* first CTA of the x pass; set by dpm_place_prepare    */
+  int32_t range_idx; /* range slot of the map                                */
+  int32_t pad;
   double cdx, cdy, cdxx, cdyy;
 } dpm_place_job;
 
-/* ------------------------------------------ K4: root + parts assembly
- * total[ry][rx] = S_root[ry][rx] + sum_i placed_i(ry, rx) + bias
- * (detection.py:449, 509-519), with the y pass of every part fused in.
- * Optional outputs: totals (double), packed part positions (uint32
- * y << 16 | x), per-part placed values (double), and detections with
- * total >= tau appended to `dets` (count in *det_count). */
+/* Optional outputs: totals (double), packed part positions (uint32
+ * (int16 y) << 16 | (uint16)(int16 x)), per-part placed values (double), and
+ * detections with total >= tau appended to `dets` (count in *det_count,
+ * which the caller zeroes; records beyond max_dets are dropped but counted). */
 typedef struct {
   int64_t root_off;   /* float offset of the root map, < 0: no root term      */
   int64_t total_off;  /* double offset of totals [hr][wr], < 0: not written   */
@@ -158,22 +160,18 @@ typedef struct {
 typedef struct {
   int32_t image, level, component, ry, rx, nparts;
   double score;
-  uint32_t parts[DPM_MAX_PARTS]; /* y << 16 | x */
+  uint32_t parts[DPM_MAX_PARTS]; /* (int16 y) << 16 | (uint16)(int16 x) */
 } dpm_detection;
 
-int64_t dpm_place_prepare(dpm_place_job* jobs_host, int njobs);
-int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs);
+/* Validates both tables (host memory), fills block0 of the assembly jobs and
+ * returns the CTA count to pass to dpm_assemble. */
+int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs, const dpm_place_job* pjobs_host,
+                             int npjobs);
 
-/* x pass of every placement job (writes the int16 argmax tables). */
-int dpm_place_xpass(const float* S, int16_t* dx, const dpm_place_job* jobs, int njobs,
-                    int64_t nblocks, const uint32_t* ranges, void* stream);
-
-/* y pass + assembly. */
-int dpm_assemble(const float* S, const int16_t* dx, const dpm_place_job* pjobs,
-                 const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
-                 const uint32_t* ranges, double* total, uint32_t* pos, double* placed,
-                 double tau, dpm_detection* dets, int max_dets, int* det_count,
-                 void* stream);
+int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
+                 int najobs, int64_t nblocks, const uint32_t* ranges, double* total,
+                 uint32_t* pos, double* placed, double tau, dpm_detection* dets, int max_dets,
+                 int* det_count, void* stream);
 
 /* ----------------------------------------------------- micro-benchmark
  * FP32 FFMA peak probe used by bench.py for the K2 roofline denominator:

@@ -1,230 +1,353 @@
-// K3 (part placement) and K4 (root + parts assembly), FP64 arithmetic on
-// FP32 response maps.
+// K3 (part placement) fused with K4 (root + parts assembly).
 //
 // Reference: _placement_grid (detection.py:320-373), best_part_placement
-// (detection.py:180-207) and the assembly lines of detect / dense_detect
+// (detection.py:180-207) and the assembly of detect / dense_detect
 // (detection.py:449, 509-538; 590-613).
 //
-// Semantics reproduced exactly (bit-identical values and argmaxes for the
-// same input map, checked against the oracle):
-//   x pass: for every map row y and centre column cx = scale*rx + ax,
+// Exact semantics (bit-identical values and argmaxes for a given FP32 map):
+//   x pass: for every needed map row y and centre cx = scale*rx + ax,
 //           best over dx = -r..r (ascending, strict '>') of
 //           S[y][cx+dx] - (c_dx*dx + (c_dxx*dx)*dx), -inf outside the map;
 //   y pass: best over dy = -r..r (ascending, strict '>') of
-//           xbest[cy+dy] - (c_dy*dy + (c_dyy*dy)*dy), cy = scale*ry + ay.
-// All penalty products/sums use round-to-nearest intrinsics so the compiler
-// cannot contract them into FMAs (the reference evaluates them unfused).
-// The x pass stores only the winning dx (int16); the y pass recomputes the
-// winning x-pass value from S, which is the same double again.
+//           xbest[cy+dy] - (c_dy*dy + (c_dyy*dy)*dy), cy = scale*ry + ay;
+//   total = root + sum_parts best + bias, summed in part order.
+// Penalties use round-to-nearest intrinsics (no FMA contraction), matching
+// the reference's unfused float64 evaluation.
 //
-// radius < 0 selects the unbounded generalised distance transform: the
-// window radius becomes r* from the map's range, past
-// which no maximiser can lie, so the window result equals the unbounded one.
+// Speed: each CTA owns a 32 x 32 tile of roots of one (image, component,
+// root level).  Per part it stages the S band its windows touch in shared
+// memory, runs the x pass for every band row at the 32 centre columns, then
+// the y pass for the 1024 roots.  Candidates are screened in FP32: with
+// E = 2^-20 * (max|S| + max pen_x + max pen_y) bounding the FP32 error of
+// every candidate value, a candidate more than 2E below the running winner
+// cannot beat it and one more than 2E above must; only candidates inside the
+// +-2E band are compared in FP64.  The scan order and the strict '>' rule are
+// those of the reference, so the winner is the reference's.
+//
+// radius < 0 selects the unbounded generalised distance transform, realised
+// as the window of radius r* computed from the map's
+// range, beyond which no maximiser lies.  Jobs whose radius exceeds RCAP use
+// an unstaged path with the same arithmetic.
 #include <math.h>
 
 #include "common.cuh"
 
 namespace dpm {
 
-constexpr int K3_THREADS = 256;
+constexpr int PT_W = 32;                    // root columns per tile (lanes)
+constexpr int PT_H = 32;                    // root rows per tile
+constexpr int PT_THREADS = 256;
+constexpr int RCAP = 24;                    // staged path radius cap
+constexpr int BAND_MAX = 2 * PT_H + 2 * RCAP;           // scale <= 2
+constexpr int COLS_MAX = 2 * (PT_W - 1) + 1 + 2 * RCAP;  // 111
+constexpr int COLS_PITCH = COLS_MAX + 1;
+
+struct __align__(16) PlaceSmem {
+  float s[BAND_MAX * COLS_PITCH];        // staged S band (-inf outside the map)
+  double xb[BAND_MAX * PT_W];            // x-pass exact values
+  float x32[BAND_MAX * PT_W];            // x-pass values rounded to FP32
+  short xdx[BAND_MAX * PT_W];            // x-pass argmax dx
+  float npx32[2 * RCAP + 1], npy32[2 * RCAP + 1];
+  double npx[2 * RCAP + 1], npy[2 * RCAP + 1];
+};
 
 __device__ __forceinline__ double pen(double c1, double c2, int d) {
   const double dd = (double)d;
   return __dadd_rn(__dmul_rn(c1, dd), __dmul_rn(__dmul_rn(c2, dd), dd));
 }
 
-// r* of App. A.2 for one axis (a = quadratic, b = linear coefficient of that
-// axis, (a_o, b_o) of the other), from the map's [min, max]; +1 guards the
-// floor against rounding (any radius >= r* gives the identical result).
-__device__ __forceinline__ int radius_of(const dpm_place_job& j, const uint32_t* ranges, bool x_axis) {
+__device__ __forceinline__ double pen_absmax(double c1, double c2, int r) {
+  double m = fmax(fabs(pen(c1, c2, -r)), fabs(pen(c1, c2, r)));
+  if (c2 > 0.0) m = fmax(m, c1 * c1 / (4.0 * c2));
+  return m;
+}
+
+// r* of App. A.2 for one axis from the map range; +1 guards the floor.
+__device__ __forceinline__ int radius_of(const dpm_place_job& j, float vmax, float vmin, bool x_axis) {
   if (j.radius >= 0) return j.radius;
-  const float vmax = key_float(ranges[2 * j.range_idx]);
-  const float vmin = key_float(ranges[2 * j.range_idx + 1]);
   const double a = x_axis ? j.cdxx : j.cdyy, b = x_axis ? j.cdx : j.cdy;
   const double ao = x_axis ? j.cdyy : j.cdxx, bo = x_axis ? j.cdy : j.cdx;
   const double dprime = ((double)vmax - (double)vmin) + bo * bo / (4.0 * ao);
-  const double r = (fabs(b) + sqrt(b * b + 4.0 * a * dprime)) / (2.0 * a);
-  return (int)floor(r) + 1;
-}
-
-__global__ void __launch_bounds__(K3_THREADS)
-xpass_kernel(const float* __restrict__ S, int16_t* __restrict__ DX,
-             const dpm_place_job* __restrict__ jobs, int njobs, const uint32_t* __restrict__ ranges) {
-  const int jid = find_job(jobs, njobs, blockIdx.x);
-  const dpm_place_job j = jobs[jid];
-  const int64_t e = (int64_t)(blockIdx.x - j.block0) * K3_THREADS + threadIdx.x;
-  if (e >= (int64_t)j.Hp * j.wr) return;
-  const int y = (int)(e / j.wr), c = (int)(e - (int64_t)y * j.wr);
-  const int cx = j.scale * (j.rx0 + c) + j.ax;
-  const int r = radius_of(j, ranges, true);
-  const float* row = S + j.s_off + (int64_t)y * j.Wp;
-  const int lo = max(-r, -cx), hi = min(r, j.Wp - 1 - cx);
-  double best = -INFINITY;
-  int bdx = -r;
-  for (int dx = lo; dx <= hi; ++dx) {
-    const double cand = __dadd_rn((double)__ldg(row + cx + dx), -pen(j.cdx, j.cdxx, dx));
-    if (cand > best) {
-      best = cand;
-      bdx = dx;
-    }
-  }
-  DX[j.dx_off + e] = (int16_t)bdx;
+  return (int)floor((fabs(b) + sqrt(b * b + 4.0 * a * dprime)) / (2.0 * a)) + 1;
 }
 
 __device__ __forceinline__ uint32_t pack_pos(int y, int x) {
   return ((uint32_t)(uint16_t)(int16_t)y << 16) | (uint32_t)(uint16_t)(int16_t)x;
 }
 
-__global__ void __launch_bounds__(K3_THREADS)
-assemble_kernel(const float* __restrict__ S, const int16_t* __restrict__ DX,
-                const dpm_place_job* __restrict__ pjobs, const dpm_asm_job* __restrict__ ajobs,
-                int najobs, const uint32_t* __restrict__ ranges, double* __restrict__ total,
-                uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
-                dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
+// Screened strict-'>' update.  (v32, vexact-on-demand) against the winner.
+struct Winner {
+  float w32, hi, lo;
+  double wx;
+  bool wx_ok;
+  int idx;
+};
+
+__device__ __forceinline__ void win_init(Winner& w, int idx0) {
+  w.w32 = -INFINITY; w.hi = -INFINITY; w.lo = -INFINITY;
+  w.wx = -INFINITY; w.wx_ok = true; w.idx = idx0;
+}
+
+// Placement of one part for one root via direct global loads (any radius).
+__device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job& pj, int cy,
+                               int cx, int rx_, int ry_, double& best, int& bdy, int& bdx) {
+  best = -INFINITY;
+  bdy = -ry_;
+  bdx = -rx_;
+  for (int dy = -ry_; dy <= ry_; ++dy) {
+    const int y = cy + dy;
+    if (y < 0 || y >= pj.Hp) continue;
+    double xb = -INFINITY;
+    int xd = -rx_;
+    const int lo = max(-rx_, -cx), hi = min(rx_, pj.Wp - 1 - cx);
+    for (int dx = lo; dx <= hi; ++dx) {
+      const double c = __dadd_rn((double)__ldg(sm + (int64_t)y * pj.Wp + cx + dx),
+                                 -pen(pj.cdx, pj.cdxx, dx));
+      if (c > xb) { xb = c; xd = dx; }
+    }
+    const double cand = __dadd_rn(xb, -pen(pj.cdy, pj.cdyy, dy));
+    if (cand > best) { best = cand; bdy = dy; bdx = xd; }
+  }
+}
+
+__global__ void __launch_bounds__(PT_THREADS, 2)
+place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restrict__ pjobs,
+                      const dpm_asm_job* __restrict__ ajobs, int najobs,
+                      const uint32_t* __restrict__ ranges, double* __restrict__ total,
+                      uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
+                      dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlaceSmem& sh = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int jid = find_job(ajobs, najobs, blockIdx.x);
   const dpm_asm_job aj = ajobs[jid];
   const int hr = aj.ry1 - aj.ry0 + 1, wr = aj.rx1 - aj.rx0 + 1;
-  const int64_t e = (int64_t)(blockIdx.x - aj.block0) * K3_THREADS + threadIdx.x;
-  const bool live = e < (int64_t)hr * wr;
-  const int iy = live ? (int)(e / wr) : 0, ix = live ? (int)(e - (int64_t)iy * wr) : 0;
-  const int ry = aj.ry0 + iy, rx = aj.rx0 + ix;
+  const int ntx = (wr + PT_W - 1) / PT_W;
+  const int tile = blockIdx.x - aj.block0;
+  const int ty0 = (tile / ntx) * PT_H, tx0 = (tile % ntx) * PT_W;  // offsets inside the rect
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int RPT = PT_H / (PT_THREADS / 32);  // roots per thread (4)
+  const int ix = tx0 + lane;
+  const bool col_ok = ix < wr;
+  const int rx = aj.rx0 + ix;
 
-  double tot = 0.0;
-  uint32_t parts[DPM_MAX_PARTS];
-  if (live) {
-    if (aj.root_off >= 0) tot = (double)__ldg(S + aj.root_off + (int64_t)ry * aj.root_pitch + rx);
-    for (int p = 0; p < aj.nparts; ++p) {
-      const dpm_place_job pj = pjobs[aj.part_job0 + p];
-      const int c = rx - pj.rx0;
-      const int cx = pj.scale * rx + pj.ax, cy = pj.scale * ry + pj.ay;
-      const int r = radius_of(pj, ranges, false);
-      const int lo = max(-r, -cy), hi = min(r, pj.Hp - 1 - cy);
-      const float* sm = S + pj.s_off;
-      const int16_t* dxt = DX + pj.dx_off + c;
-      double best = -INFINITY;
-      int bdy = -r, bdx = -r;
-      for (int dy = lo; dy <= hi; ++dy) {
-        const int y = cy + dy;
-        const int dx = dxt[(int64_t)y * pj.wr];
-        const int x = cx + dx;
-        double vx = -INFINITY;
-        if (x >= 0 && x < pj.Wp)
-          vx = __dadd_rn((double)__ldg(sm + (int64_t)y * pj.Wp + x), -pen(pj.cdx, pj.cdxx, dx));
-        const double cand = __dadd_rn(vx, -pen(pj.cdy, pj.cdyy, dy));
-        if (cand > best) {
-          best = cand;
-          bdy = dy;
-          bdx = dx;
-        }
+  double tot[RPT];
+  uint32_t parts[RPT][DPM_MAX_PARTS];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int iy = ty0 + warp + 8 * k;
+    tot[k] = 0.0;
+    if (aj.root_off >= 0 && col_ok && iy < hr)
+      tot[k] = (double)__ldg(S + aj.root_off + (int64_t)(aj.ry0 + iy) * aj.root_pitch + rx);
+  }
+
+  const int ry_lo = aj.ry0 + ty0;
+  const int ry_hi = aj.ry0 + min(ty0 + PT_H, hr) - 1;
+  const int rx_lo = aj.rx0 + tx0;
+
+  for (int p = 0; p < aj.nparts; ++p) {
+    const dpm_place_job pj = pjobs[aj.part_job0 + p];
+    const float vmax = key_float(ranges[2 * pj.range_idx]);
+    const float vmin = key_float(ranges[2 * pj.range_idx + 1]);
+    const int rxr = radius_of(pj, vmax, vmin, true);
+    const int ryr = radius_of(pj, vmax, vmin, false);
+    const float* sm = S + pj.s_off;
+    const bool staged = rxr <= RCAP && ryr <= RCAP && pj.scale <= 2;
+    if (!staged) {
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const int iy = ty0 + warp + 8 * k;
+        if (!col_ok || iy >= hr) continue;
+        const int ry = aj.ry0 + iy;
+        const int cy = pj.scale * ry + pj.ay, cx = pj.scale * rx + pj.ax;
+        double best;
+        int bdy, bdx;
+        place_unstaged(sm, pj, cy, cx, rxr, ryr, best, bdy, bdx);
+        tot[k] = __dadd_rn(tot[k], best);
+        const uint32_t pk = pack_pos(cy + bdy, cx + bdx);
+        if (p < DPM_MAX_PARTS) parts[k][p] = pk;
+        const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
+        if (aj.pos_off >= 0) pos[aj.pos_off + o] = pk;
+        if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
       }
-      tot = __dadd_rn(tot, best);
-      const uint32_t pk = pack_pos(cy + bdy, cx + bdx);
-      if (p < DPM_MAX_PARTS) parts[p] = pk;
+      continue;
+    }
+    const double mabs = fmax(fabs((double)vmax), fabs((double)vmin));
+    const float E2 = (float)(2.0 * ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, rxr) +
+                                         pen_absmax(pj.cdy, pj.cdyy, ryr), -20));
+    // band: map rows / cols the windows of this tile can reach
+    const int yb0 = pj.scale * ry_lo + pj.ay - ryr;
+    const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * ryr;
+    const int xb0 = pj.scale * rx_lo + pj.ax - rxr;
+    const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * rxr;
+
+    __syncthreads();  // previous part done with the band
+    for (int d = threadIdx.x; d <= 2 * RCAP; d += PT_THREADS) {
+      const int dd = d - RCAP;
+      const double px = pen(pj.cdx, pj.cdxx, dd), py = pen(pj.cdy, pj.cdyy, dd);
+      sh.npx[d] = -px; sh.npy[d] = -py;
+      sh.npx32[d] = (float)(-px); sh.npy32[d] = (float)(-py);
+    }
+    for (int e = threadIdx.x; e < nrows * ncols; e += PT_THREADS) {
+      const int r = e / ncols, c = e - r * ncols;
+      const int y = yb0 + r, x = xb0 + c;
+      float v = -INFINITY;
+      if (y >= 0 && y < pj.Hp && x >= 0 && x < pj.Wp) v = __ldg(sm + (int64_t)y * pj.Wp + x);
+      sh.s[r * COLS_PITCH + c] = v;
+    }
+    __syncthreads();
+
+    // x pass: band row r (warp-strided), centre column = lane
+    for (int r = warp; r < nrows; r += PT_THREADS / 32) {
+      const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + rxr;  // dx = 0
+      Winner w;
+      win_init(w, -rxr);
+      for (int dx = -rxr; dx <= rxr; ++dx) {
+        const float v = srow[dx] + sh.npx32[dx + RCAP];
+        if (v <= w.lo) continue;
+        if (v > w.hi) {
+          w.w32 = v; w.idx = dx; w.wx_ok = false;
+        } else {
+          const double vx = __dadd_rn((double)srow[dx], sh.npx[dx + RCAP]);
+          if (!w.wx_ok) { w.wx = __dadd_rn((double)srow[w.idx], sh.npx[w.idx + RCAP]); w.wx_ok = true; }
+          if (vx > w.wx) { w.wx = vx; w.w32 = v; w.idx = dx; }
+        }
+        w.hi = w.w32 + E2; w.lo = w.w32 - E2;
+      }
+      if (!w.wx_ok) w.wx = __dadd_rn((double)srow[w.idx], sh.npx[w.idx + RCAP]);
+      sh.xb[r * PT_W + lane] = w.wx;
+      sh.x32[r * PT_W + lane] = (float)w.wx;
+      sh.xdx[r * PT_W + lane] = (short)w.idx;
+    }
+    __syncthreads();
+
+    // y pass for this thread's roots
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const int iy = ty0 + warp + 8 * k;
+      if (!col_ok || iy >= hr) continue;
+      const int ry = aj.ry0 + iy;
+      const int r0 = pj.scale * (ry - ry_lo) + ryr;  // band row of dy = 0
+      Winner w;
+      win_init(w, -ryr);
+      for (int dy = -ryr; dy <= ryr; ++dy) {
+        const int rr = (r0 + dy) * PT_W + lane;
+        const float v = sh.x32[rr] + sh.npy32[dy + RCAP];
+        if (v <= w.lo) continue;
+        if (v > w.hi) {
+          w.w32 = v; w.idx = dy; w.wx_ok = false;
+        } else {
+          const double vx = __dadd_rn(sh.xb[rr], sh.npy[dy + RCAP]);
+          if (!w.wx_ok) {
+            w.wx = __dadd_rn(sh.xb[(r0 + w.idx) * PT_W + lane], sh.npy[w.idx + RCAP]);
+            w.wx_ok = true;
+          }
+          if (vx > w.wx) { w.wx = vx; w.w32 = v; w.idx = dy; }
+        }
+        w.hi = w.w32 + E2; w.lo = w.w32 - E2;
+      }
+      const int rr = (r0 + w.idx) * PT_W + lane;
+      if (!w.wx_ok) w.wx = __dadd_rn(sh.xb[rr], sh.npy[w.idx + RCAP]);
+      const int bdx = (w.w32 == -INFINITY) ? -rxr : sh.xdx[rr];
+      const int cy = pj.scale * ry + pj.ay, cx = pj.scale * rx + pj.ax;
+      tot[k] = __dadd_rn(tot[k], w.wx);
+      const uint32_t pk = pack_pos(cy + w.idx, cx + bdx);
+      if (p < DPM_MAX_PARTS) parts[k][p] = pk;
       const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
       if (aj.pos_off >= 0) pos[aj.pos_off + o] = pk;
-      if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
+      if (aj.placed_off >= 0) placed[aj.placed_off + o] = w.wx;
     }
-    tot = __dadd_rn(tot, aj.bias);
-    if (aj.total_off >= 0) total[aj.total_off + (int64_t)iy * wr + ix] = tot;
   }
-  if (dets == nullptr) return;
-  const bool hit = live && tot >= tau;
-  const unsigned mask = __ballot_sync(0xffffffffu, hit);
-  if (mask == 0u) return;
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(det_count, __popc(mask));
-  base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
-  if (!hit) return;
-  const int slot = base + __popc(mask & ((1u << lane) - 1u));
-  if (slot >= max_dets) return;
-  dpm_detection d;
-  d.image = aj.image;
-  d.level = aj.level;
-  d.component = aj.component;
-  d.ry = ry;
-  d.rx = rx;
-  d.nparts = aj.nparts;
-  d.score = tot;
-  for (int p = 0; p < DPM_MAX_PARTS; ++p) d.parts[p] = p < aj.nparts ? parts[p] : 0u;
-  dets[slot] = d;
+
+  // bias, totals, tau compaction
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int iy = ty0 + warp + 8 * k;
+    const bool live = col_ok && iy < hr;
+    if (live) {
+      tot[k] = __dadd_rn(tot[k], aj.bias);
+      if (aj.total_off >= 0) total[aj.total_off + (int64_t)iy * wr + ix] = tot[k];
+    }
+    if (dets == nullptr) continue;
+    const bool hit = live && tot[k] >= tau;
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (mask == 0u) continue;
+    const int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(det_count, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!hit) continue;
+    const int slot = base + __popc(mask & ((1u << lane) - 1u));
+    if (slot >= max_dets) continue;
+    dpm_detection d;
+    d.image = aj.image;
+    d.level = aj.level;
+    d.component = aj.component;
+    d.ry = aj.ry0 + iy;
+    d.rx = rx;
+    d.nparts = aj.nparts;
+    d.score = tot[k];
+#pragma unroll
+    for (int p = 0; p < DPM_MAX_PARTS; ++p) d.parts[p] = p < aj.nparts ? parts[k][p] : 0u;
+    dets[slot] = d;
+  }
 }
 
 }  // namespace dpm
 
 using namespace dpm;
 
-extern "C" int64_t dpm_place_prepare(dpm_place_job* jobs, int njobs) {
-  if (njobs < 0 || (njobs > 0 && !jobs)) {
-    set_error("dpm_place_prepare: bad job table");
+extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_place_job* pjobs,
+                                        int npjobs) {
+  if (njobs < 0 || (njobs > 0 && !jobs) || npjobs < 0 || (npjobs > 0 && !pjobs)) {
+    set_error("dpm_assemble_prepare: bad job tables");
     return DPM_ERR_ARG;
   }
-  int64_t b = 0;
-  for (int i = 0; i < njobs; ++i) {
-    const dpm_place_job& j = jobs[i];
-    if (j.Hp < 1 || j.Wp < 1 || j.wr < 1 || j.scale < 1) {
-      set_error("dpm_place_prepare: job %d has Hp=%d Wp=%d wr=%d scale=%d", i, j.Hp, j.Wp, j.wr,
-                j.scale);
-      return DPM_ERR_ARG;
-    }
-    if (j.radius > 32000) {
-      set_error("dpm_place_prepare: job %d radius %d too large", i, j.radius);
+  for (int i = 0; i < npjobs; ++i) {
+    const dpm_place_job& j = pjobs[i];
+    if (j.Hp < 1 || j.Wp < 1 || j.scale < 1 || j.radius > 32000 || j.range_idx < 0) {
+      set_error("dpm_assemble_prepare: placement job %d has Hp=%d Wp=%d scale=%d radius=%d "
+                "range_idx=%d", i, j.Hp, j.Wp, j.scale, j.radius, j.range_idx);
       return DPM_ERR_ARG;
     }
     if (j.radius < 0 && !(j.cdxx > 0.0 && j.cdyy > 0.0)) {
-      set_error("dpm_place_prepare: job %d: the unbounded transform needs c_dxx, c_dyy > 0", i);
+      set_error("dpm_assemble_prepare: placement job %d: the unbounded transform needs "
+                "c_dxx, c_dyy > 0", i);
       return DPM_ERR_ARG;
     }
-    if (j.radius < 0 && j.range_idx < 0) {
-      set_error("dpm_place_prepare: job %d: GDT mode needs a range slot", i);
-      return DPM_ERR_ARG;
-    }
-    jobs[i].block0 = (int32_t)b;
-    b += ((int64_t)j.Hp * j.wr + K3_THREADS - 1) / K3_THREADS;
-  }
-  return b;
-}
-
-extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs) {
-  if (njobs < 0 || (njobs > 0 && !jobs)) {
-    set_error("dpm_assemble_prepare: bad job table");
-    return DPM_ERR_ARG;
   }
   int64_t b = 0;
   for (int i = 0; i < njobs; ++i) {
     const dpm_asm_job& j = jobs[i];
-    if (j.ry1 < j.ry0 || j.rx1 < j.rx0 || j.nparts < 0 || j.nparts > DPM_MAX_PARTS) {
-      set_error("dpm_assemble_prepare: job %d has rect (%d,%d,%d,%d) nparts=%d", i, j.ry0, j.ry1,
-                j.rx0, j.rx1, j.nparts);
+    if (j.ry1 < j.ry0 || j.rx1 < j.rx0 || j.nparts < 0 || j.nparts > DPM_MAX_PARTS ||
+        j.part_job0 < 0 || j.part_job0 + j.nparts > npjobs) {
+      set_error("dpm_assemble_prepare: job %d has rect (%d,%d,%d,%d) parts [%d, +%d)", i, j.ry0,
+                j.ry1, j.rx0, j.rx1, j.part_job0, j.nparts);
       return DPM_ERR_ARG;
     }
     jobs[i].block0 = (int32_t)b;
-    b += ((int64_t)(j.ry1 - j.ry0 + 1) * (j.rx1 - j.rx0 + 1) + K3_THREADS - 1) / K3_THREADS;
+    const int64_t hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
+    b += ((hr + PT_H - 1) / PT_H) * ((wr + PT_W - 1) / PT_W);
+  }
+  if (b > INT32_MAX) {
+    set_error("dpm_assemble_prepare: too many CTAs");
+    return DPM_ERR_ARG;
   }
   return b;
 }
 
-extern "C" int dpm_place_xpass(const float* S, int16_t* dx, const dpm_place_job* jobs, int njobs,
-                               int64_t nblocks, const uint32_t* ranges, void* stream) {
-  DPM_REQUIRE(S && dx && jobs, "dpm_place_xpass: null pointer");
-  DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_place_xpass: nblocks");
-  if (njobs == 0 || nblocks == 0) return DPM_OK;
-  xpass_kernel<<<(unsigned)nblocks, K3_THREADS, 0, as_stream(stream)>>>(S, dx, jobs, njobs, ranges);
-  DPM_LAUNCHED("xpass_kernel");
-  return DPM_OK;
-}
-
-extern "C" int dpm_assemble(const float* S, const int16_t* dx, const dpm_place_job* pjobs,
-                            const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
-                            const uint32_t* ranges, double* total, uint32_t* pos, double* placed,
-                            double tau, dpm_detection* dets, int max_dets, int* det_count,
-                            void* stream) {
-  DPM_REQUIRE(S && pjobs && ajobs, "dpm_assemble: null pointer");
+extern "C" int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
+                            int najobs, int64_t nblocks, const uint32_t* ranges, double* total,
+                            uint32_t* pos, double* placed, double tau, dpm_detection* dets,
+                            int max_dets, int* det_count, void* stream) {
+  DPM_REQUIRE(S && pjobs && ajobs && ranges, "dpm_assemble: null pointer");
   DPM_REQUIRE(!dets || det_count, "dpm_assemble: detections need a counter");
   DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_assemble: nblocks");
   if (najobs == 0 || nblocks == 0) return DPM_OK;
-  assemble_kernel<<<(unsigned)nblocks, K3_THREADS, 0, as_stream(stream)>>>(
-      S, dx, pjobs, ajobs, najobs, ranges, total, pos, placed, tau, dets, max_dets, det_count);
-  DPM_LAUNCHED("assemble_kernel");
+  const size_t smem = sizeof(PlaceSmem);
+  DPM_CUDA(cudaFuncSetAttribute(place_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  place_assemble_kernel<<<(unsigned)nblocks, PT_THREADS, smem, as_stream(stream)>>>(
+      S, pjobs, ajobs, najobs, ranges, total, pos, placed, tau, dets, max_dets, det_count);
+  DPM_LAUNCHED("place_assemble_kernel");
   return DPM_OK;
 }

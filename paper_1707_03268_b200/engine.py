@@ -12,7 +12,6 @@ HBM layout (per image, images stacked):
             axis-major feature-map order, validation.py:65-86)
   P arena : levels back to back, each planar [Rtot][H][pitch] float32
   S arena : response maps, one block [nf][Ho][Wo] per (level, filter group)
-  DX arena: x-pass argmax tables, [Hp][wr] int16 per placed part
 """
 
 from dataclasses import dataclass, field
@@ -140,7 +139,9 @@ class Plan:
             if fd.h > H or fd.w > W:
                 raise ValidationError(f"filter extent ({fd.h}, {fd.w}) exceeds image extent "
                                       f"({H}, {W})")
-        gdt_maps = set((p.level, p.filt) for a in self.assemblies for p in a.parts if p.radius < 0)
+        # every placed map gets a range slot: r* (GDT mode) and the FP32
+        # screening error bound of the placement kernel both come from it
+        placed_maps = set((p.level, p.filt) for a in self.assemblies for p in a.parts)
 
         # per-image level offsets
         xa, pa = _Arena(), _Arena()
@@ -200,7 +201,7 @@ class Plan:
                 ho, wo = H - fd.h + 1, W - fd.w + 1
                 s_off = sa.take(len(fl) * ho * wo, align=4)
                 rng = -1
-                if any((k, f) in gdt_maps for f in fl):
+                if any((k, f) in placed_maps for f in fl):
                     rng = nslots
                     nslots += len(fl)
                 for i, f in enumerate(fl):
@@ -237,7 +238,6 @@ class Plan:
                                                               len(self._proj_jobs)), "project")
 
         # placement + assembly jobs
-        da = _Arena()
         ta, oa, pla = _Arena(), _Arena(), _Arena()
         place, asm_jobs = [], []
         self.asm_index = {}  # (image, a) -> (total_off, pos_off, placed_off, hr, wr)
@@ -252,10 +252,9 @@ class Plan:
                 first = len(place)
                 for p in a.parts:
                     hp, wp = self.map_shape[(p.level, p.filt)]
-                    dxo = da.take(hp * wr, align=8)
-                    rslot = self.range_slot.get((img, p.level, p.filt), -1)
-                    place.append((self.map_off[(img, p.level, p.filt)], dxo, hp, wp,
-                                  p.anchor[0], p.anchor[1], p.scale, p.radius, rx0, wr, rslot, 0,
+                    place.append((self.map_off[(img, p.level, p.filt)], hp, wp,
+                                  p.anchor[0], p.anchor[1], p.scale, p.radius,
+                                  self.range_slot[(img, p.level, p.filt)], 0,
                                   *[float(v) for v in p.deformation]))
                 root_off, root_pitch = -1, 0
                 if a.root is not None:
@@ -274,11 +273,9 @@ class Plan:
                                  float(a.bias)))
         self._place_jobs = np.array(place, dtype=_lib.PLACE_JOB) if place else np.zeros(0, _lib.PLACE_JOB)
         self._asm_jobs = np.array(asm_jobs, dtype=_lib.ASM_JOB) if asm_jobs else np.zeros(0, _lib.ASM_JOB)
-        self._place_blocks = _lib.check(lib.dpm_place_prepare(_lib.table_ptr(self._place_jobs),
-                                                             len(self._place_jobs)), "placement")
-        self._asm_blocks = _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(self._asm_jobs),
-                                                              len(self._asm_jobs)), "assembly")
-        self.dx_size = max(da.size, 8)
+        self._asm_blocks = _lib.check(lib.dpm_assemble_prepare(
+            _lib.table_ptr(self._asm_jobs), len(self._asm_jobs),
+            _lib.table_ptr(self._place_jobs), len(self._place_jobs)), "assembly")
         self.total_size, self.pos_size, self.placed_size = ta.size, oa.size, pla.size
 
     _tile_cache = {}
@@ -306,7 +303,6 @@ class Plan:
         self.X = t.empty(self.n_images * self.x_image_stride, dtype=t.float32, device=dev)
         self.P = t.empty(self.n_images * self.p_image_stride, dtype=t.float32, device=dev)
         self.S = t.empty(self.s_size, dtype=t.float32, device=dev)
-        self.DX = t.empty(self.dx_size, dtype=t.int16, device=dev)
         self.ranges = t.empty(max(2 * self.n_ranges, 2), dtype=t.int32, device=dev)
         self.totals = t.empty(max(self.total_size, 1), dtype=t.float64, device=dev)
         self.positions = t.empty(max(self.pos_size, 1), dtype=t.int32, device=dev)
@@ -350,16 +346,12 @@ class Plan:
                                              ptr(self.corr_jobs_d), ptr(tiles_d), len(tiles), h,
                                              nf, R, w_max, rng, s), "correlate")
         if "place" in stages and len(self._asm_jobs):
-            rng = ptr(self.ranges) if self.n_ranges else None
-            if len(self._place_jobs):
-                _lib.check(lib.dpm_place_xpass(ptr(self.S), ptr(self.DX), ptr(self.place_jobs_d),
-                                               len(self._place_jobs), self._place_blocks, rng, s),
-                           "placement")
+            rng = ptr(self.ranges)
             if self.det_count is not None:
                 with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
                     self.det_count.zero_()
             _lib.check(lib.dpm_assemble(
-                ptr(self.S), ptr(self.DX), ptr(self.place_jobs_d), ptr(self.asm_jobs_d),
+                ptr(self.S), ptr(self.place_jobs_d), ptr(self.asm_jobs_d),
                 len(self._asm_jobs), self._asm_blocks, rng,
                 ptr(self.totals) if self.total_size else None,
                 ptr(self.positions) if self.pos_size else None,
