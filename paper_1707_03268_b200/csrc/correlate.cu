@@ -54,6 +54,7 @@ struct CorrArgs {
   int ntiles;
   int nwf, nwy;
   int w_max;
+  int R_max;
   uint32_t* ranges;
 };
 
@@ -69,6 +70,38 @@ __device__ __forceinline__ void fold_range(uint32_t* ranges, int slot, float vma
   }
 }
 
+// Stage the P chunk of one tile (nr planes x TROWS x (32 + w - 1)) with
+// cp.async; zero-fill outside the level.
+__device__ __forceinline__ void stage_p(float* dst, const CorrArgs& a, const dpm_corr_job& job,
+                                        int rc, int nr, int y0, int x0, int TROWS, int TPITCH) {
+  const int tcols = 32 + job.w - 1;
+  const int per_plane = TROWS * tcols;
+  const int64_t plane = (int64_t)job.H * job.pitch;
+  const float* pbase = a.P + job.p_off + (int64_t)(job.chan_off + rc) * plane;
+  for (int e = threadIdx.x; e < nr * per_plane; e += blockDim.x) {
+    const int r = e / per_plane, rem = e - r * per_plane;
+    const int row = rem / tcols, col = rem - row * tcols;
+    const int gy = y0 + row, gx = x0 + col;
+    const bool ok = gy < job.H && gx < job.W;
+    const float* src = ok ? pbase + r * plane + (int64_t)gy * job.pitch + gx : a.P;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + (r * TROWS + row) * TPITCH + col);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src),
+                 "r"(ok ? 4 : 0));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+__device__ __forceinline__ void stage_g(float* sG, const CorrArgs& a, const dpm_corr_job& job,
+                                        int FH, int rc, int nr) {
+  const int nfp = job.nf_pad;
+  const int per_ij = nr * nfp;
+  const int total = FH * job.w * per_ij;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int ij = e / per_ij, rem = e - ij * per_ij;
+    sG[ij * per_ij + rem] = __ldg(a.G + job.g_off + ((int64_t)ij * job.R + rc) * nfp + rem);
+  }
+}
+
 template <int FH, int NF>
 __global__ void __launch_bounds__(32 * K2_MAX_WARPS)
 corr_kernel(const CorrArgs a) {
@@ -80,19 +113,26 @@ corr_kernel(const CorrArgs a) {
   const int TY = a.nwy * MP;
   const int TROWS = TY + FH - 1;
   const int TPITCH = 32 + a.w_max - 1;
-  float* sP = smem;                                             // [RCH][TROWS][TPITCH]
-  float* sG = smem + ((K2_RCH * TROWS * TPITCH + 3) & ~3);      // [FH][w][RCH][nf_pad]
+  const int PBUF = (K2_RCH * TROWS * TPITCH + 3) & ~3;
+  float* sPb[2] = {smem, smem + PBUF};                   // [RCH][TROWS][TPITCH] x 2
+  float* sG = smem + 2 * PBUF;                           // [FH][w][RCH][nf_pad]
+  // one rank chunk per tile: prefetch the next tile's P during this one
+  const bool pipelined = a.R_max <= K2_RCH;
 
   int64_t staged_g = -1;
   int staged_chunk = -1;
-  for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+  int it = 0;
+  if (pipelined && blockIdx.x < a.ntiles) {
+    const dpm_corr_tile t0 = a.tiles[blockIdx.x];
+    const dpm_corr_job j0 = a.jobs[t0.job];
+    stage_p(sPb[0], a, j0, 0, j0.R, t0.ty * TY, t0.tx * 32, TROWS, TPITCH);
+  }
+  for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
     const dpm_corr_tile tile = a.tiles[t];
     const dpm_corr_job job = a.jobs[tile.job];
     const int ho = job.H - FH + 1, wo = job.W - job.w + 1;
     const int y0 = tile.ty * TY, x0 = tile.tx * 32;
     const int w = job.w, nfp = job.nf_pad;
-    const int tcols = 32 + w - 1;
-    const int64_t plane = (int64_t)job.H * job.pitch;
 
     float acc[MP][NF];
 #pragma unroll
@@ -102,30 +142,26 @@ corr_kernel(const CorrArgs a) {
 
     for (int rc = 0; rc < job.R; rc += K2_RCH) {
       const int nr = min(K2_RCH, job.R - rc);
-      __syncthreads();  // previous users of sP / sG are done
-      // stage the core chunk unless it is already resident
-      if (staged_g != job.g_off || staged_chunk != rc) {
-        const int per_ij = nr * nfp;
-        const int total = FH * w * per_ij;
-        for (int e = threadIdx.x; e < total; e += blockDim.x) {
-          const int ij = e / per_ij, rem = e - ij * per_ij;
-          sG[ij * per_ij + rem] = __ldg(a.G + job.g_off + ((int64_t)ij * job.R + rc) * nfp + rem);
+      float* sP = sPb[pipelined ? (it & 1) : 0];
+      __syncthreads();  // every warp is done with the buffers about to be refilled
+      if (pipelined) {
+        const int tn = t + gridDim.x;
+        if (tn < a.ntiles) {
+          const dpm_corr_tile nt = a.tiles[tn];
+          const dpm_corr_job nj = a.jobs[nt.job];
+          stage_p(sPb[(it + 1) & 1], a, nj, 0, nj.R, nt.ty * TY, nt.tx * 32, TROWS, TPITCH);
+          asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
         }
+      } else {
+        stage_p(sP, a, job, rc, nr, y0, x0, TROWS, TPITCH);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
+      if (staged_g != job.g_off || staged_chunk != rc) {
+        stage_g(sG, a, job, FH, rc, nr);
         staged_g = job.g_off;
         staged_chunk = rc;
-      }
-      // stage the P chunk: nr planes x TROWS x tcols (zero outside the level)
-      {
-        const int per_plane = TROWS * tcols;
-        const float* pbase = a.P + job.p_off + (int64_t)(job.chan_off + rc) * plane;
-        for (int e = threadIdx.x; e < nr * per_plane; e += blockDim.x) {
-          const int r = e / per_plane, rem = e - r * per_plane;
-          const int row = rem / tcols, col = rem - row * tcols;
-          const int gy = y0 + row, gx = x0 + col;
-          float v = 0.f;
-          if (gy < job.H && gx < job.W) v = __ldg(pbase + r * plane + (int64_t)gy * job.pitch + gx);
-          sP[(r * TROWS + row) * TPITCH + col] = v;
-        }
       }
       __syncthreads();
 
@@ -175,6 +211,7 @@ corr_kernel(const CorrArgs a) {
         fold_range(a.ranges, job.range_idx + fg, vmax, vmin);
     }
   }
+  asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 // Generic fallback: any h, any nf; one thread per (position, filter loop).
@@ -224,7 +261,7 @@ static bool pick(int h, int nf, Shape* s) {
   if (nf <= 8) {
     s->nf_kernel = nf <= 2 ? 2 : nf <= 4 ? 4 : nf <= 6 ? 6 : 8;
     s->nwf = 1;
-    s->nwy = 4;
+    s->nwy = 2;
   } else {
     s->nf_kernel = 8;
     s->nwf = (nf + 7) / 8;
@@ -298,7 +335,7 @@ extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm
   int dev = 0, sms = 148;
   DPM_CUDA(cudaGetDevice(&dev));
   DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CorrArgs a{P, G, S, jobs, tiles, ntiles, 1, 1, w_max, ranges};
+  CorrArgs a{P, G, S, jobs, tiles, ntiles, 1, 1, w_max, R, ranges};
   Shape s;
   if (!pick(h, nf, &s)) {
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 8);
@@ -311,7 +348,7 @@ extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm
   const int TROWS = s.nwy * K2_MP + h - 1;
   const int TPITCH = 32 + w_max - 1;
   const int nfp = (nf + 7) & ~7;  // core filter stride (dpm_corr_job.nf_pad)
-  const size_t smem = sizeof(float) * ((((size_t)K2_RCH * TROWS * TPITCH) + 3 & ~(size_t)3) +
+  const size_t smem = sizeof(float) * (2 * ((((size_t)K2_RCH * TROWS * TPITCH) + 3) & ~(size_t)3) +
                                        (size_t)h * w_max * K2_RCH * nfp);
   DPM_REQUIRE(smem <= 227 * 1024, "dpm_correlate: h=%d w=%d nf=%d needs %zu B shared memory",
               h, w_max, nf, smem);

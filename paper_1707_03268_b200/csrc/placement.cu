@@ -17,13 +17,14 @@
 // Speed: each CTA owns a 32 x 32 tile of roots of one (image, component,
 // root level).  Per part it stages the S band its windows touch in shared
 // memory, runs the x pass for every band row at the 32 centre columns, then
-// the y pass for the 1024 roots.  Candidates are screened in FP32: with
-// E = 2^-20 * (max|S| + max pen_x + max pen_y) bounding the FP32 error of
-// every candidate value, a candidate more than 2E below the running winner
-// cannot beat it and one more than 2E above must; only candidates inside the
-// +-2E band are compared in FP64.  The scan order and the strict '>' rule are
-// those of the reference, so the winner is the reference's.
-//
+// the y pass for the 1024 roots.  Candidates are screened in FP32, branch
+// free: the scan keeps the running maximum m1 (first index on ties, strict
+// '>') and the best value m2 of all other candidates.  With
+// E2 = 2^-19 * (max|S| + max pen_x + max pen_y) at least twice the FP32 error
+// of any candidate value, m2 < m1 - E2 proves the FP32 winner is the unique
+// exact winner, whose value is then evaluated once in FP64; otherwise (ties,
+// near ties) the candidates within E2 of m1 are rescanned in FP64 in the
+// reference's order with strict '>'.
 // radius < 0 selects the unbounded generalised distance transform, realised
 // as the window of radius r* computed from the map's
 // range, beyond which no maximiser lies.  Jobs whose radius exceeds RCAP use
@@ -47,8 +48,6 @@ struct __align__(16) PlaceSmem {
   double xb[BAND_MAX * PT_W];            // x-pass exact values
   float x32[BAND_MAX * PT_W];            // x-pass values rounded to FP32
   short xdx[BAND_MAX * PT_W];            // x-pass argmax dx
-  float npx32[2 * RCAP + 1], npy32[2 * RCAP + 1];
-  double npx[2 * RCAP + 1], npy[2 * RCAP + 1];
 };
 
 __device__ __forceinline__ double pen(double c1, double c2, int d) {
@@ -75,17 +74,23 @@ __device__ __forceinline__ uint32_t pack_pos(int y, int x) {
   return ((uint32_t)(uint16_t)(int16_t)y << 16) | (uint32_t)(uint16_t)(int16_t)x;
 }
 
-// Screened strict-'>' update.  (v32, vexact-on-demand) against the winner.
-struct Winner {
-  float w32, hi, lo;
-  double wx;
-  bool wx_ok;
-  int idx;
+// Branch-free FP32 screen of one window (see file comment).
+struct Screen {
+  float m1, m2;
+  int i1;
 };
 
-__device__ __forceinline__ void win_init(Winner& w, int idx0) {
-  w.w32 = -INFINITY; w.hi = -INFINITY; w.lo = -INFINITY;
-  w.wx = -INFINITY; w.wx_ok = true; w.idx = idx0;
+__device__ __forceinline__ void screen_init(Screen& sc, int r) {
+  sc.m1 = -INFINITY;
+  sc.m2 = -INFINITY;
+  sc.i1 = -r;
+}
+
+__device__ __forceinline__ void screen_add(Screen& sc, float v, int d) {
+  const bool gt = v > sc.m1;
+  sc.m2 = fmaxf(sc.m2, fminf(sc.m1, v));
+  sc.i1 = gt ? d : sc.i1;
+  sc.m1 = fmaxf(sc.m1, v);
 }
 
 // Placement of one part for one root via direct global loads (any radius).
@@ -172,8 +177,8 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       continue;
     }
     const double mabs = fmax(fabs((double)vmax), fabs((double)vmin));
-    const float E2 = (float)(2.0 * ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, rxr) +
-                                         pen_absmax(pj.cdy, pj.cdyy, ryr), -20));
+    const float E2 = (float)ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, rxr) +
+                                  pen_absmax(pj.cdy, pj.cdyy, ryr), -19);
     // band: map rows / cols the windows of this tile can reach
     const int yb0 = pj.scale * ry_lo + pj.ay - ryr;
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * ryr;
@@ -181,42 +186,57 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * rxr;
 
     __syncthreads();  // previous part done with the band
-    for (int d = threadIdx.x; d <= 2 * RCAP; d += PT_THREADS) {
-      const int dd = d - RCAP;
-      const double px = pen(pj.cdx, pj.cdxx, dd), py = pen(pj.cdy, pj.cdyy, dd);
-      sh.npx[d] = -px; sh.npy[d] = -py;
-      sh.npx32[d] = (float)(-px); sh.npy32[d] = (float)(-py);
+    // stage the band with cp.async (all loads in flight), -inf outside the map
+    for (int r = warp; r < nrows; r += PT_THREADS / 32) {
+      const int y = yb0 + r;
+      const bool yok = y >= 0 && y < pj.Hp;
+      const float* srcrow = sm + (int64_t)y * pj.Wp;
+      for (int c = lane; c < ncols; c += 32) {
+        const int x = xb0 + c;
+        float* dst = sh.s + r * COLS_PITCH + c;
+        if (yok && x >= 0 && x < pj.Wp) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(srcrow + x));
+        } else {
+          *dst = -INFINITY;
+        }
+      }
     }
-    for (int e = threadIdx.x; e < nrows * ncols; e += PT_THREADS) {
-      const int r = e / ncols, c = e - r * ncols;
-      const int y = yb0 + r, x = xb0 + c;
-      float v = -INFINITY;
-      if (y >= 0 && y < pj.Hp && x >= 0 && x < pj.Wp) v = __ldg(sm + (int64_t)y * pj.Wp + x);
-      sh.s[r * COLS_PITCH + c] = v;
-    }
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
+    const float nax = (float)(-pj.cdxx), nbx = (float)(-pj.cdx);
+    const float nay = (float)(-pj.cdyy), nby = (float)(-pj.cdy);
     // x pass: band row r (warp-strided), centre column = lane
     for (int r = warp; r < nrows; r += PT_THREADS / 32) {
       const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + rxr;  // dx = 0
-      Winner w;
-      win_init(w, -rxr);
-      for (int dx = -rxr; dx <= rxr; ++dx) {
-        const float v = srow[dx] + sh.npx32[dx + RCAP];
-        if (v <= w.lo) continue;
-        if (v > w.hi) {
-          w.w32 = v; w.idx = dx; w.wx_ok = false;
-        } else {
-          const double vx = __dadd_rn((double)srow[dx], sh.npx[dx + RCAP]);
-          if (!w.wx_ok) { w.wx = __dadd_rn((double)srow[w.idx], sh.npx[w.idx + RCAP]); w.wx_ok = true; }
-          if (vx > w.wx) { w.wx = vx; w.w32 = v; w.idx = dx; }
+      Screen sc;
+      screen_init(sc, rxr);
+      float d = (float)(-rxr);
+      for (int dx = -rxr; dx <= rxr; ++dx, d += 1.f)
+        screen_add(sc, fmaf(fmaf(nax, d, nbx), d, srow[dx]), dx);
+      double xv;
+      int xi = sc.i1;
+      if (sc.m1 == -INFINITY) {  // no candidate inside the map: reference gives (-inf, -r)
+        xv = -INFINITY;
+        xi = -rxr;
+      } else if (sc.m2 >= sc.m1 - E2) {  // tie or near tie: exact rescan
+        const float lo = sc.m1 - E2;
+        xv = -INFINITY;
+        xi = -rxr;
+        d = (float)(-rxr);
+        for (int dx = -rxr; dx <= rxr; ++dx, d += 1.f) {
+          if (fmaf(fmaf(nax, d, nbx), d, srow[dx]) >= lo) {
+            const double e = __dadd_rn((double)srow[dx], -pen(pj.cdx, pj.cdxx, dx));
+            if (e > xv) { xv = e; xi = dx; }
+          }
         }
-        w.hi = w.w32 + E2; w.lo = w.w32 - E2;
+      } else {
+        xv = __dadd_rn((double)srow[xi], -pen(pj.cdx, pj.cdxx, xi));
       }
-      if (!w.wx_ok) w.wx = __dadd_rn((double)srow[w.idx], sh.npx[w.idx + RCAP]);
-      sh.xb[r * PT_W + lane] = w.wx;
-      sh.x32[r * PT_W + lane] = (float)w.wx;
-      sh.xdx[r * PT_W + lane] = (short)w.idx;
+      sh.xb[r * PT_W + lane] = xv;
+      sh.x32[r * PT_W + lane] = (float)xv;
+      sh.xdx[r * PT_W + lane] = (short)xi;
     }
     __syncthreads();
 
@@ -227,34 +247,40 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       if (!col_ok || iy >= hr) continue;
       const int ry = aj.ry0 + iy;
       const int r0 = pj.scale * (ry - ry_lo) + ryr;  // band row of dy = 0
-      Winner w;
-      win_init(w, -ryr);
-      for (int dy = -ryr; dy <= ryr; ++dy) {
-        const int rr = (r0 + dy) * PT_W + lane;
-        const float v = sh.x32[rr] + sh.npy32[dy + RCAP];
-        if (v <= w.lo) continue;
-        if (v > w.hi) {
-          w.w32 = v; w.idx = dy; w.wx_ok = false;
-        } else {
-          const double vx = __dadd_rn(sh.xb[rr], sh.npy[dy + RCAP]);
-          if (!w.wx_ok) {
-            w.wx = __dadd_rn(sh.xb[(r0 + w.idx) * PT_W + lane], sh.npy[w.idx + RCAP]);
-            w.wx_ok = true;
+      const float* xcol = sh.x32 + r0 * PT_W + lane;
+      const double* xbcol = sh.xb + r0 * PT_W + lane;
+      Screen sc;
+      screen_init(sc, ryr);
+      float d = (float)(-ryr);
+      for (int dy = -ryr; dy <= ryr; ++dy, d += 1.f)
+        screen_add(sc, fmaf(fmaf(nay, d, nby), d, xcol[dy * PT_W]), dy);
+      double best;
+      int bi = sc.i1;
+      if (sc.m1 == -INFINITY) {
+        best = -INFINITY;
+        bi = -ryr;
+      } else if (sc.m2 >= sc.m1 - E2) {
+        const float lo = sc.m1 - E2;
+        best = -INFINITY;
+        bi = -ryr;
+        d = (float)(-ryr);
+        for (int dy = -ryr; dy <= ryr; ++dy, d += 1.f) {
+          if (fmaf(fmaf(nay, d, nby), d, xcol[dy * PT_W]) >= lo) {
+            const double e = __dadd_rn(xbcol[dy * PT_W], -pen(pj.cdy, pj.cdyy, dy));
+            if (e > best) { best = e; bi = dy; }
           }
-          if (vx > w.wx) { w.wx = vx; w.w32 = v; w.idx = dy; }
         }
-        w.hi = w.w32 + E2; w.lo = w.w32 - E2;
+      } else {
+        best = __dadd_rn(xbcol[bi * PT_W], -pen(pj.cdy, pj.cdyy, bi));
       }
-      const int rr = (r0 + w.idx) * PT_W + lane;
-      if (!w.wx_ok) w.wx = __dadd_rn(sh.xb[rr], sh.npy[w.idx + RCAP]);
-      const int bdx = (w.w32 == -INFINITY) ? -rxr : sh.xdx[rr];
+      const int bdx = sh.xdx[(r0 + bi) * PT_W + lane];
       const int cy = pj.scale * ry + pj.ay, cx = pj.scale * rx + pj.ax;
-      tot[k] = __dadd_rn(tot[k], w.wx);
-      const uint32_t pk = pack_pos(cy + w.idx, cx + bdx);
+      tot[k] = __dadd_rn(tot[k], best);
+      const uint32_t pk = pack_pos(cy + bi, cx + bdx);
       if (p < DPM_MAX_PARTS) parts[k][p] = pk;
       const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
       if (aj.pos_off >= 0) pos[aj.pos_off + o] = pk;
-      if (aj.placed_off >= 0) placed[aj.placed_off + o] = w.wx;
+      if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
     }
   }
 

@@ -92,7 +92,7 @@ def test_tile_shapes():
     tw, th = ctypes.c_int(), ctypes.c_int()
     assert lib.dpm_correlate_tile_shape(6, 48, ctypes.byref(tw), ctypes.byref(th)) == 6
     assert (tw.value, th.value) == (32, 8)
-    assert lib.dpm_correlate_tile_shape(6, 6, ctypes.byref(tw), ctypes.byref(th)) == 4
-    assert th.value == 32
+    assert lib.dpm_correlate_tile_shape(6, 6, ctypes.byref(tw), ctypes.byref(th)) == 2
+    assert th.value == 16
     assert lib.dpm_correlate_tile_shape(9, 2, ctypes.byref(tw), ctypes.byref(th)) < 0
     assert th.value == 8  # generic kernel tile
