@@ -45,6 +45,22 @@ __device__ __forceinline__ void load_g(float (&g)[NF], const float* p) {
   }
 }
 
+// Packed FP32 pair (one 64-bit register pair) for FFMA2: sm_100a issues
+// fma.rn.f32x2 as a single instruction at the scalar FFMA's FLOP rate, which
+// halves the FMA issue slots of the outer-product loop.  A scalar first
+// operand packed as {c, c} folds into FFMA2's broadcast operand (no MOV).
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ void ffma2(unsigned long long& acc, float a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(pack2(a, a)), "l"(b));
+}
+
 struct CorrArgs {
   const float* P;
   const float* G;
@@ -78,15 +94,20 @@ __device__ __forceinline__ void stage_p(float* dst, const CorrArgs& a, const dpm
   const int per_plane = TROWS * tcols;
   const int64_t plane = (int64_t)job.H * job.pitch;
   const float* pbase = a.P + job.p_off + (int64_t)(job.chan_off + rc) * plane;
-  for (int e = threadIdx.x; e < nr * per_plane; e += blockDim.x) {
-    const int r = e / per_plane, rem = e - r * per_plane;
-    const int row = rem / tcols, col = rem - row * tcols;
-    const int gy = y0 + row, gx = x0 + col;
-    const bool ok = gy < job.H && gx < job.W;
-    const float* src = ok ? pbase + r * plane + (int64_t)gy * job.pitch + gx : a.P;
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + (r * TROWS + row) * TPITCH + col);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src),
-                 "r"(ok ? 4 : 0));
+  (void)per_plane;
+  const int nwarps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int rr = threadIdx.x >> 5; rr < nr * TROWS; rr += nwarps) {
+    const int r = rr / TROWS, row = rr - r * TROWS;
+    const int gy = y0 + row;
+    const float* srow = pbase + r * plane + (int64_t)gy * job.pitch;
+    float* drow = dst + (r * TROWS + row) * TPITCH;
+    for (int col = lane; col < tcols; col += 32) {
+      const int gx = x0 + col;
+      const bool ok = gy < job.H && gx < job.W;
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(drow + col);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa),
+                   "l"(ok ? srow + gx : a.P), "r"(ok ? 4 : 0));
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::);
 }
@@ -114,8 +135,8 @@ corr_kernel(const CorrArgs a) {
   const int TROWS = TY + FH - 1;
   const int TPITCH = 32 + a.w_max - 1;
   const int PBUF = (K2_RCH * TROWS * TPITCH + 3) & ~3;
-  float* sPb[2] = {smem, smem + PBUF};                   // [RCH][TROWS][TPITCH] x 2
-  float* sG = smem + 2 * PBUF;                           // [FH][w][RCH][nf_pad]
+  // P double buffer [2][RCH][TROWS][TPITCH] at smem, core [FH][w][RCH][nf_pad] after it
+  float* sG = smem + 2 * PBUF;
   // one rank chunk per tile: prefetch the next tile's P during this one
   const bool pipelined = a.R_max <= K2_RCH;
 
@@ -125,7 +146,7 @@ corr_kernel(const CorrArgs a) {
   if (pipelined && blockIdx.x < a.ntiles) {
     const dpm_corr_tile t0 = a.tiles[blockIdx.x];
     const dpm_corr_job j0 = a.jobs[t0.job];
-    stage_p(sPb[0], a, j0, 0, j0.R, t0.ty * TY, t0.tx * 32, TROWS, TPITCH);
+    stage_p(smem, a, j0, 0, j0.R, t0.ty * TY, t0.tx * 32, TROWS, TPITCH);
   }
   for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
     const dpm_corr_tile tile = a.tiles[t];
@@ -134,22 +155,24 @@ corr_kernel(const CorrArgs a) {
     const int y0 = tile.ty * TY, x0 = tile.tx * 32;
     const int w = job.w, nfp = job.nf_pad;
 
-    float acc[MP][NF];
+    constexpr int NP = NF / 2;  // filter pairs (FFMA2 lanes)
+    unsigned long long acc[MP][NP];
 #pragma unroll
     for (int p = 0; p < MP; ++p)
 #pragma unroll
-      for (int f = 0; f < NF; ++f) acc[p][f] = 0.f;
+      for (int f = 0; f < NP; ++f) acc[p][f] = 0ull;
 
     for (int rc = 0; rc < job.R; rc += K2_RCH) {
       const int nr = min(K2_RCH, job.R - rc);
-      float* sP = sPb[pipelined ? (it & 1) : 0];
+      float* sP = smem + ((pipelined && (it & 1)) ? PBUF : 0);
       __syncthreads();  // every warp is done with the buffers about to be refilled
       if (pipelined) {
         const int tn = t + gridDim.x;
         if (tn < a.ntiles) {
           const dpm_corr_tile nt = a.tiles[tn];
           const dpm_corr_job nj = a.jobs[nt.job];
-          stage_p(sPb[(it + 1) & 1], a, nj, 0, nj.R, nt.ty * TY, nt.tx * 32, TROWS, TPITCH);
+          stage_p(smem + (((it + 1) & 1) ? PBUF : 0), a, nj, 0, nj.R, nt.ty * TY, nt.tx * 32, TROWS,
+                  TPITCH);
           asm volatile("cp.async.wait_group 1;\n" ::);
         } else {
           asm volatile("cp.async.wait_group 0;\n" ::);
@@ -179,10 +202,13 @@ corr_kernel(const CorrArgs a) {
           for (int i = 0; i < FH; ++i) {
             float g[NF];
             load_g<NF>(g, gp + i * gstride_i);
+            unsigned long long g2[NP];
+#pragma unroll
+            for (int f = 0; f < NP; ++f) g2[f] = pack2(g[2 * f], g[2 * f + 1]);
 #pragma unroll
             for (int p = 0; p < MP; ++p)
 #pragma unroll
-              for (int f = 0; f < NF; ++f) acc[p][f] = fmaf(col[p + i], g[f], acc[p][f]);
+              for (int f = 0; f < NP; ++f) ffma2(acc[p][f], col[p + i], g2[f]);
           }
         }
       }
@@ -191,6 +217,11 @@ corr_kernel(const CorrArgs a) {
     // epilogue: coalesced stores (lane = x), optional per-map range fold
     const int x = x0 + lane;
     const int yb = y0 + wy * MP;
+    float out[MP][NF];
+#pragma unroll
+    for (int p = 0; p < MP; ++p)
+#pragma unroll
+      for (int f = 0; f < NP; ++f) unpack2(acc[p][f], out[p][2 * f], out[p][2 * f + 1]);
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int fg = wf * NF + f;
@@ -201,9 +232,9 @@ corr_kernel(const CorrArgs a) {
         for (int p = 0; p < MP; ++p) {
           const int y = yb + p;
           if (x < wo && y < ho) {
-            dst[(int64_t)y * wo + x] = acc[p][f];
-            vmax = fmaxf(vmax, acc[p][f]);
-            vmin = fminf(vmin, acc[p][f]);
+            dst[(int64_t)y * wo + x] = out[p][f];
+            vmax = fmaxf(vmax, out[p][f]);
+            vmin = fminf(vmin, out[p][f]);
           }
         }
       }
