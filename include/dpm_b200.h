@@ -110,6 +110,20 @@ int dpm_correlate(const float* P, const float* G, float* S, const dpm_corr_job* 
                   const dpm_corr_tile* tiles, int ntiles, int h, int nf, int R,
                   int w_max, uint32_t* ranges, void* stream);
 
+/* K2 on tcgen05 (kind::tf32, 3xTF32 split) for one filter group:
+ * M = 128 output positions of one row, N = nf filters (padded to 16),
+ * K = 8 ranks per tap; A is the staged input row shifted per tap, B the
+ * resident core.  Each work item is a 128-wide column strip
+ * (dpm_corr_tile.tx = strip index) of one job, processed top to bottom.
+ * `Gtc` is the core in the tensor layout [h*w][R/4][2N][4]: rows < N hold
+ * the tf32-truncated filter values, rows >= N the exact remainders.
+ * Requirements: R % 8 == 0, 1 <= nf <= 64, h + 2 <= 16 and the returned
+ * shared-memory size <= 227 KB. */
+size_t dpm_correlate_tc_smem(int h, int w, int R, int nf);
+int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
+                     const dpm_corr_tile* strips, int nstrips, int h, int w, int R, int nf,
+                     uint32_t* ranges, void* stream);
+
 /* Initialise `n` range slots to (-inf, +inf). */
 int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
 

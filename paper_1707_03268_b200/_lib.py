@@ -62,6 +62,8 @@ _SIGNATURES = {
     "dpm_correlate_tile_shape": (_i32, [_i32, _i32, _vp, _vp]),
     "dpm_correlate": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "dpm_ranges_init": (_i32, [_vp, _i32, _vp]),
+    "dpm_correlate_tc_smem": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
+    "dpm_correlate_tc": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
     "dpm_assemble": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32, _vp,
                             _vp]),

@@ -1,0 +1,369 @@
+// K2 on the 5th-generation tensor cores: shortened correlation as an
+// implicit GEMM on tcgen05 (kind::tf32, 3xTF32 split for FP32 accuracy).
+//
+//   S_f[y][x] = sum_{i<h, j<w, r<R} G[i][j][r][f] * P[r][y+i][x+j]
+//
+// GEMM shape per MMA: M = 128 consecutive output positions of one output
+// row, N = filters, K = 8 ranks of one tap (i, j).  The A operand of tap
+// (i, j) is a plain shifted window of the staged input row y+i: in the
+// K-major no-swizzle canonical layout each position is one 16-byte row per
+// 4-rank quad, so shifting by j positions is just +16*j bytes on the smem
+// descriptor's start address -- no im2col copy.
+//
+// 3xTF32: A = A_hi + A_lo, B = B_hi + B_lo with hi = fp32 truncated to tf32
+// (low 13 mantissa bits cleared) and lo = the exact remainder; per tap
+//   MMA1: D[:, 0:2N] += A_hi x [B_hi | B_lo]      (N2 = 2N)
+//   MMA2: D[:, 0:N]  += A_lo x  B_hi
+// and the epilogue adds D[:, f] + D[:, N+f]; the dropped A_lo*B_lo term is
+// ~2^-22 relative, far inside the 1e-5 parity bar.
+//
+// Warp roles (256 threads, one persistent CTA per SM):
+//   warp 0      : TMEM allocation; one elected lane issues tcgen05.mma
+//   warps 1..3  : producers -- stream input rows of P (planar fp32) into an
+//                 smem ring as quad-interleaved hi/lo tf32 (mbarrier full/empty)
+//   warps 4..7  : epilogue -- tcgen05.ld the accumulator of an output row,
+//                 add the split halves, store S (coalesced per filter) and
+//                 fold per-map extrema for the placement kernel
+// Each CTA walks 128-wide column strips of levels top to bottom; every input
+// row is staged once per strip.  The group's core B (hi | lo) stays resident
+// in shared memory for the whole launch.
+#include "common.cuh"
+
+namespace dpm {
+
+constexpr int TC_M = 128;
+constexpr int TC_THREADS = 256;
+constexpr int TC_PRODUCERS = 3;  // warps 1..3
+constexpr int TC_MAX_RING = 16;
+constexpr int TC_MAX_ACC = 4;
+
+struct TcArgs {
+  const float* P;
+  const float* Gtc;  // [h*w][R/4][2N][4] fp32: rows < N hi, rows >= N lo
+  float* S;
+  const dpm_corr_job* jobs;
+  const dpm_corr_tile* strips;  // (job, -, strip index)
+  int nstrips;
+  int h, w, R, N;               // N: padded filter count (multiple of 16)
+  int ring, acc_cols, nacc;
+  uint32_t* ranges;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Wait for the phase with parity `parity`; traps (instead of hanging the GPU)
+// if it has not completed after ~20 s, which can only be a pipeline bug.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (int spin = 0; spin < 2000 && !done; ++spin) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t"
+        "}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(10000000u)
+        : "memory");
+  }
+  if (!done) asm volatile("trap;");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// K-major, no-swizzle smem matrix descriptor (SM100 UMMA):
+// start >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46), version 1 at 46.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+__device__ __forceinline__ float tf32_hi(float a) {
+  return __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+}
+
+template <int NMAX>  // max filters handled by the epilogue registers
+__global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nq = a.R >> 2;                       // rank quads
+  const int taps = a.h * a.w;
+  const int tcols = TC_M + a.w - 1;
+  const uint32_t b_bytes = (uint32_t)taps * nq * (2 * a.N) * 16u;
+  const uint32_t slot_bytes = 2u * nq * tcols * 16u;  // hi then lo
+  unsigned char* sB = smem;
+  unsigned char* sA = smem + ((b_bytes + 1023u) & ~1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + ((a.ring * slot_bytes + 15u) & ~15u));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + TC_MAX_RING;
+  uint64_t* tfull = bars + 2 * TC_MAX_RING;
+  uint64_t* tempty = tfull + TC_MAX_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_MAX_ACC);
+
+  // ---- setup: core B -> smem (all threads), barriers, TMEM
+  {
+    const float4* src = reinterpret_cast<const float4*>(a.Gtc);
+    float4* dst = reinterpret_cast<float4*>(sB);
+    for (uint32_t e = threadIdx.x; e < b_bytes / 16u; e += TC_THREADS) dst[e] = __ldg(src + e);
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.ring; ++s) {
+      mbar_init(full + s, TC_PRODUCERS);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < a.nacc; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B visible to the tensor core
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // =================== MMA issuer ===================
+    const uint32_t idesc1 = idesc_tf32(2 * a.N), idesc2 = idesc_tf32(a.N);
+    const uint32_t lboA = (uint32_t)tcols * 16u, lboB = (uint32_t)(2 * a.N) * 16u;
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+    uint32_t q_glob = 0, row_glob = 0;
+    for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
+      const dpm_corr_job job = a.jobs[a.strips[st].job];
+      const int ho = job.H - a.h + 1;
+      for (int y = 0; y < ho; ++y, ++row_glob) {
+        const int b = row_glob % a.nacc;
+        mbar_wait(tempty + b, ((row_glob / a.nacc) & 1) ^ 1);
+        for (int rr = (y == 0 ? 0 : a.h - 1); rr < a.h; ++rr) {
+          const uint32_t q = q_glob + y + rr;
+          mbar_wait(full + q % a.ring, (q / a.ring) & 1);
+        }
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
+          for (int i = 0; i < a.h; ++i) {
+            const uint32_t slot = (q_glob + y + i) % a.ring;
+            const uint32_t a_hi = sA0 + slot * slot_bytes;
+            const uint32_t a_lo = a_hi + (uint32_t)nq * lboA;
+            for (int j = 0; j < a.w; ++j) {
+              const uint32_t tap_b = sB0 + (uint32_t)(i * a.w + j) * nq * lboB;
+              for (int kc = 0; kc < nq; kc += 2) {
+                const uint32_t off = (uint32_t)kc * lboA + (uint32_t)j * 16u;
+                const uint64_t da_hi = umma_desc(a_hi + off, lboA, 128);
+                const uint64_t da_lo = umma_desc(a_lo + off, lboA, 128);
+                const uint64_t db = umma_desc(tap_b + (uint32_t)kc * lboB, lboB, 128);
+                mma_tf32(d, da_hi, db, idesc1, (i | j | kc) != 0);
+                mma_tf32(d, da_lo, db, idesc2, 1);
+              }
+            }
+          }
+          tc_commit(tfull + b);                          // accumulator ready
+          tc_commit(empty + (q_glob + y) % a.ring);      // input row y no longer needed
+        }
+        __syncwarp();
+      }
+      if (lane == 0)
+        for (int rr = ho; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
+      __syncwarp();
+      q_glob += job.H;
+    }
+  } else if (warp <= TC_PRODUCERS) {
+    // =================== producers ===================
+    const int pt = threadIdx.x - 32;  // 0..95
+    uint32_t q_glob = 0;
+    for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
+      const dpm_corr_tile strip = a.strips[st];
+      const dpm_corr_job job = a.jobs[strip.job];
+      const int x0 = strip.tx * TC_M;
+      const int64_t plane = (int64_t)job.H * job.pitch;
+      const float* pbase = a.P + job.p_off + (int64_t)job.chan_off * plane;
+      for (int q = 0; q < job.H; ++q, ++q_glob) {
+        const uint32_t slot = q_glob % a.ring;
+        mbar_wait(empty + slot, ((q_glob / a.ring) & 1) ^ 1);
+        float4* hi = reinterpret_cast<float4*>(sA + slot * slot_bytes);
+        float4* lo = hi + nq * tcols;
+        const float* prow = pbase + (int64_t)q * job.pitch;
+        for (int e = pt; e < nq * tcols; e += 32 * TC_PRODUCERS) {
+          const int quad = e / tcols, c = e - quad * tcols;
+          const int x = x0 + c;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (x < job.W) {
+            const float* p = prow + (int64_t)(4 * quad) * plane + x;
+            v.x = __ldg(p);
+            v.y = __ldg(p + plane);
+            v.z = __ldg(p + 2 * plane);
+            v.w = __ldg(p + 3 * plane);
+          }
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          hi[e] = h;
+          lo[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full + slot);
+      }
+    }
+  } else {
+    // =================== epilogue ===================
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter ..
+    uint32_t row_glob = 0;
+    for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
+      const dpm_corr_tile strip = a.strips[st];
+      const dpm_corr_job job = a.jobs[strip.job];
+      const int ho = job.H - a.h + 1, wo = job.W - a.w + 1;
+      const int x = strip.tx * TC_M + quarter * 32 + lane;
+      float vmax[NMAX], vmin[NMAX];
+#pragma unroll
+      for (int f = 0; f < NMAX; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
+      for (int y = 0; y < ho; ++y, ++row_glob) {
+        const int b = row_glob % a.nacc;
+        mbar_wait(tfull + b, (row_glob / a.nacc) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.acc_cols);
+        float* dst = a.S + job.s_off + (int64_t)y * wo + x;
+        // 16 filters at a time: hi-half columns [fc, fc+16) and lo-half [N+fc, ...)
+#pragma unroll
+        for (int fc = 0; fc < NMAX; fc += 16) {
+          if (fc < a.N) {
+            float vh[16], vl[16];
+            tmem_ld16(taddr + fc, vh);
+            tmem_ld16(taddr + a.N + fc, vl);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int f = fc + k;
+              if (f < job.nf && x < wo) {
+                const float sv = vh[k] + vl[k];
+                dst[(int64_t)f * ho * wo] = sv;
+                vmax[f] = fmaxf(vmax[f], sv);
+                vmin[f] = fminf(vmin[f], sv);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + b);
+      }
+      if (a.ranges != nullptr && job.range_idx >= 0) {
+#pragma unroll
+        for (int f = 0; f < NMAX; ++f) {
+          if (f >= job.nf) break;
+          float mx = vmax[f], mn = vmin[f];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          }
+          if (lane == 0 && mx >= mn) {
+            atomicMax(a.ranges + 2 * (job.range_idx + f), float_key(mx));
+            atomicMin(a.ranges + 2 * (job.range_idx + f) + 1, float_key(mn));
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+}  // namespace dpm
+
+using namespace dpm;
+
+extern "C" size_t dpm_correlate_tc_smem(int h, int w, int R, int nf) {
+  const int N = (nf + 15) & ~15;
+  const int nq = R / 4;
+  const size_t b = (size_t)h * w * nq * 2 * N * 16;
+  const int ring = h + 2 <= TC_MAX_RING ? h + 2 : TC_MAX_RING;
+  const size_t slot = 2ull * nq * (TC_M + w - 1) * 16;
+  return ((b + 1023) & ~(size_t)1023) + ((ring * slot + 15) & ~(size_t)15) +
+         (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
+}
+
+extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
+                                const dpm_corr_tile* strips, int nstrips, int h, int w, int R,
+                                int nf, uint32_t* ranges, void* stream) {
+  DPM_REQUIRE(P && Gtc && S && jobs && strips, "dpm_correlate_tc: null pointer");
+  DPM_REQUIRE(R % 8 == 0 && R >= 8, "dpm_correlate_tc: R=%d must be a multiple of 8", R);
+  DPM_REQUIRE(nf >= 1 && nf <= 64, "dpm_correlate_tc: nf=%d outside [1, 64]", nf);
+  DPM_REQUIRE(h >= 1 && w >= 1 && h + 2 <= TC_MAX_RING, "dpm_correlate_tc: filter %dx%d", h, w);
+  if (nstrips == 0) return DPM_OK;
+  const int N = (nf + 15) & ~15;
+  const size_t smem = dpm_correlate_tc_smem(h, w, R, nf);
+  DPM_REQUIRE(smem <= 227 * 1024, "dpm_correlate_tc: needs %zu B shared memory", smem);
+  int dev = 0, sms = 148;
+  DPM_CUDA(cudaGetDevice(&dev));
+  DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  TcArgs a{P, Gtc, S, jobs, strips, nstrips, h, w, R, N, h + 2, 0, 0, ranges};
+  a.acc_cols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
+  a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
+  void (*fn)(const TcArgs) = N <= 16 ? corr_tc_kernel<16>
+                             : N <= 32 ? corr_tc_kernel<32>
+                             : N <= 48 ? corr_tc_kernel<48>
+                                       : corr_tc_kernel<64>;
+  DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = nstrips < sms ? nstrips : sms;
+  fn<<<grid, TC_THREADS, smem, as_stream(stream)>>>(a);
+  DPM_LAUNCHED("corr_tc_kernel");
+  return DPM_OK;
+}

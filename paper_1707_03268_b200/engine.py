@@ -98,7 +98,8 @@ class Plan:
     """
 
     def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
-                 outputs=("totals", "positions"), max_dets=0, device=None):
+                 outputs=("totals", "positions"), max_dets=0, device=None, tensor_cores=True,
+                 tc_min_width=64):
         import torch
 
         require_cuda()
@@ -115,6 +116,8 @@ class Plan:
         self.assemblies = list(assemblies)
         self.outputs = set(outputs)
         self.max_dets = int(max_dets)
+        self.tensor_cores = bool(tensor_cores)
+        self.tc_min_width = int(tc_min_width)
         for k, f in enumerate(self.filters):
             if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
                 raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
@@ -187,8 +190,24 @@ class Plan:
         for off, block in core_blocks:
             self._core_host[off:off + block.size] = block.ravel()
 
+        # tensor-core eligible groups (tcgen05 3xTF32 path) and their cores in
+        # the [tap][R/4][2N][4] hi|lo layout
+        tca = _Arena()
+        self.tc_core_off = {}
+        tc_blocks = []
+        for _, fl in self.groups:
+            if fl in self.tc_core_off or not self._tc_eligible(fl):
+                continue
+            block = _tc_core([self.filters[f].core for f in fl])
+            self.tc_core_off[fl] = tca.take(block.size, align=64)
+            tc_blocks.append((self.tc_core_off[fl], block))
+        self._tc_core_host = np.zeros(max(tca.size, 4), dtype=np.float32)
+        for off, block in tc_blocks:
+            self._tc_core_host[off:off + block.size] = block.ravel()
+
         # S arena, K2 jobs, tiles, range slots
         sa = _Arena()
+        tc_classes = {}
         self.map_off = {}  # (image, level, filt) -> float offset
         self.map_shape = {}
         self.range_slot = {}
@@ -213,6 +232,11 @@ class Plan:
                 jobs.append((img * self.p_image_stride + self.p_level_off[k], s_off,
                              self.core_off[fl], H, W, self.pitch[k], fd.chan_off, fd.h, fd.w,
                              fd.R, len(fl), _round_up(len(fl), 8), 0, rng, 0))
+                if fl in self.tc_core_off and wo >= self.tc_min_width:
+                    tcc = tc_classes.setdefault(fl, [])
+                    for sx in range((wo + 127) // 128):
+                        tcc.append((jid, 0, sx, ho))
+                    continue
                 tw, th = self._tile_shape(fd.h, len(fl))
                 cls = classes.setdefault((fd.h, len(fl)), {"tiles": [], "w_max": 1, "R": 1})
                 cls["w_max"] = max(cls["w_max"], fd.w)
@@ -228,6 +252,13 @@ class Plan:
             # tiles sorted by core so persistent CTAs keep it resident
             tl = sorted(cls["tiles"], key=lambda t: (jobs[t[0]][2], t[0], t[1], t[2]))
             self._classes.append((h, nf, cls["R"], cls["w_max"], np.array(tl, dtype=_lib.CORR_TILE)))
+
+        self._tc_classes = []
+        for fl, strips in sorted(tc_classes.items()):
+            strips.sort(key=lambda t: -t[3])  # tall strips first (static round robin)
+            fd = self.filters[fl[0]]
+            arr = np.array([(j, 0, sx, 0) for j, _, sx, _ in strips], dtype=_lib.CORR_TILE)
+            self._tc_classes.append((fd.h, fd.w, fd.R, len(fl), self.tc_core_off[fl], arr))
 
         # K1 jobs
         pj = [(img * self.x_image_stride + self.x_level_off[k],
@@ -278,6 +309,14 @@ class Plan:
             _lib.table_ptr(self._place_jobs), len(self._place_jobs)), "assembly")
         self.total_size, self.pos_size, self.placed_size = ta.size, oa.size, pla.size
 
+    def _tc_eligible(self, fl):
+        if not self.tensor_cores:
+            return False
+        fd = self.filters[fl[0]]
+        if fd.R % 8 or not (9 <= len(fl) <= 64) or fd.h + 2 > 16:
+            return False
+        return _lib.lib().dpm_correlate_tc_smem(fd.h, fd.w, fd.R, len(fl)) <= 227 * 1024
+
     _tile_cache = {}
 
     def _tile_shape(self, h, nf):
@@ -298,6 +337,8 @@ class Plan:
         self.proj_jobs_d = upload_table(self._proj_jobs, dev)
         self.corr_jobs_d = upload_table(self._corr_jobs, dev)
         self.class_tiles_d = [upload_table(c[4], dev) for c in self._classes]
+        self.Gtc = t.from_numpy(self._tc_core_host).to(dev)
+        self.tc_strips_d = [upload_table(c[5], dev) for c in self._tc_classes]
         self.place_jobs_d = upload_table(self._place_jobs, dev)
         self.asm_jobs_d = upload_table(self._asm_jobs, dev)
         self.X = t.empty(self.n_images * self.x_image_stride, dtype=t.float32, device=dev)
@@ -341,6 +382,10 @@ class Plan:
             if self.n_ranges:
                 _lib.check(lib.dpm_ranges_init(ptr(self.ranges), self.n_ranges, s), "ranges")
             rng = ptr(self.ranges) if self.n_ranges else None
+            for (h, w, R, nf, goff, strips), strips_d in zip(self._tc_classes, self.tc_strips_d):
+                _lib.check(lib.dpm_correlate_tc(ptr(self.P), ptr(self.Gtc) + 4 * goff, ptr(self.S),
+                                                ptr(self.corr_jobs_d), ptr(strips_d), len(strips),
+                                                h, w, R, nf, rng, s), "correlate_tc")
             for (h, nf, R, w_max, tiles), tiles_d in zip(self._classes, self.class_tiles_d):
                 _lib.check(lib.dpm_correlate(ptr(self.P), ptr(self.G), ptr(self.S),
                                              ptr(self.corr_jobs_d), ptr(tiles_d), len(tiles), h,
@@ -408,6 +453,21 @@ class Plan:
 
     def k1_bytes(self):
         return sum(4 * (self.L + self.Rtot) * H * W for H, W in self.levels)
+
+
+def _tc_core(cores):
+    """Cores of one group in the tcgen05 B layout [h*w][R/4][2N][4]: rows < N
+    the tf32-truncated values, rows >= N the exact fp32 remainders."""
+    core = np.stack([np.asarray(c, np.float32) for c in cores], axis=-1)  # (h, w, R, nf)
+    h, w, R, nf = core.shape
+    N = _round_up(nf, 16)
+    hi = (core.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    lo = (core - hi).astype(np.float32)
+    out = np.zeros((h * w, R // 4, 2 * N, 4), dtype=np.float32)
+    for src, base in ((hi, 0), (lo, N)):
+        t = src.reshape(h * w, R // 4, 4, nf).transpose(0, 1, 3, 2)  # (tap, quad, nf, 4)
+        out[:, :, base:base + nf, :] = t
+    return out
 
 
 def unpack_positions(packed):

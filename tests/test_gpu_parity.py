@@ -380,3 +380,30 @@ def test_tau_compaction_matches_totals():
         rec = res[(int(d["level"]), int(d["component"]))]
         ry0, _, rx0, _ = rec["rect"]
         assert d["score"] == rec["scores"][d["ry"] - ry0, d["rx"] - rx0]
+
+
+def test_tensor_core_correlation_matches_oracle_and_ffma():
+    """tcgen05 3xTF32 K2 path: same maps as the oracle and the FFMA path."""
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    rng = np.random.default_rng(11)
+    for H, W, nf, h, w, R in [(40, 300, 48, 6, 6, 8), (23, 130, 16, 6, 6, 8),
+                              (17, 200, 33, 5, 7, 8), (12, 70, 64, 3, 4, 8)]:
+        level = rng.random((H, W, 32)).astype(np.float32)
+        C = rng.normal(size=(32, R)).astype(np.float32)
+        cores = [rng.normal(0, 0.05, (h, w, R)).astype(np.float32) for _ in range(nf)]
+        plans = []
+        for tc in (True, False):
+            plan = Plan(32, [(H, W)], C, [FilterDef(c) for c in cores],
+                        apps=[(0, f) for f in range(nf)], outputs=(), tensor_cores=tc)
+            assert bool(plan._tc_classes) == tc
+            plan.load_levels(0, [level])
+            plan.run(stages=("project", "correlate"))
+            plans.append(plan)
+        P = O.project(level, C.astype(np.float64))
+        for f in range(nf):
+            ref = O.correlate3_full(P, cores[f])
+            g_tc = plans[0].map(0, 0, f).double().cpu().numpy()
+            g_ff = plans[1].map(0, 0, f).double().cpu().numpy()
+            assert_map_close(g_tc, ref, f"tc {H}x{W} filter {f}")
+            assert_map_close(g_tc, g_ff, f"tc vs ffma {H}x{W} filter {f}")
