@@ -127,11 +127,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t"
+      "}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ float tf32_hi(float a) {
   return __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
 }
 
-template <int NMAX>  // max filters handled by the epilogue registers
+// NMAX: max filters held by the epilogue registers.  FH, FW > 0: filter
+// extent fixed at compile time (R == 8), fully unrolled MMA issue.
+template <int NMAX, int FH, int FW>
 __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -157,7 +171,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.ring; ++s) {
-      mbar_init(full + s, TC_PRODUCERS);
+      mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
     for (int b = 0; b < a.nacc; ++b) {
@@ -180,9 +194,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
 
   if (warp == 0) {
     // =================== MMA issuer ===================
+    // The whole warp walks the loop (warp-uniform descriptors live in uniform
+    // registers); one elected lane issues.  A descriptor differs from the
+    // base only in its 14-bit start-address field, so per tap it is the base
+    // plus (byte offset >> 4).
     const uint32_t idesc1 = idesc_tf32(2 * a.N), idesc2 = idesc_tf32(a.N);
     const uint32_t lboA = (uint32_t)tcols * 16u, lboB = (uint32_t)(2 * a.N) * 16u;
-    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+    const uint64_t dA0 = umma_desc(smem_u32(sA), lboA, 128);
+    const uint64_t dB0 = umma_desc(smem_u32(sB), lboB, 128);
+    const uint32_t lo_step = (uint32_t)nq * lboA >> 4;   // hi -> lo plane block
+    const uint32_t slot_step = slot_bytes >> 4;
+    const uint32_t tap_step = (uint32_t)nq * lboB >> 4;
+    const uint32_t kcA = 2u * lboA >> 4, kcB = 2u * lboB >> 4;
     uint32_t q_glob = 0, row_glob = 0;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
@@ -195,37 +218,60 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
           mbar_wait(full + q % a.ring, (q / a.ring) & 1);
         }
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
+        const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
+        if constexpr (FH > 0) {
+          // compile-time taps: every descriptor is a row base + immediate
+          uint64_t da_row[FH];
+#pragma unroll
+          for (int i = 0; i < FH; ++i) da_row[i] = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
+          if (elect_one()) {
+#pragma unroll
+            for (int i = 0; i < FH; ++i)
+#pragma unroll
+              for (int j = 0; j < FW; ++j) {
+                const uint64_t ahi = da_row[i] + (uint32_t)j;
+                const uint64_t bb = dB0 + (uint32_t)((i * FW + j) * 2) * (uint32_t)(lboB >> 4);
+                mma_tf32(d, ahi, bb, idesc1, (i | j) != 0);
+                mma_tf32(d, ahi + lo_step, bb, idesc2, 1);
+              }
+          }
+          __syncwarp();
+        } else {
+          uint64_t db = dB0;
           for (int i = 0; i < a.h; ++i) {
-            const uint32_t slot = (q_glob + y + i) % a.ring;
-            const uint32_t a_hi = sA0 + slot * slot_bytes;
-            const uint32_t a_lo = a_hi + (uint32_t)nq * lboA;
-            for (int j = 0; j < a.w; ++j) {
-              const uint32_t tap_b = sB0 + (uint32_t)(i * a.w + j) * nq * lboB;
+            const uint64_t da_row = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
+            for (int j = 0; j < a.w; ++j, db += tap_step) {
+              const uint64_t da = da_row + (uint32_t)j;
               for (int kc = 0; kc < nq; kc += 2) {
-                const uint32_t off = (uint32_t)kc * lboA + (uint32_t)j * 16u;
-                const uint64_t da_hi = umma_desc(a_hi + off, lboA, 128);
-                const uint64_t da_lo = umma_desc(a_lo + off, lboA, 128);
-                const uint64_t db = umma_desc(tap_b + (uint32_t)kc * lboB, lboB, 128);
-                mma_tf32(d, da_hi, db, idesc1, (i | j | kc) != 0);
-                mma_tf32(d, da_lo, db, idesc2, 1);
+                const uint64_t ahi = da + (uint32_t)(kc >> 1) * kcA;
+                const uint64_t bb = db + (uint32_t)(kc >> 1) * kcB;
+                if (elect_one()) {
+                  mma_tf32(d, ahi, bb, idesc1, (i | j | kc) != 0);
+                  mma_tf32(d, ahi + lo_step, bb, idesc2, 1);
+                }
+                __syncwarp();
               }
             }
           }
-          tc_commit(tfull + b);                          // accumulator ready
-          tc_commit(empty + (q_glob + y) % a.ring);      // input row y no longer needed
+        }
+        if (elect_one()) {
+          tc_commit(tfull + b);                      // accumulator ready
+          tc_commit(empty + (q_glob + y) % a.ring);  // input row y no longer needed
         }
         __syncwarp();
       }
-      if (lane == 0)
+      if (elect_one())
         for (int rr = ho; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
       __syncwarp();
       q_glob += job.H;
     }
   } else if (warp <= TC_PRODUCERS) {
     // =================== producers ===================
-    const int pt = threadIdx.x - 32;  // 0..95
+    // Producer warp p stages input rows q = p, p+3, ... of every strip: each
+    // lane issues all of its (up to PQ) quad-column loads before converting,
+    // so one row costs one memory latency, and three rows are in flight.
+    constexpr int PQ = 10;  // quad-columns per lane: 2 quads x (128 + w - 1) <= 320
+    const int pw = warp - 1;
     uint32_t q_glob = 0;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_tile strip = a.strips[st];
@@ -233,31 +279,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
       const int x0 = strip.tx * TC_M;
       const int64_t plane = (int64_t)job.H * job.pitch;
       const float* pbase = a.P + job.p_off + (int64_t)job.chan_off * plane;
-      for (int q = 0; q < job.H; ++q, ++q_glob) {
-        const uint32_t slot = q_glob % a.ring;
-        mbar_wait(empty + slot, ((q_glob / a.ring) & 1) ^ 1);
+      const int nelem = nq * tcols;
+      for (int q = pw; q < job.H; q += TC_PRODUCERS) {
+        const uint32_t qg = q_glob + q;
+        const uint32_t slot = qg % a.ring;
+        mbar_wait(empty + slot, ((qg / a.ring) & 1) ^ 1);
         float4* hi = reinterpret_cast<float4*>(sA + slot * slot_bytes);
-        float4* lo = hi + nq * tcols;
+        float4* lo = hi + nelem;
         const float* prow = pbase + (int64_t)q * job.pitch;
-        for (int e = pt; e < nq * tcols; e += 32 * TC_PRODUCERS) {
-          const int quad = e / tcols, c = e - quad * tcols;
-          const int x = x0 + c;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (x < job.W) {
-            const float* p = prow + (int64_t)(4 * quad) * plane + x;
-            v.x = __ldg(p);
-            v.y = __ldg(p + plane);
-            v.z = __ldg(p + 2 * plane);
-            v.w = __ldg(p + 3 * plane);
+        float4 v[PQ];
+#pragma unroll
+        for (int k = 0; k < PQ; ++k) {
+          const int e = lane + 32 * k;
+          v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (e < nelem) {
+            const int quad = e / tcols, c = e - quad * tcols;
+            const int x = x0 + c;
+            if (x < job.W) {
+              const float* p = prow + (int64_t)(4 * quad) * plane + x;
+              v[k].x = __ldg(p);
+              v[k].y = __ldg(p + plane);
+              v[k].z = __ldg(p + 2 * plane);
+              v[k].w = __ldg(p + 3 * plane);
+            }
           }
-          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          hi[e] = h;
-          lo[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+#pragma unroll
+        for (int k = 0; k < PQ; ++k) {
+          const int e = lane + 32 * k;
+          if (e < nelem) {
+            const float4 h = make_float4(tf32_hi(v[k].x), tf32_hi(v[k].y), tf32_hi(v[k].z),
+                                         tf32_hi(v[k].w));
+            hi[e] = h;
+            lo[e] = make_float4(v[k].x - h.x, v[k].y - h.y, v[k].z - h.z, v[k].w - h.w);
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(full + slot);
       }
+      q_glob += job.H;
     }
   } else {
     // =================== epilogue ===================
@@ -345,6 +406,8 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
                                 int nf, uint32_t* ranges, void* stream) {
   DPM_REQUIRE(P && Gtc && S && jobs && strips, "dpm_correlate_tc: null pointer");
   DPM_REQUIRE(R % 8 == 0 && R >= 8, "dpm_correlate_tc: R=%d must be a multiple of 8", R);
+  DPM_REQUIRE((R / 4) * (TC_M + w - 1) <= 320, "dpm_correlate_tc: R=%d w=%d exceed the producer "
+              "staging width", R, w);
   DPM_REQUIRE(nf >= 1 && nf <= 64, "dpm_correlate_tc: nf=%d outside [1, 64]", nf);
   DPM_REQUIRE(h >= 1 && w >= 1 && h + 2 <= TC_MAX_RING, "dpm_correlate_tc: filter %dx%d", h, w);
   if (nstrips == 0) return DPM_OK;
@@ -357,10 +420,15 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
   TcArgs a{P, Gtc, S, jobs, strips, nstrips, h, w, R, N, h + 2, 0, 0, ranges};
   a.acc_cols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
-  void (*fn)(const TcArgs) = N <= 16 ? corr_tc_kernel<16>
-                             : N <= 32 ? corr_tc_kernel<32>
-                             : N <= 48 ? corr_tc_kernel<48>
-                                       : corr_tc_kernel<64>;
+  void (*fn)(const TcArgs) = N <= 16 ? corr_tc_kernel<16, 0, 0>
+                             : N <= 32 ? corr_tc_kernel<32, 0, 0>
+                             : N <= 48 ? corr_tc_kernel<48, 0, 0>
+                                       : corr_tc_kernel<64, 0, 0>;
+  if (h == 6 && w == 6 && R == 8)  // DPM part filters
+    fn = N <= 16 ? corr_tc_kernel<16, 6, 6>
+       : N <= 32 ? corr_tc_kernel<32, 6, 6>
+       : N <= 48 ? corr_tc_kernel<48, 6, 6>
+                 : corr_tc_kernel<64, 6, 6>;
   DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = nstrips < sms ? nstrips : sms;
   fn<<<grid, TC_THREADS, smem, as_stream(stream)>>>(a);
