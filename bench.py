@@ -83,7 +83,8 @@ def _cpu_init():
     _cpu_task.cores = cores_from_stacked(wl.bank, fx["G"])
 
 
-def _cpu_sample_tasks(image, n_root, stride=4):
+def _cpu_sample_tasks(image, n_root, stride=1):
+    # biggest levels first so the pool's tail is short
     return [(image, i, c) for i in range(0, n_root, stride) for c in range(6)]
 
 
@@ -204,7 +205,7 @@ def run_ours(args):
     mine = list(shard(args.images, world, rank))
     n = len(mine)
     sc = PyramidScorer(wl.bank, fx["C"], fx["G"], wl.pyramid, n_images=n,
-                       outputs=("totals",), max_dets=args.max_dets)
+                       outputs=("totals", "positions"), max_dets=args.max_dets)
     plan = sc.plan
     host = sc.host_arena(pinned=True)
     for j, img in enumerate(mine):
@@ -239,23 +240,26 @@ def run_ours(args):
         plan.run(tau=tau)
     barrier()
 
-    # ---- device-resident timing (value); K2 share via events on the same stream
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # ---- device-resident timing (value); per-kernel shares via events recorded
+    # on the launching stream between launches
+    marks = []
+
+    def mark(name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        marks[-1].append((name, ev))
+
     with ClockSampler(local) as clocks:
         barrier()
-        for k in range(args.steps):
-            ev[k][0].record(stream)
-            plan.run(tau=tau, stages=("project",))
-            ev[k][1].record(stream)
-            plan.run(tau=tau, stages=("correlate",))
-            ev[k][2].record(stream)
-            plan.run(tau=tau, stages=("place",))
-            ev[k][3].record(stream)
+        for _ in range(args.steps):
+            marks.append([])
+            plan.run(tau=tau, mark=mark)
         barrier()
-    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
-    k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    k2_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    k34_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    step_ms = [m[0][1].elapsed_time(m[-1][1]) for m in marks]
+    kernel_ms = {}
+    for m in marks:
+        for (name, ev), (_, ev2) in zip(m[:-1], m[1:]):
+            kernel_ms[name] = kernel_ms.get(name, 0.0) + ev.elapsed_time(ev2) / args.steps
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
 
@@ -285,7 +289,7 @@ def run_ours(args):
     from paper_1707_03268_b200._lib import DETECTION
     d2h = 4 + int(statistics.mean(ndets)) * DETECTION.itemsize
 
-    # ---- FFMA peak probe (roofline denominator for K2)
+    # ---- FFMA peak probe (context for the FFMA launches' denominator)
     from paper_1707_03268_b200 import _lib
     import ctypes
 
@@ -303,21 +307,75 @@ def run_ours(args):
 
     peaks = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    nominal_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12
-    k2_flops = sc.k2_flops_per_image() * n
-    k2_avg_ms = statistics.mean(k2_ms)
-    achieved = k2_flops / (k2_avg_ms / 1e3) / 1e12
+    ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    bf16 = float(peaks.get("bf16_tflops", 1590.0))
+    tc_peak = bf16 / 2.0 / 3.0  # tf32 = half the bf16 rate; 3xTF32 = 3 MMA passes per MAC
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
     traffic = _traffic()
+
+    launch_flops = plan.launch_flops()
+    k2 = []
+    for name, fl in launch_flops.items():
+        ms = kernel_ms.get(name)
+        if not ms:
+            continue
+        pk = tc_peak if "tcgen05" in name else ffma_peak
+        k2.append({"kernel": name, "ms": ms, "algorithmic_flops": fl,
+                   "achieved_tflops": fl / (ms / 1e3) / 1e12, "peak_tflops": pk,
+                   "frac": fl / (ms / 1e3) / 1e12 / pk,
+                   "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 3 (3xTF32 passes)"
+                                   if "tcgen05" in name else
+                                   f"148 SMs x 128 FFMA x 2 x {sm_max:.0f} MHz (sm_max_mhz)")})
+    k2_ms = sum(d["ms"] for d in k2)
+    k2_flops = sum(d["algorithmic_flops"] for d in k2)
+    k2_roof_ms = sum(d["algorithmic_flops"] / (d["peak_tflops"] * 1e12) * 1e3 for d in k2)
+
+    # K3/K4 algorithmic bytes: 12 B per part-map cell (read S,
+    # write D and the packed argmax) + 4*(2 + 2*n_parts) B per root eval
+    part_cells, root_evals = 0, 0
+    for a in plan.assemblies:
+        hr, wr = a.rect[1] - a.rect[0] + 1, a.rect[3] - a.rect[2] + 1
+        root_evals += hr * wr
+        for p in a.parts:
+            part_cells += plan.map_shape[(p.level, p.filt)][0] * plan.map_shape[(p.level, p.filt)][1]
+    k34_bytes = n * (12 * part_cells + 4 * (2 + 2 * 8) * root_evals)
+    k34_ms = kernel_ms.get("k3k4_place_assemble", 0.0)
+    k1_bytes = n * plan.k1_bytes()
+    k1_ms = kernel_ms.get("k1_project", 0.0)
+    rooflines = {
+        "k3k4_place_assemble": {"bound": "hbm", "achieved": k34_bytes / (k34_ms / 1e3) / 1e9,
+                                "peak": hbm, "unit": "GB/s",
+                                "frac": k34_bytes / (k34_ms / 1e3) / 1e9 / hbm,
+                                "algorithmic_bytes_per_launch": k34_bytes,
+                                "traffic": (traffic or {}).get("place_assemble_kernel")},
+        "k2_correlate": {"bound": "tensor", "achieved": k2_flops / (k2_ms / 1e3) / 1e12,
+                         "peak": k2_flops / (k2_roof_ms / 1e3) / 1e12, "unit": "TFLOP/s",
+                         "frac": k2_roof_ms / k2_ms,
+                         "algorithmic_flops_per_launch": k2_flops, "launches": k2,
+                         "note": "peak = per-launch roofline mix: tcgen05 3xTF32 launches vs the "
+                                 "tf32 rate / 3, FFMA launches vs the FP32 FFMA rate",
+                         "ffma_probe_tflops": probe_tflops,
+                         "traffic": (traffic or {}).get("corr_tc_kernel")},
+        "k1_project": {"bound": "hbm", "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm,
+                       "unit": "GB/s", "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm,
+                       "algorithmic_bytes_per_launch": k1_bytes,
+                       "traffic": (traffic or {}).get("project_kernel")},
+    }
+    shares = {"k1_project": k1_ms, "k2_correlate": k2_ms, "k3k4_place_assemble": k34_ms}
+    dominant = max(shares, key=shares.get)
+    roofline = dict(rooflines[dominant], kernel=dominant,
+                    peak_source="MEASURED_PEAKS.json" if rooflines[dominant]["bound"] == "hbm"
+                    else "derived from MEASURED_PEAKS.json / FFMA rate (see launches)")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         tasks = _cpu_sample_tasks(image=0, n_root=len(wl.pyramid.root_levels))
-        workers = os.cpu_count() or 1
+        workers = min(os.cpu_count() or 1, len(tasks))
         evals, wall = cpu_run(tasks, workers)
         cpu = {"value": evals / wall, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": f"image 0, root levels 0,4,...,36 x 6 components ({len(tasks)} "
-                         f"(level, component) tasks, {evals} evals) on a {workers}-process pool "
-                         f"of the numpy oracle; {wall:.1f} s wall"}
+               "sample": f"one full image of config {CFG} ({len(tasks)} (root level, component) "
+                         f"tasks, {evals} evals) on a {workers}-process pool running the numpy "
+                         f"oracle (reference algorithm restated); {wall:.1f} s wall"}
 
     if rank == 0:
         out = {
@@ -333,22 +391,13 @@ def run_ours(args):
                        "parallelism": f"image shards x{world}",
                        "l2": "inputs 3.6 GB per step > 126 MB L2 (no flush needed)"},
             "images_per_s": images_s,
-            "stage_ms": {"k1_project": statistics.mean(k1_ms), "k2_correlate": k2_avg_ms,
-                         "k3k4_place_assemble": statistics.mean(k34_ms)},
-            "roofline": {"kernel": "K2 shortened correlation (all launch classes)",
-                         "bound": "fp32", "achieved": achieved,
-                         "peak": nominal_tflops, "unit": "TFLOP/s",
-                         "frac": achieved / nominal_tflops,
-                         "peak_source": f"148 SMs x 128 FFMA x 2 x {sm_max:.0f} MHz "
-                                        "(MEASURED_PEAKS.json sm_max_mhz; no FP32 number there)",
-                         "ffma_probe_tflops": probe_tflops,
-                         "frac_of_probe": achieved / probe_tflops,
-                         "algorithmic_flops_per_launch": k2_flops,
-                         "traffic": traffic},
+            "kernel_ms": kernel_ms,
+            "roofline": roofline,
+            "rooflines": rooflines,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sc.h2d_bytes(),
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
                     "detections_per_step": statistics.mean(ndets), "tau": tau},
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": plan.launches_per_run() * args.steps,
             "clocks": clocks.summary(),
             "clocks_e2e": clocks_e2e.summary(),
             "cpu_baseline": cpu,
@@ -375,7 +424,7 @@ def run_reference(args):
     times, evals = [], 0
     with ctx.Pool(workers, initializer=_cpu_init) as pool:
         for k in range(args.warmup + args.steps):
-            tasks = _cpu_sample_tasks(image=k % N_IMAGES, n_root=n_root, stride=8)
+            tasks = _cpu_sample_tasks(image=k % N_IMAGES, n_root=n_root)
             t0 = time.perf_counter()
             out = pool.map(_cpu_task, tasks, chunksize=1)
             dt = time.perf_counter() - t0
@@ -384,10 +433,10 @@ def run_reference(args):
                 evals = sum(e for e, _ in out)
     total = sum(times)
     value = evals * len(times) / total
-    sample = (f"per step: one image, root levels 0,8,...,32 x 6 components ({len(tasks)} "
-              f"(level, component) tasks, {evals} evals) of config {CFG} on a {workers}-process "
-              "pool of the numpy oracle port (the reference is pure Python and cannot travel "
-              "to the GPU box)")
+    sample = (f"per step: one full image of config {CFG} ({len(tasks)} (root level, component) "
+              f"tasks, {evals} evals; each task also synthesises its two HOG levels) on a "
+              f"{workers}-process pool of the numpy oracle port (the reference is pure "
+              "Python/numpy and cannot travel to the GPU box)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),

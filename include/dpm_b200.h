@@ -143,14 +143,20 @@ int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
  * dpm_correlate): it bounds the FP32 screening error and gives r*. */
 typedef struct {
   int64_t s_off;     /* float offset of the part response map [Hp][Wp]       */
+  int64_t x_off;     /* reserved                                             */
   int32_t Hp, Wp;
   int32_t ay, ax;
   int32_t scale;
   int32_t radius;    /* >= 0 windowed, < 0 GDT via r*                        */
+  int32_t rx0, wr;   /* root columns (centres scale*rx + ax) = the assembly's */
   int32_t range_idx; /* range slot of the map                                */
-  int32_t pad;
+  int32_t block0;    /* reserved                                             */
   double cdx, cdy, cdxx, cdyy;
 } dpm_place_job;
+
+/* Validates the placement jobs (host table); returns 0 or a negative
+ * dpm_status.  (block0 is reserved.) */
+int64_t dpm_place_prepare(dpm_place_job* jobs_host, int njobs);
 
 /* Optional outputs: totals (double), packed part positions (uint32
  * (int16 y) << 16 | (uint16)(int16 x)), per-part placed values (double), and
@@ -182,6 +188,8 @@ typedef struct {
 int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs, const dpm_place_job* pjobs_host,
                              int npjobs);
 
+/* Placement of every part (x pass + y pass) fused with the assembly; one
+ * CTA per 32 x 64 tile of roots.  Detections require the positions output. */
 int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
                  int najobs, int64_t nblocks, const uint32_t* ranges, double* total,
                  uint32_t* pos, double* placed, double tau, dpm_detection* dets, int max_dets,

@@ -29,10 +29,11 @@ CORR_JOB = np.dtype([("p_off", "<i8"), ("s_off", "<i8"), ("g_off", "<i8"),
                      ("nf_pad", "<i4"), ("mode", "<i4"), ("range_idx", "<i4"), ("pad", "<i4")],
                     align=True)
 CORR_TILE = np.dtype([("job", "<i4"), ("ty", "<i4"), ("tx", "<i4"), ("pad", "<i4")], align=True)
-PLACE_JOB = np.dtype([("s_off", "<i8"), ("Hp", "<i4"), ("Wp", "<i4"), ("ay", "<i4"),
-                      ("ax", "<i4"), ("scale", "<i4"), ("radius", "<i4"), ("range_idx", "<i4"),
-                      ("pad", "<i4"), ("cdx", "<f8"), ("cdy", "<f8"), ("cdxx", "<f8"),
-                      ("cdyy", "<f8")], align=True)
+PLACE_JOB = np.dtype([("s_off", "<i8"), ("x_off", "<i8"), ("Hp", "<i4"), ("Wp", "<i4"),
+                      ("ay", "<i4"), ("ax", "<i4"), ("scale", "<i4"), ("radius", "<i4"),
+                      ("rx0", "<i4"), ("wr", "<i4"), ("range_idx", "<i4"), ("block0", "<i4"),
+                      ("cdx", "<f8"), ("cdy", "<f8"), ("cdxx", "<f8"), ("cdyy", "<f8")],
+                     align=True)
 ASM_JOB = np.dtype([("root_off", "<i8"), ("total_off", "<i8"), ("pos_off", "<i8"),
                     ("placed_off", "<i8"), ("root_pitch", "<i4"), ("ry0", "<i4"),
                     ("ry1", "<i4"), ("rx0", "<i4"), ("rx1", "<i4"), ("part_job0", "<i4"),
@@ -43,7 +44,7 @@ DETECTION = np.dtype([("image", "<i4"), ("level", "<i4"), ("component", "<i4"), 
                       ("rx", "<i4"), ("nparts", "<i4"), ("score", "<f8"),
                       ("parts", "<u4", (MAX_PARTS,))], align=True)
 
-_SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 72, "ASM_JOB": 88,
+_SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 88, "ASM_JOB": 88,
           "DETECTION": 96}
 for _n, _s in _SIZES.items():
     assert globals()[_n].itemsize == _s, (_n, globals()[_n].itemsize)
@@ -64,6 +65,7 @@ _SIGNATURES = {
     "dpm_ranges_init": (_i32, [_vp, _i32, _vp]),
     "dpm_correlate_tc_smem": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
     "dpm_correlate_tc": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "dpm_place_prepare": (_i64, [_vp, _i32]),
     "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
     "dpm_assemble": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32, _vp,
                             _vp]),

@@ -1,11 +1,11 @@
-// K3 (part placement) fused with K4 (root + parts assembly).
+// K3 (part placement) and K4 (root + parts assembly).
 //
 // Reference: _placement_grid (detection.py:320-373), best_part_placement
 // (detection.py:180-207) and the assembly of detect / dense_detect
 // (detection.py:449, 509-538; 590-613).
 //
 // Exact semantics (bit-identical values and argmaxes for a given FP32 map):
-//   x pass: for every needed map row y and centre cx = scale*rx + ax,
+//   x pass: for every map row y and centre cx = scale*rx + ax,
 //           best over dx = -r..r (ascending, strict '>') of
 //           S[y][cx+dx] - (c_dx*dx + (c_dxx*dx)*dx), -inf outside the map;
 //   y pass: best over dy = -r..r (ascending, strict '>') of
@@ -14,41 +14,38 @@
 // Penalties use round-to-nearest intrinsics (no FMA contraction), matching
 // the reference's unfused float64 evaluation.
 //
-// Speed: each CTA owns a 32 x 32 tile of roots of one (image, component,
-// root level).  Per part it stages the S band its windows touch in shared
-// memory, runs the x pass for every band row at the 32 centre columns, then
-// the y pass for the 1024 roots.  Candidates are screened in FP32, branch
-// free: the scan keeps the running maximum m1 (first index on ties, strict
-// '>') and the best value m2 of all other candidates.  With
-// E2 = 2^-19 * (max|S| + max pen_x + max pen_y) at least twice the FP32 error
-// of any candidate value, m2 < m1 - E2 proves the FP32 winner is the unique
-// exact winner, whose value is then evaluated once in FP64; otherwise (ties,
-// near ties) the candidates within E2 of m1 are rescanned in FP64 in the
-// reference's order with strict '>'.
+// One kernel: each CTA owns a 32 x 64 tile of roots of one (image,
+// component, root level).  Per part it stages the S band its windows touch
+// in shared memory, runs the x pass for every band row at the 32 centre
+// columns (64-row tiles keep the band overlap between vertically adjacent
+// tiles at 2r / 128 rows), then the y pass for its roots; exact FP64 values
+// are recomputed from the staged band.  Root + parts + bias are summed in
+// registers and written with the part positions; detections >= tau are
+// compacted with one atomic per warp.
+// Candidates are screened in FP32, branch free: the scan keeps the running
+// maximum m1 (first index on ties, strict '>') and the best value m2 of all
+// other candidates.  With E2 = 2^-19 * (max|S| + max pen_x + max pen_y) at
+// least twice the FP32 error of any candidate value, m2 < m1 - E2 proves the
+// FP32 winner is the unique exact winner; otherwise (ties, near ties) the
+// candidates within E2 of m1 are rescanned in FP64 in the reference's order.
+//
 // radius < 0 selects the unbounded generalised distance transform, realised
 // as the window of radius r* computed from the map's
-// range, beyond which no maximiser lies.  Jobs whose radius exceeds RCAP use
-// an unstaged path with the same arithmetic.
+// range, beyond which no maximiser lies.  Radii above RCAP use unstaged loops
+// with the same arithmetic.
 #include <math.h>
 
 #include "common.cuh"
 
 namespace dpm {
 
-constexpr int PT_W = 32;                    // root columns per tile (lanes)
-constexpr int PT_H = 32;                    // root rows per tile
-constexpr int PT_THREADS = 256;
-constexpr int RCAP = 24;                    // staged path radius cap
-constexpr int BAND_MAX = 2 * PT_H + 2 * RCAP;           // scale <= 2
-constexpr int COLS_MAX = 2 * (PT_W - 1) + 1 + 2 * RCAP;  // 111
-constexpr int COLS_PITCH = COLS_MAX + 1;
-
-struct __align__(16) PlaceSmem {
-  float s[BAND_MAX * COLS_PITCH];        // staged S band (-inf outside the map)
-  double xb[BAND_MAX * PT_W];            // x-pass exact values
-  float x32[BAND_MAX * PT_W];            // x-pass values rounded to FP32
-  short xdx[BAND_MAX * PT_W];            // x-pass argmax dx
-};
+constexpr int RCAP = 16;                                  // staged-path radius cap
+constexpr int PT_W = 32;                                  // root columns per tile (lanes)
+constexpr int PT_H = 64;                                  // root rows per tile
+constexpr int PT_THREADS = 512;
+constexpr int PT_WARPS = PT_THREADS / 32;
+constexpr int BAND_MAX = 2 * (PT_H - 1) + 1 + 2 * RCAP;   // 159 (scale <= 2)
+constexpr int COLS_PITCH = 2 * (PT_W - 1) + 1 + 2 * RCAP + 2;  // 97
 
 __device__ __forceinline__ double pen(double c1, double c2, int d) {
   const double dd = (double)d;
@@ -68,6 +65,24 @@ __device__ __forceinline__ int radius_of(const dpm_place_job& j, float vmax, flo
   const double ao = x_axis ? j.cdyy : j.cdxx, bo = x_axis ? j.cdy : j.cdx;
   const double dprime = ((double)vmax - (double)vmin) + bo * bo / (4.0 * ao);
   return (int)floor((fabs(b) + sqrt(b * b + 4.0 * a * dprime)) / (2.0 * a)) + 1;
+}
+
+struct JobRange {
+  float vmax, vmin;
+  int rx, ry;
+  float E2;
+};
+
+__device__ __forceinline__ JobRange job_range(const dpm_place_job& pj, const uint32_t* ranges) {
+  JobRange jr;
+  jr.vmax = key_float(ranges[2 * pj.range_idx]);
+  jr.vmin = key_float(ranges[2 * pj.range_idx + 1]);
+  jr.rx = radius_of(pj, jr.vmax, jr.vmin, true);
+  jr.ry = radius_of(pj, jr.vmax, jr.vmin, false);
+  const double mabs = fmax(fabs((double)jr.vmax), fabs((double)jr.vmin));
+  jr.E2 = (float)ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, jr.rx) + pen_absmax(pj.cdy, pj.cdyy, jr.ry),
+                       -19);
+  return jr;
 }
 
 __device__ __forceinline__ uint32_t pack_pos(int y, int x) {
@@ -115,6 +130,14 @@ __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job
   }
 }
 
+struct __align__(16) PlaceSmem {
+  float s[BAND_MAX * COLS_PITCH];  // staged S band (-inf outside the map)
+  float x32[BAND_MAX * PT_W];      // x-pass winners rounded to FP32
+  int8_t xdx[BAND_MAX * PT_W];     // x-pass winning dx
+  float npx[2 * RCAP + 1];         // -pen_x(dx) in FP32 (screening only)
+  float npy[2 * RCAP + 1];
+};
+
 __global__ void __launch_bounds__(PT_THREADS, 2)
 place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restrict__ pjobs,
                       const dpm_asm_job* __restrict__ ajobs, int najobs,
@@ -130,73 +153,67 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   const int tile = blockIdx.x - aj.block0;
   const int ty0 = (tile / ntx) * PT_H, tx0 = (tile % ntx) * PT_W;  // offsets inside the rect
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int RPT = PT_H / (PT_THREADS / 32);  // roots per thread (4)
+  constexpr int RPT = PT_H / PT_WARPS;  // roots per thread (4)
   const int ix = tx0 + lane;
   const bool col_ok = ix < wr;
   const int rx = aj.rx0 + ix;
+  const int ry_lo = aj.ry0 + ty0;
+  const int ry_hi = aj.ry0 + min(ty0 + PT_H, hr) - 1;
+  const int rx_lo = aj.rx0 + tx0;
 
   double tot[RPT];
-  uint32_t parts[RPT][DPM_MAX_PARTS];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    const int iy = ty0 + warp + 8 * k;
+    const int iy = ty0 + warp + PT_WARPS * k;
     tot[k] = 0.0;
     if (aj.root_off >= 0 && col_ok && iy < hr)
       tot[k] = (double)__ldg(S + aj.root_off + (int64_t)(aj.ry0 + iy) * aj.root_pitch + rx);
   }
 
-  const int ry_lo = aj.ry0 + ty0;
-  const int ry_hi = aj.ry0 + min(ty0 + PT_H, hr) - 1;
-  const int rx_lo = aj.rx0 + tx0;
-
   for (int p = 0; p < aj.nparts; ++p) {
     const dpm_place_job pj = pjobs[aj.part_job0 + p];
-    const float vmax = key_float(ranges[2 * pj.range_idx]);
-    const float vmin = key_float(ranges[2 * pj.range_idx + 1]);
-    const int rxr = radius_of(pj, vmax, vmin, true);
-    const int ryr = radius_of(pj, vmax, vmin, false);
+    const JobRange jr = job_range(pj, ranges);
     const float* sm = S + pj.s_off;
-    const bool staged = rxr <= RCAP && ryr <= RCAP && pj.scale <= 2;
-    if (!staged) {
+    const int cx = pj.scale * rx + pj.ax;
+    if (!(jr.rx <= RCAP && jr.ry <= RCAP && pj.scale <= 2)) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
-        const int iy = ty0 + warp + 8 * k;
+        const int iy = ty0 + warp + PT_WARPS * k;
         if (!col_ok || iy >= hr) continue;
-        const int ry = aj.ry0 + iy;
-        const int cy = pj.scale * ry + pj.ay, cx = pj.scale * rx + pj.ax;
+        const int cy = pj.scale * (aj.ry0 + iy) + pj.ay;
         double best;
         int bdy, bdx;
-        place_unstaged(sm, pj, cy, cx, rxr, ryr, best, bdy, bdx);
+        place_unstaged(sm, pj, cy, cx, jr.rx, jr.ry, best, bdy, bdx);
         tot[k] = __dadd_rn(tot[k], best);
-        const uint32_t pk = pack_pos(cy + bdy, cx + bdx);
-        if (p < DPM_MAX_PARTS) parts[k][p] = pk;
         const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
-        if (aj.pos_off >= 0) pos[aj.pos_off + o] = pk;
+        if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bdy, cx + bdx);
         if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
       }
       continue;
     }
-    const double mabs = fmax(fabs((double)vmax), fabs((double)vmin));
-    const float E2 = (float)ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, rxr) +
-                                  pen_absmax(pj.cdy, pj.cdyy, ryr), -19);
-    // band: map rows / cols the windows of this tile can reach
-    const int yb0 = pj.scale * ry_lo + pj.ay - ryr;
-    const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * ryr;
-    const int xb0 = pj.scale * rx_lo + pj.ax - rxr;
-    const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * rxr;
+    // band: map rows / cols the windows of this tile reach
+    const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
+    const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
+    const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
+    const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * jr.rx;
 
     __syncthreads();  // previous part done with the band
-    // stage the band with cp.async (all loads in flight), -inf outside the map
-    for (int r = warp; r < nrows; r += PT_THREADS / 32) {
+    if (threadIdx.x <= 2 * RCAP) {
+      const int d = threadIdx.x - RCAP;
+      sh.npx[threadIdx.x] = (float)(-pen(pj.cdx, pj.cdxx, d));
+      sh.npy[threadIdx.x] = (float)(-pen(pj.cdy, pj.cdyy, d));
+    }
+    for (int r = warp; r < nrows; r += PT_WARPS) {
       const int y = yb0 + r;
       const bool yok = y >= 0 && y < pj.Hp;
-      const float* srcrow = sm + (int64_t)y * pj.Wp;
+      const float* srow = sm + (int64_t)y * pj.Wp;
       for (int c = lane; c < ncols; c += 32) {
         const int x = xb0 + c;
         float* dst = sh.s + r * COLS_PITCH + c;
         if (yok && x >= 0 && x < pj.Wp) {
-          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(srcrow + x));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(dst)),
+                       "l"(srow + x));
         } else {
           *dst = -INFINITY;
         }
@@ -205,89 +222,87 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
-    const float nax = (float)(-pj.cdxx), nbx = (float)(-pj.cdx);
-    const float nay = (float)(-pj.cdyy), nby = (float)(-pj.cdy);
     // x pass: band row r (warp-strided), centre column = lane
-    for (int r = warp; r < nrows; r += PT_THREADS / 32) {
-      const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + rxr;  // dx = 0
+    const float* npx = sh.npx + RCAP;
+    for (int r = warp; r < nrows; r += PT_WARPS) {
+      const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
       Screen sc;
-      screen_init(sc, rxr);
-      float d = (float)(-rxr);
-      for (int dx = -rxr; dx <= rxr; ++dx, d += 1.f)
-        screen_add(sc, fmaf(fmaf(nax, d, nbx), d, srow[dx]), dx);
-      double xv;
+      screen_init(sc, jr.rx);
+      for (int dx = -jr.rx; dx <= jr.rx; ++dx) screen_add(sc, srow[dx] + npx[dx], dx);
       int xi = sc.i1;
+      float x32;
       if (sc.m1 == -INFINITY) {  // no candidate inside the map: reference gives (-inf, -r)
-        xv = -INFINITY;
-        xi = -rxr;
-      } else if (sc.m2 >= sc.m1 - E2) {  // tie or near tie: exact rescan
-        const float lo = sc.m1 - E2;
-        xv = -INFINITY;
-        xi = -rxr;
-        d = (float)(-rxr);
-        for (int dx = -rxr; dx <= rxr; ++dx, d += 1.f) {
-          if (fmaf(fmaf(nax, d, nbx), d, srow[dx]) >= lo) {
+        x32 = -INFINITY;
+        xi = -jr.rx;
+      } else if (sc.m2 >= sc.m1 - jr.E2) {  // tie or near tie: exact rescan, reference order
+        const float lo = sc.m1 - jr.E2;
+        double xv = -INFINITY;
+        xi = -jr.rx;
+        for (int dx = -jr.rx; dx <= jr.rx; ++dx) {
+          if (srow[dx] + npx[dx] >= lo) {
             const double e = __dadd_rn((double)srow[dx], -pen(pj.cdx, pj.cdxx, dx));
             if (e > xv) { xv = e; xi = dx; }
           }
         }
+        x32 = (float)xv;
       } else {
-        xv = __dadd_rn((double)srow[xi], -pen(pj.cdx, pj.cdxx, xi));
+        x32 = (float)__dadd_rn((double)srow[xi], -pen(pj.cdx, pj.cdxx, xi));
       }
-      sh.xb[r * PT_W + lane] = xv;
-      sh.x32[r * PT_W + lane] = (float)xv;
-      sh.xdx[r * PT_W + lane] = (short)xi;
+      sh.x32[r * PT_W + lane] = x32;
+      sh.xdx[r * PT_W + lane] = (int8_t)xi;
     }
     __syncthreads();
 
-    // y pass for this thread's roots
+    // y pass for this thread's roots; exact values from the staged band
+    const float* npy = sh.npy + RCAP;
+    const float* scol = sh.s + pj.scale * lane + jr.rx;  // band column of the centre
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
-      const int iy = ty0 + warp + 8 * k;
+      const int iy = ty0 + warp + PT_WARPS * k;
       if (!col_ok || iy >= hr) continue;
       const int ry = aj.ry0 + iy;
-      const int r0 = pj.scale * (ry - ry_lo) + ryr;  // band row of dy = 0
+      const int cy = pj.scale * ry + pj.ay;
+      const int r0 = cy - yb0;  // band row of dy = 0
       const float* xcol = sh.x32 + r0 * PT_W + lane;
-      const double* xbcol = sh.xb + r0 * PT_W + lane;
       Screen sc;
-      screen_init(sc, ryr);
-      float d = (float)(-ryr);
-      for (int dy = -ryr; dy <= ryr; ++dy, d += 1.f)
-        screen_add(sc, fmaf(fmaf(nay, d, nby), d, xcol[dy * PT_W]), dy);
+      screen_init(sc, jr.ry);
+      for (int dy = -jr.ry; dy <= jr.ry; ++dy) screen_add(sc, xcol[dy * PT_W] + npy[dy], dy);
+      auto exact = [&](int dy) -> double {
+        const int row = r0 + dy;
+        const int dx = sh.xdx[row * PT_W + lane];
+        const double xv = __dadd_rn((double)scol[row * COLS_PITCH + dx], -pen(pj.cdx, pj.cdxx, dx));
+        return __dadd_rn(xv, -pen(pj.cdy, pj.cdyy, dy));
+      };
       double best;
       int bi = sc.i1;
       if (sc.m1 == -INFINITY) {
         best = -INFINITY;
-        bi = -ryr;
-      } else if (sc.m2 >= sc.m1 - E2) {
-        const float lo = sc.m1 - E2;
+        bi = -jr.ry;
+      } else if (sc.m2 >= sc.m1 - jr.E2) {
+        const float lo = sc.m1 - jr.E2;
         best = -INFINITY;
-        bi = -ryr;
-        d = (float)(-ryr);
-        for (int dy = -ryr; dy <= ryr; ++dy, d += 1.f) {
-          if (fmaf(fmaf(nay, d, nby), d, xcol[dy * PT_W]) >= lo) {
-            const double e = __dadd_rn(xbcol[dy * PT_W], -pen(pj.cdy, pj.cdyy, dy));
+        bi = -jr.ry;
+        for (int dy = -jr.ry; dy <= jr.ry; ++dy) {
+          if (xcol[dy * PT_W] + npy[dy] >= lo) {
+            const double e = exact(dy);
             if (e > best) { best = e; bi = dy; }
           }
         }
       } else {
-        best = __dadd_rn(xbcol[bi * PT_W], -pen(pj.cdy, pj.cdyy, bi));
+        best = exact(bi);
       }
       const int bdx = sh.xdx[(r0 + bi) * PT_W + lane];
-      const int cy = pj.scale * ry + pj.ay, cx = pj.scale * rx + pj.ax;
       tot[k] = __dadd_rn(tot[k], best);
-      const uint32_t pk = pack_pos(cy + bi, cx + bdx);
-      if (p < DPM_MAX_PARTS) parts[k][p] = pk;
       const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
-      if (aj.pos_off >= 0) pos[aj.pos_off + o] = pk;
+      if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bi, cx + bdx);
       if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
     }
   }
 
-  // bias, totals, tau compaction
+  // bias, totals, tau compaction (part positions read back from `pos`)
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    const int iy = ty0 + warp + 8 * k;
+    const int iy = ty0 + warp + PT_WARPS * k;
     const bool live = col_ok && iy < hr;
     if (live) {
       tot[k] = __dadd_rn(tot[k], aj.bias);
@@ -304,17 +319,19 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     if (!hit) continue;
     const int slot = base + __popc(mask & ((1u << lane) - 1u));
     if (slot >= max_dets) continue;
-    dpm_detection d;
-    d.image = aj.image;
-    d.level = aj.level;
-    d.component = aj.component;
-    d.ry = aj.ry0 + iy;
-    d.rx = rx;
-    d.nparts = aj.nparts;
-    d.score = tot[k];
-#pragma unroll
-    for (int p = 0; p < DPM_MAX_PARTS; ++p) d.parts[p] = p < aj.nparts ? parts[k][p] : 0u;
-    dets[slot] = d;
+    dpm_detection dd;
+    dd.image = aj.image;
+    dd.level = aj.level;
+    dd.component = aj.component;
+    dd.ry = aj.ry0 + iy;
+    dd.rx = rx;
+    dd.nparts = aj.nparts;
+    dd.score = tot[k];
+    for (int q = 0; q < DPM_MAX_PARTS; ++q)
+      dd.parts[q] = (q < aj.nparts && aj.pos_off >= 0)
+                        ? pos[aj.pos_off + ((int64_t)q * hr + iy) * wr + ix]
+                        : 0u;
+    dets[slot] = dd;
   }
 }
 
@@ -322,24 +339,34 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
 
 using namespace dpm;
 
+extern "C" int64_t dpm_place_prepare(dpm_place_job* jobs, int njobs) {
+  if (njobs < 0 || (njobs > 0 && !jobs)) {
+    set_error("dpm_place_prepare: bad job table");
+    return DPM_ERR_ARG;
+  }
+  int64_t b = 0;
+  for (int i = 0; i < njobs; ++i) {
+    const dpm_place_job& j = jobs[i];
+    if (j.Hp < 1 || j.Wp < 1 || j.wr < 1 || j.scale < 1 || j.radius > 32000 || j.range_idx < 0) {
+      set_error("dpm_place_prepare: placement job %d has Hp=%d Wp=%d wr=%d scale=%d radius=%d "
+                "range_idx=%d", i, j.Hp, j.Wp, j.wr, j.scale, j.radius, j.range_idx);
+      return DPM_ERR_ARG;
+    }
+    if (j.radius < 0 && !(j.cdxx > 0.0 && j.cdyy > 0.0)) {
+      set_error("dpm_place_prepare: placement job %d: the unbounded transform needs "
+                "c_dxx, c_dyy > 0", i);
+      return DPM_ERR_ARG;
+    }
+    jobs[i].block0 = 0;
+  }
+  return b;
+}
+
 extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_place_job* pjobs,
                                         int npjobs) {
   if (njobs < 0 || (njobs > 0 && !jobs) || npjobs < 0 || (npjobs > 0 && !pjobs)) {
     set_error("dpm_assemble_prepare: bad job tables");
     return DPM_ERR_ARG;
-  }
-  for (int i = 0; i < npjobs; ++i) {
-    const dpm_place_job& j = pjobs[i];
-    if (j.Hp < 1 || j.Wp < 1 || j.scale < 1 || j.radius > 32000 || j.range_idx < 0) {
-      set_error("dpm_assemble_prepare: placement job %d has Hp=%d Wp=%d scale=%d radius=%d "
-                "range_idx=%d", i, j.Hp, j.Wp, j.scale, j.radius, j.range_idx);
-      return DPM_ERR_ARG;
-    }
-    if (j.radius < 0 && !(j.cdxx > 0.0 && j.cdyy > 0.0)) {
-      set_error("dpm_assemble_prepare: placement job %d: the unbounded transform needs "
-                "c_dxx, c_dyy > 0", i);
-      return DPM_ERR_ARG;
-    }
   }
   int64_t b = 0;
   for (int i = 0; i < njobs; ++i) {
@@ -349,6 +376,14 @@ extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_
       set_error("dpm_assemble_prepare: job %d has rect (%d,%d,%d,%d) parts [%d, +%d)", i, j.ry0,
                 j.ry1, j.rx0, j.rx1, j.part_job0, j.nparts);
       return DPM_ERR_ARG;
+    }
+    for (int p = 0; p < j.nparts; ++p) {
+      const dpm_place_job& pj = pjobs[j.part_job0 + p];
+      if (pj.rx0 != j.rx0 || pj.wr != j.rx1 - j.rx0 + 1) {
+        set_error("dpm_assemble_prepare: job %d part %d: x-pass columns [%d, +%d) differ from the "
+                  "root columns", i, p, pj.rx0, pj.wr);
+        return DPM_ERR_ARG;
+      }
     }
     jobs[i].block0 = (int32_t)b;
     const int64_t hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
@@ -366,7 +401,7 @@ extern "C" int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dp
                             uint32_t* pos, double* placed, double tau, dpm_detection* dets,
                             int max_dets, int* det_count, void* stream) {
   DPM_REQUIRE(S && pjobs && ajobs && ranges, "dpm_assemble: null pointer");
-  DPM_REQUIRE(!dets || det_count, "dpm_assemble: detections need a counter");
+  DPM_REQUIRE(!dets || (det_count && pos), "dpm_assemble: detections need a counter and positions");
   DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_assemble: nblocks");
   if (najobs == 0 || nblocks == 0) return DPM_OK;
   const size_t smem = sizeof(PlaceSmem);

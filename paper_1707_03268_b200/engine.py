@@ -283,8 +283,8 @@ class Plan:
                 first = len(place)
                 for p in a.parts:
                     hp, wp = self.map_shape[(p.level, p.filt)]
-                    place.append((self.map_off[(img, p.level, p.filt)], hp, wp,
-                                  p.anchor[0], p.anchor[1], p.scale, p.radius,
+                    place.append((self.map_off[(img, p.level, p.filt)], 0,
+                                  hp, wp, p.anchor[0], p.anchor[1], p.scale, p.radius, rx0, wr,
                                   self.range_slot[(img, p.level, p.filt)], 0,
                                   *[float(v) for v in p.deformation]))
                 root_off, root_pitch = -1, 0
@@ -304,6 +304,8 @@ class Plan:
                                  float(a.bias)))
         self._place_jobs = np.array(place, dtype=_lib.PLACE_JOB) if place else np.zeros(0, _lib.PLACE_JOB)
         self._asm_jobs = np.array(asm_jobs, dtype=_lib.ASM_JOB) if asm_jobs else np.zeros(0, _lib.ASM_JOB)
+        _lib.check(lib.dpm_place_prepare(_lib.table_ptr(self._place_jobs), len(self._place_jobs)),
+                   "placement")
         self._asm_blocks = _lib.check(lib.dpm_assemble_prepare(
             _lib.table_ptr(self._asm_jobs), len(self._asm_jobs),
             _lib.table_ptr(self._place_jobs), len(self._place_jobs)), "assembly")
@@ -368,29 +370,39 @@ class Plan:
             self.x_view(image, k).copy_(src, non_blocking=True)
 
     # ------------------------------------------------------------ execute
-    def run(self, tau=float("inf"), stream=None, stages=("project", "correlate", "place")):
-        """Issue K1..K4 on ``stream`` (default: torch's current stream)."""
+    def run(self, tau=float("inf"), stream=None, stages=("project", "correlate", "place"),
+            mark=None):
+        """Issue K1..K4 on ``stream`` (default: torch's current stream).
+
+        ``mark(name)``, if given, is called before every kernel launch and
+        once at the end with name None (the bench records CUDA events there)."""
         lib = _lib.lib()
         t = self.torch
         s = stream_handle(stream)
         ptr = lambda x: x.data_ptr()  # noqa: E731
+        mark = mark or (lambda name: None)
         if "project" in stages:
+            mark("k1_project")
             _lib.check(lib.dpm_project(ptr(self.X), ptr(self.P), ptr(self.C), self.L, self.Rtot,
                                        ptr(self.proj_jobs_d), len(self._proj_jobs),
                                        self._proj_blocks, s), "project")
         if "correlate" in stages:
             if self.n_ranges:
+                mark("ranges_init")
                 _lib.check(lib.dpm_ranges_init(ptr(self.ranges), self.n_ranges, s), "ranges")
             rng = ptr(self.ranges) if self.n_ranges else None
             for (h, w, R, nf, goff, strips), strips_d in zip(self._tc_classes, self.tc_strips_d):
+                mark(f"k2_tcgen05_{h}x{w}_nf{nf}")
                 _lib.check(lib.dpm_correlate_tc(ptr(self.P), ptr(self.Gtc) + 4 * goff, ptr(self.S),
                                                 ptr(self.corr_jobs_d), ptr(strips_d), len(strips),
                                                 h, w, R, nf, rng, s), "correlate_tc")
             for (h, nf, R, w_max, tiles), tiles_d in zip(self._classes, self.class_tiles_d):
+                mark(f"k2_ffma_h{h}_nf{nf}")
                 _lib.check(lib.dpm_correlate(ptr(self.P), ptr(self.G), ptr(self.S),
                                              ptr(self.corr_jobs_d), ptr(tiles_d), len(tiles), h,
                                              nf, R, w_max, rng, s), "correlate")
         if "place" in stages and len(self._asm_jobs):
+            mark("k3k4_place_assemble")
             rng = ptr(self.ranges)
             if self.det_count is not None:
                 with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
@@ -404,6 +416,7 @@ class Plan:
                 float(tau),
                 ptr(self.dets) if self.dets is not None else None, self.max_dets,
                 ptr(self.det_count) if self.det_count is not None else None, s), "assemble")
+        mark(None)
         return self
 
     # ------------------------------------------------------------ outputs
@@ -436,6 +449,14 @@ class Plan:
         return raw.view(_lib.DETECTION).copy()
 
     # ------------------------------------------------------------ accounting
+    def launches_per_run(self):
+        """Kernels of libdpm_b200 one full run() launches."""
+        n = 1 + len(self._tc_classes) + len(self._classes)  # K1, K2 classes
+        n += 1 if self.n_ranges else 0
+        if len(self._asm_jobs):
+            n += 1
+        return n
+
     def evals(self):
         """cell x filter evaluations per image (BASELINE.md §3 unit of work)."""
         return sum(self.map_shape[(k, f)][0] * self.map_shape[(k, f)][1]
@@ -450,6 +471,22 @@ class Plan:
                 ho, wo = self.map_shape[(k, f)]
                 tot += 2 * fd.h * fd.w * fd.R * ho * wo
         return tot
+
+    def launch_flops(self):
+        """Algorithmic K2 FLOPs (2*h*w*R per eval, all images) of each K2
+        launch, keyed like the names run() passes to ``mark``."""
+        jobs = self._corr_jobs
+        out = {}
+
+        def fl(jids):
+            return sum(2 * int(jobs[j]["h"]) * int(jobs[j]["w"]) * int(jobs[j]["R"]) *
+                       int(jobs[j]["nf"]) * (int(jobs[j]["H"]) - int(jobs[j]["h"]) + 1) *
+                       (int(jobs[j]["W"]) - int(jobs[j]["w"]) + 1) for j in set(jids))
+        for h, w, R, nf, _, strips in self._tc_classes:
+            out[f"k2_tcgen05_{h}x{w}_nf{nf}"] = fl(strips["job"].tolist())
+        for h, nf, R, _, tiles in self._classes:
+            out[f"k2_ffma_h{h}_nf{nf}"] = fl(tiles["job"].tolist())
+        return out
 
     def k1_bytes(self):
         return sum(4 * (self.L + self.Rtot) * H * W for H, W in self.levels)

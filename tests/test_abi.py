@@ -32,7 +32,7 @@ def test_struct_sizes_match_header_comments():
     # sizes asserted at import against the C layout (int64 first, natural alignment)
     assert _lib.PROJ_JOB.itemsize == 32
     assert _lib.CORR_JOB.itemsize == 72
-    assert _lib.PLACE_JOB.itemsize == 72
+    assert _lib.PLACE_JOB.itemsize == 88
     assert _lib.ASM_JOB.itemsize == 88
     assert _lib.DETECTION.itemsize == 96
 
@@ -43,7 +43,7 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
     fields = {
         "dpm_proj_job": ("x_off", "p_off", "H", "W", "pitch", "block0"),
         "dpm_corr_job": ("p_off", "s_off", "g_off", "H", "nf_pad", "range_idx"),
-        "dpm_place_job": ("s_off", "Hp", "range_idx", "cdx", "cdyy"),
+        "dpm_place_job": ("s_off", "x_off", "Hp", "rx0", "block0", "cdx", "cdyy"),
         "dpm_asm_job": ("root_off", "placed_off", "root_pitch", "block0", "bias"),
         "dpm_detection": ("image", "score", "parts"),
     }
@@ -78,12 +78,16 @@ def test_prepare_validates_and_numbers_blocks():
     with pytest.raises(Exception, match="pitch"):
         _lib.check(lib.dpm_project_prepare(_lib.table_ptr(jobs), 2))
     pj = np.zeros(1, dtype=_lib.PLACE_JOB)
-    pj["Hp"], pj["Wp"], pj["scale"], pj["radius"], pj["range_idx"] = 5, 5, 1, -1, 0
-    aj = np.zeros(1, dtype=_lib.ASM_JOB)
-    aj["ry1"], aj["rx1"], aj["nparts"] = 3, 4, 1
+    pj["Hp"], pj["Wp"], pj["scale"], pj["radius"], pj["range_idx"], pj["wr"] = 5, 5, 1, -1, 0, 5
     with pytest.raises(Exception, match="c_dxx"):
-        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1))
+        _lib.check(lib.dpm_place_prepare(_lib.table_ptr(pj), 1))
     pj["cdxx"], pj["cdyy"] = 0.01, 0.01
+    assert lib.dpm_place_prepare(_lib.table_ptr(pj), 1) == 0
+    aj = np.zeros(1, dtype=_lib.ASM_JOB)
+    aj["ry1"], aj["rx1"], aj["nparts"] = 3, 3, 1
+    with pytest.raises(Exception, match="x-pass columns"):
+        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1))
+    aj["rx1"] = 4
     assert lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1) == 1
 
 
