@@ -176,13 +176,15 @@ def _peaks():
         return {}
 
 
-def _traffic():
-    """K2 dram bytes per launch from the committed ncu --set full summary."""
+def _traffic(images):
+    """DRAM bytes per launch (scaled to `images`) from the committed ncu --set full
+    summary (profiles/kernel_traffic.json, written by tools/ncu_summary.py)."""
     try:
-        with open(os.path.join(REPO, "profiles", "k2_traffic.json")) as fh:
-            return json.load(fh)
+        with open(os.path.join(REPO, "profiles", "kernel_traffic.json")) as fh:
+            per_image = json.load(fh)["per_image"]
     except Exception:
-        return None
+        return {}
+    return {k: v * images for k, v in per_image.items()}
 
 
 # ---------------------------------------------------------------- our arm
@@ -311,7 +313,7 @@ def run_ours(args):
     bf16 = float(peaks.get("bf16_tflops", 1590.0))
     tc_peak = bf16 / 2.0 / 3.0  # tf32 = half the bf16 rate; 3xTF32 = 3 MMA passes per MAC
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = _traffic()
+    traffic = _traffic(n)
 
     launch_flops = plan.launch_flops()
     k2 = []
@@ -347,7 +349,7 @@ def run_ours(args):
                                 "peak": hbm, "unit": "GB/s",
                                 "frac": k34_bytes / (k34_ms / 1e3) / 1e9 / hbm,
                                 "algorithmic_bytes_per_launch": k34_bytes,
-                                "traffic": (traffic or {}).get("place_assemble_kernel")},
+                                "traffic": traffic.get("place_assemble_kernel")},
         "k2_correlate": {"bound": "tensor", "achieved": k2_flops / (k2_ms / 1e3) / 1e12,
                          "peak": k2_flops / (k2_roof_ms / 1e3) / 1e12, "unit": "TFLOP/s",
                          "frac": k2_roof_ms / k2_ms,
@@ -355,11 +357,11 @@ def run_ours(args):
                          "note": "peak = per-launch roofline mix: tcgen05 3xTF32 launches vs the "
                                  "tf32 rate / 3, FFMA launches vs the FP32 FFMA rate",
                          "ffma_probe_tflops": probe_tflops,
-                         "traffic": (traffic or {}).get("corr_tc_kernel")},
+                         "traffic": traffic.get("corr_tc_kernel")},
         "k1_project": {"bound": "hbm", "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm,
                        "unit": "GB/s", "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm,
                        "algorithmic_bytes_per_launch": k1_bytes,
-                       "traffic": (traffic or {}).get("project_kernel")},
+                       "traffic": traffic.get("project_kernel")},
     }
     shares = {"k1_project": k1_ms, "k2_correlate": k2_ms, "k3k4_place_assemble": k34_ms}
     dominant = max(shares, key=shares.get)
