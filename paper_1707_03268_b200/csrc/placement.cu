@@ -132,10 +132,11 @@ __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job
 
 struct __align__(16) PlaceSmem {
   float s[BAND_MAX * COLS_PITCH];  // staged S band (-inf outside the map)
-  float x32[BAND_MAX * PT_W];      // x-pass winners rounded to FP32
+  float x32[BAND_MAX * PT_W];      // x-pass winners' FP32 screen values
   int8_t xdx[BAND_MAX * PT_W];     // x-pass winning dx
   float npx[2 * RCAP + 1];         // -pen_x(dx) in FP32 (screening only)
   float npy[2 * RCAP + 1];
+  JobRange jr;                     // r*, E2 of the current part (computed once per CTA)
 };
 
 __global__ void __launch_bounds__(PT_THREADS, 2)
@@ -172,7 +173,15 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
 
   for (int p = 0; p < aj.nparts; ++p) {
     const dpm_place_job pj = pjobs[aj.part_job0 + p];
-    const JobRange jr = job_range(pj, ranges);
+    __syncthreads();  // previous part done with the shared band and parameters
+    if (threadIdx.x == 0) sh.jr = job_range(pj, ranges);
+    if (threadIdx.x >= 32 && threadIdx.x <= 32 + 2 * RCAP) {
+      const int d = threadIdx.x - 32 - RCAP;
+      sh.npx[d + RCAP] = (float)(-pen(pj.cdx, pj.cdxx, d));
+      sh.npy[d + RCAP] = (float)(-pen(pj.cdy, pj.cdyy, d));
+    }
+    __syncthreads();
+    const JobRange jr = sh.jr;
     const float* sm = S + pj.s_off;
     const int cx = pj.scale * rx + pj.ax;
     if (!(jr.rx <= RCAP && jr.ry <= RCAP && pj.scale <= 2)) {
@@ -197,29 +206,22 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
     const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * jr.rx;
 
-    __syncthreads();  // previous part done with the band
-    if (threadIdx.x <= 2 * RCAP) {
-      const int d = threadIdx.x - RCAP;
-      sh.npx[threadIdx.x] = (float)(-pen(pj.cdx, pj.cdxx, d));
-      sh.npy[threadIdx.x] = (float)(-pen(pj.cdy, pj.cdyy, d));
-    }
+    // stage the band: warp per row, up to 3 loads in flight per lane, -inf outside
     for (int r = warp; r < nrows; r += PT_WARPS) {
       const int y = yb0 + r;
       const bool yok = y >= 0 && y < pj.Hp;
-      const float* srow = sm + (int64_t)y * pj.Wp;
-      for (int c = lane; c < ncols; c += 32) {
-        const int x = xb0 + c;
-        float* dst = sh.s + r * COLS_PITCH + c;
-        if (yok && x >= 0 && x < pj.Wp) {
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(dst)),
-                       "l"(srow + x));
-        } else {
-          *dst = -INFINITY;
-        }
+      const float* srow = sm + (int64_t)(yok ? y : 0) * pj.Wp;
+      float v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int c = lane + 32 * q, x = xb0 + c;
+        v[q] = (yok && c < ncols && x >= 0 && x < pj.Wp) ? __ldg(srow + x) : -INFINITY;
       }
+      float* drow = sh.s + r * COLS_PITCH;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (lane + 32 * q < ncols) drow[lane + 32 * q] = v[q];
     }
-    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
     // x pass: band row r (warp-strided), centre column = lane
@@ -229,10 +231,11 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       Screen sc;
       screen_init(sc, jr.rx);
       for (int dx = -jr.rx; dx <= jr.rx; ++dx) screen_add(sc, srow[dx] + npx[dx], dx);
+      // the y-pass screen only needs the winner's value to FP32 accuracy
+      // (the FP32 screen max is within 2^-22 M of it); exact values are
+      // recomputed from the band for y winners and ties
       int xi = sc.i1;
-      float x32;
       if (sc.m1 == -INFINITY) {  // no candidate inside the map: reference gives (-inf, -r)
-        x32 = -INFINITY;
         xi = -jr.rx;
       } else if (sc.m2 >= sc.m1 - jr.E2) {  // tie or near tie: exact rescan, reference order
         const float lo = sc.m1 - jr.E2;
@@ -244,11 +247,8 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
             if (e > xv) { xv = e; xi = dx; }
           }
         }
-        x32 = (float)xv;
-      } else {
-        x32 = (float)__dadd_rn((double)srow[xi], -pen(pj.cdx, pj.cdxx, xi));
       }
-      sh.x32[r * PT_W + lane] = x32;
+      sh.x32[r * PT_W + lane] = sc.m1;
       sh.xdx[r * PT_W + lane] = (int8_t)xi;
     }
     __syncthreads();

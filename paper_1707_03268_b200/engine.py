@@ -212,6 +212,7 @@ class Plan:
         self.map_shape = {}
         self.range_slot = {}
         jobs, classes = [], {}
+        job_image = []
         nslots = 0
         for img in range(nimg):
             for k, fl in self.groups:
@@ -229,6 +230,7 @@ class Plan:
                     if rng >= 0:
                         self.range_slot[(img, k, f)] = rng + i
                 jid = len(jobs)
+                job_image.append(img)
                 jobs.append((img * self.p_image_stride + self.p_level_off[k], s_off,
                              self.core_off[fl], H, W, self.pitch[k], fd.chan_off, fd.h, fd.w,
                              fd.R, len(fl), _round_up(len(fl), 8), 0, rng, 0))
@@ -247,6 +249,7 @@ class Plan:
         self.s_size = max(sa.size, 4)
         self.n_ranges = nslots
         self._corr_jobs = np.array(jobs, dtype=_lib.CORR_JOB) if jobs else np.zeros(0, _lib.CORR_JOB)
+        self._corr_job_image = np.array(job_image, dtype=np.int64)
         self._classes = []
         for (h, nf), cls in sorted(classes.items()):
             # tiles sorted by core so persistent CTAs keep it resident
@@ -265,8 +268,6 @@ class Plan:
                img * self.p_image_stride + self.p_level_off[k], H, W, self.pitch[k], 0)
               for img in range(nimg) for k, (H, W) in enumerate(self.levels)]
         self._proj_jobs = np.array(pj, dtype=_lib.PROJ_JOB)
-        self._proj_blocks = _lib.check(lib.dpm_project_prepare(_lib.table_ptr(self._proj_jobs),
-                                                              len(self._proj_jobs)), "project")
 
         # placement + assembly jobs
         ta, oa, pla = _Arena(), _Arena(), _Arena()
@@ -306,9 +307,6 @@ class Plan:
         self._asm_jobs = np.array(asm_jobs, dtype=_lib.ASM_JOB) if asm_jobs else np.zeros(0, _lib.ASM_JOB)
         _lib.check(lib.dpm_place_prepare(_lib.table_ptr(self._place_jobs), len(self._place_jobs)),
                    "placement")
-        self._asm_blocks = _lib.check(lib.dpm_assemble_prepare(
-            _lib.table_ptr(self._asm_jobs), len(self._asm_jobs),
-            _lib.table_ptr(self._place_jobs), len(self._place_jobs)), "assembly")
         self.total_size, self.pos_size, self.placed_size = ta.size, oa.size, pla.size
 
     def _tc_eligible(self, fl):
@@ -336,13 +334,11 @@ class Plan:
         dev = self.device
         self.C = t.from_numpy(C).to(dev)
         self.G = t.from_numpy(self._core_host).to(dev)
-        self.proj_jobs_d = upload_table(self._proj_jobs, dev)
         self.corr_jobs_d = upload_table(self._corr_jobs, dev)
-        self.class_tiles_d = [upload_table(c[4], dev) for c in self._classes]
         self.Gtc = t.from_numpy(self._tc_core_host).to(dev)
-        self.tc_strips_d = [upload_table(c[5], dev) for c in self._tc_classes]
         self.place_jobs_d = upload_table(self._place_jobs, dev)
-        self.asm_jobs_d = upload_table(self._asm_jobs, dev)
+        self._full = self._make_tables(range(self.n_images))
+        self._chunk_tables = {}
         self.X = t.empty(self.n_images * self.x_image_stride, dtype=t.float32, device=dev)
         self.P = t.empty(self.n_images * self.p_image_stride, dtype=t.float32, device=dev)
         self.S = t.empty(self.s_size, dtype=t.float32, device=dev)
@@ -355,6 +351,39 @@ class Plan:
             self.det_count = t.zeros(1, dtype=t.int32, device=dev)
         else:
             self.dets = self.det_count = None
+
+    def _make_tables(self, images):
+        """Launch tables restricted to ``images`` (all of them for run())."""
+        lib = _lib.lib()
+        dev = self.device
+        imgs = set(images)
+        tb = {}
+        pj = self._proj_jobs[[i // len(self.levels) in imgs for i in range(len(self._proj_jobs))]]
+        pj = np.ascontiguousarray(pj)
+        nblk = _lib.check(lib.dpm_project_prepare(_lib.table_ptr(pj), len(pj)), "project")
+        tb["proj"] = (upload_table(pj, dev), len(pj), nblk)  # upload after block0 is filled
+        keep = np.isin(self._corr_job_image, list(imgs))
+        tb["tc"] = []
+        for h, w, R, nf, goff, strips in self._tc_classes:
+            sub = np.ascontiguousarray(strips[keep[strips["job"]]])
+            tb["tc"].append((h, w, R, nf, goff, len(sub), upload_table(sub, dev)))
+        tb["ffma"] = []
+        for h, nf, R, w_max, tiles in self._classes:
+            sub = np.ascontiguousarray(tiles[keep[tiles["job"]]])
+            tb["ffma"].append((h, nf, R, w_max, len(sub), upload_table(sub, dev)))
+        aj = np.ascontiguousarray(self._asm_jobs[np.isin(self._asm_jobs["image"], list(imgs))])
+        blocks = _lib.check(lib.dpm_assemble_prepare(
+            _lib.table_ptr(aj), len(aj), _lib.table_ptr(self._place_jobs), len(self._place_jobs)),
+            "assembly")
+        tb["asm"] = (upload_table(aj, dev), len(aj), blocks)
+        return tb
+
+    def chunk(self, images):
+        """Launch tables of an image range (cached), for pipelined runs."""
+        key = (images.start, images.stop)
+        if key not in self._chunk_tables:
+            self._chunk_tables[key] = self._make_tables(images)
+        return self._chunk_tables[key]
 
     # ------------------------------------------------------------ inputs
     def x_view(self, image, level):
@@ -371,9 +400,10 @@ class Plan:
 
     # ------------------------------------------------------------ execute
     def run(self, tau=float("inf"), stream=None, stages=("project", "correlate", "place"),
-            mark=None):
+            mark=None, tables=None, reset_dets=True, init_ranges=True):
         """Issue K1..K4 on ``stream`` (default: torch's current stream).
 
+        ``tables`` restricts the run to an image chunk (``chunk()``);
         ``mark(name)``, if given, is called before every kernel launch and
         once at the end with name None (the bench records CUDA events there)."""
         lib = _lib.lib()
@@ -381,35 +411,40 @@ class Plan:
         s = stream_handle(stream)
         ptr = lambda x: x.data_ptr()  # noqa: E731
         mark = mark or (lambda name: None)
-        if "project" in stages:
+        tb = self._full if tables is None else tables
+        if "project" in stages and tb["proj"][1]:
             mark("k1_project")
+            pj_d, npj, nblk = tb["proj"]
             _lib.check(lib.dpm_project(ptr(self.X), ptr(self.P), ptr(self.C), self.L, self.Rtot,
-                                       ptr(self.proj_jobs_d), len(self._proj_jobs),
-                                       self._proj_blocks, s), "project")
+                                       ptr(pj_d), npj, nblk, s), "project")
         if "correlate" in stages:
-            if self.n_ranges:
+            if self.n_ranges and init_ranges:
                 mark("ranges_init")
                 _lib.check(lib.dpm_ranges_init(ptr(self.ranges), self.n_ranges, s), "ranges")
             rng = ptr(self.ranges) if self.n_ranges else None
-            for (h, w, R, nf, goff, strips), strips_d in zip(self._tc_classes, self.tc_strips_d):
+            for h, w, R, nf, goff, n, strips_d in tb["tc"]:
+                if not n:
+                    continue
                 mark(f"k2_tcgen05_{h}x{w}_nf{nf}")
                 _lib.check(lib.dpm_correlate_tc(ptr(self.P), ptr(self.Gtc) + 4 * goff, ptr(self.S),
-                                                ptr(self.corr_jobs_d), ptr(strips_d), len(strips),
+                                                ptr(self.corr_jobs_d), ptr(strips_d), n,
                                                 h, w, R, nf, rng, s), "correlate_tc")
-            for (h, nf, R, w_max, tiles), tiles_d in zip(self._classes, self.class_tiles_d):
+            for h, nf, R, w_max, n, tiles_d in tb["ffma"]:
+                if not n:
+                    continue
                 mark(f"k2_ffma_h{h}_nf{nf}")
                 _lib.check(lib.dpm_correlate(ptr(self.P), ptr(self.G), ptr(self.S),
-                                             ptr(self.corr_jobs_d), ptr(tiles_d), len(tiles), h,
+                                             ptr(self.corr_jobs_d), ptr(tiles_d), n, h,
                                              nf, R, w_max, rng, s), "correlate")
-        if "place" in stages and len(self._asm_jobs):
+        if "place" in stages and tb["asm"][1]:
             mark("k3k4_place_assemble")
             rng = ptr(self.ranges)
-            if self.det_count is not None:
+            if self.det_count is not None and reset_dets:
                 with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
                     self.det_count.zero_()
+            aj_d, naj, nblk = tb["asm"]
             _lib.check(lib.dpm_assemble(
-                ptr(self.S), ptr(self.place_jobs_d), ptr(self.asm_jobs_d),
-                len(self._asm_jobs), self._asm_blocks, rng,
+                ptr(self.S), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk, rng,
                 ptr(self.totals) if self.total_size else None,
                 ptr(self.positions) if self.pos_size else None,
                 ptr(self.placed) if self.placed_size else None,

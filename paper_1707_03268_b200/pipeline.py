@@ -108,15 +108,40 @@ class PyramidScorer:
         """Feature bytes one batch moves host -> device (excluding arena padding)."""
         return 4 * self.plan.L * self.n_images * sum(h * w for h, w in self.plan.levels)
 
-    def score_batch(self, host_arena, tau, stream=None):
-        """Public end-to-end call: host pyramids (arena layout) in, detections
-        (structured numpy array, DETECTION records with score >= tau) out."""
+    def score_batch(self, host_arena, tau, stream=None, chunk_images=8):
+        """Public end-to-end call: host pyramids (arena layout, pinned) in,
+        detections (structured numpy array of DETECTION records with
+        score >= tau) out.
+
+        The batch is pipelined in chunks of ``chunk_images`` images: the
+        host->device copy of chunk k+1 runs on a copy stream while chunk k is
+        scored, so the step costs about max(copy, compute) instead of their sum."""
         t = self.plan.torch
+        plan = self.plan
         s = t.cuda.current_stream() if stream is None else stream
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = t.cuda.Stream()
+        cs = self._copy_stream
+        stride = plan.x_image_stride
+        chunks = [range(i, min(i + chunk_images, self.n_images))
+                  for i in range(0, self.n_images, chunk_images)]
+        copied = []
+        cs.wait_stream(s)  # the previous step's readers of X are done
+        with t.cuda.stream(cs):
+            for c in chunks:
+                lo, hi = c.start * stride, c.stop * stride
+                plan.X[lo:hi].copy_(host_arena[lo:hi], non_blocking=True)
+                ev = t.cuda.Event()
+                ev.record(cs)
+                copied.append(ev)
         with t.cuda.stream(s):
-            self.plan.X.copy_(host_arena, non_blocking=True)
-            self.plan.run(tau=tau, stream=s)
-            return self.plan.detections()
+            if plan.det_count is not None:
+                plan.det_count.zero_()
+            for k, (c, ev) in enumerate(zip(chunks, copied)):
+                s.wait_event(ev)
+                plan.run(tau=tau, stream=s, tables=plan.chunk(c), reset_dets=False,
+                         init_ranges=(k == 0))
+            return plan.detections()
 
     @property
     def X(self):

@@ -407,3 +407,25 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
             g_ff = plans[1].map(0, 0, f).double().cpu().numpy()
             assert_map_close(g_tc, ref, f"tc {H}x{W} filter {f}")
             assert_map_close(g_tc, g_ff, f"tc vs ffma {H}x{W} filter {f}")
+
+
+def test_score_batch_pipelined_matches_full_run():
+    """The chunk-pipelined public call returns exactly the detections of one
+    full-batch run (same records as a set)."""
+    wl = synth.workload(4)
+    C, G = _shared(4, 8)
+    sc = PyramidScorer(wl.bank, C, G, wl.pyramid, n_images=5, max_dets=1 << 18)
+    host = sc.host_arena(pinned=True)
+    for i in range(5):
+        sc.fill_host(host, i, synth.hog_pyramid(4, i, wl.pyramid))
+    sc.plan.X.copy_(host)
+    sc.run()
+    tot = np.concatenate([r["scores"].ravel() for img in range(5) for r in sc.results(img)])
+    tau = float(np.quantile(tot, 0.995))
+    sc.run(tau=tau)
+    full = np.sort(sc.detections(), order=["image", "level", "component", "ry", "rx"])
+    for chunk in (2, 5, 1):
+        got = np.sort(sc.score_batch(host, tau, chunk_images=chunk),
+                      order=["image", "level", "component", "ry", "rx"])
+        assert got.tobytes() == full.tobytes()
+    assert len(full) > 0
