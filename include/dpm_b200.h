@@ -143,7 +143,7 @@ int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
  * dpm_correlate): it bounds the FP32 screening error and gives r*. */
 typedef struct {
   int64_t s_off;     /* float offset of the part response map [Hp][Wp]       */
-  int64_t x_off;     /* reserved                                             */
+  int64_t x_off;     /* GDT path: offset of the x-pass scratch (sv/dx)      */
   int32_t Hp, Wp;
   int32_t ay, ax;
   int32_t scale;
@@ -194,6 +194,34 @@ int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* 
                  int najobs, int64_t nblocks, const uint32_t* ranges, double* total,
                  uint32_t* pos, double* placed, double tau, dpm_detection* dets, int max_dets,
                  int* det_count, void* stream);
+
+/* ------------------------------- K3 as a lower-envelope GDT (+ K4 fused)
+ * Unbounded placement (radius < 0, c_dxx, c_dyy > 0) on the GDT root domain
+ * (every part centre scale*root + anchor inside its map): Felzenszwalb's
+ * generalised distance transform, rows then columns, evaluated at the
+ * centres.  Same values as dpm_assemble with radius < 0; argmaxes identical
+ * except at exact ties.  Replaces _placement_grid (detection.py:320-373) at
+ * an unbounded radius, and the assembly of detect (detection.py:449, 509-538).
+ *
+ * x pass: for every map row and centre column, the winning S value and dx
+ * are written to sv / dx at the job's x_off ([Hp][wr], row-major; sv float,
+ * dx int16).  block0 (in units of 32-row warps) is set by the prepare call,
+ * which returns the CTA count. */
+int64_t dpm_gdt_x_prepare(dpm_place_job* jobs_host, int njobs);
+int dpm_gdt_x(const float* S, float* sv, int16_t* dx, const dpm_place_job* jobs, int njobs,
+              int64_t nblocks, const uint32_t* ranges, void* stream);
+
+/* y pass fused with the assembly: one warp per 32 root columns of an
+ * assembly; parts are placed and summed into totals (required) in part
+ * order, then bias and tau compaction as in dpm_assemble.  `pjobs` is the
+ * full placement table the assemblies index (part_job0), with x_off set as
+ * for dpm_gdt_x. */
+int64_t dpm_gdt_y_prepare(dpm_asm_job* ajobs_host, int najobs, const dpm_place_job* pjobs_host,
+                          int npjobs);
+int dpm_gdt_y(const float* S, const float* sv, const int16_t* dx, const dpm_place_job* pjobs,
+              const dpm_asm_job* ajobs, int najobs, int64_t nblocks, const uint32_t* ranges,
+              double* total, uint32_t* pos, double* placed, double tau, dpm_detection* dets,
+              int max_dets, int* det_count, void* stream);
 
 /* ----------------------------------------------------- micro-benchmark
  * FP32 FFMA peak probe used by bench.py for the K2 roofline denominator:

@@ -69,6 +69,11 @@ _SIGNATURES = {
     "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
     "dpm_assemble": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32, _vp,
                             _vp]),
+    "dpm_gdt_x_prepare": (_i64, [_vp, _i32]),
+    "dpm_gdt_x": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
+    "dpm_gdt_y_prepare": (_i64, [_vp, _i32, _vp, _i32]),
+    "dpm_gdt_y": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32,
+                         _vp, _vp]),
     "dpm_ffma_probe": (_i32, [_vp, _i32, _vp, _vp]),
 }
 

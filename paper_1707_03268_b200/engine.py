@@ -95,11 +95,16 @@ class Plan:
     assemblies : [AssemblyDef] (root + parts placed and summed).
     outputs : subset of {"totals", "positions", "placed"}.
     max_dets : capacity of the on-device detection buffer (0 = none).
+    envelope : place unbounded (radius < 0) assemblies on the GDT root domain
+        with the Felzenszwalb lower-envelope kernels (dpm_gdt_x / dpm_gdt_y)
+        instead of the windowed r* kernel (dpm_assemble).  Both give the same
+        placements (up to exact ties); the window is the default because it
+        is faster at the r* (~10) of the benchmark maps.
     """
 
     def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
                  outputs=("totals", "positions"), max_dets=0, device=None, tensor_cores=True,
-                 tc_min_width=64):
+                 tc_min_width=64, envelope=False):
         import torch
 
         require_cuda()
@@ -118,6 +123,7 @@ class Plan:
         self.max_dets = int(max_dets)
         self.tensor_cores = bool(tensor_cores)
         self.tc_min_width = int(tc_min_width)
+        self.envelope = bool(envelope)
         for k, f in enumerate(self.filters):
             if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
                 raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
@@ -270,8 +276,8 @@ class Plan:
         self._proj_jobs = np.array(pj, dtype=_lib.PROJ_JOB)
 
         # placement + assembly jobs
-        ta, oa, pla = _Arena(), _Arena(), _Arena()
-        place, asm_jobs = [], []
+        ta, oa, pla, ga = _Arena(), _Arena(), _Arena(), _Arena()
+        place, asm_jobs, asm_gdt = [], [], []
         self.asm_index = {}  # (image, a) -> (total_off, pos_off, placed_off, hr, wr)
         for img in range(nimg):
             for ai, a in enumerate(self.assemblies):
@@ -282,9 +288,11 @@ class Plan:
                 if len(a.parts) > _lib.MAX_PARTS:
                     raise ValidationError(f"assembly {ai}: more than {_lib.MAX_PARTS} parts")
                 first = len(place)
+                use_gdt = self._gdt_eligible(a)
                 for p in a.parts:
                     hp, wp = self.map_shape[(p.level, p.filt)]
-                    place.append((self.map_off[(img, p.level, p.filt)], 0,
+                    x_off = ga.take(hp * wr, align=8) if use_gdt else 0
+                    place.append((self.map_off[(img, p.level, p.filt)], x_off,
                                   hp, wp, p.anchor[0], p.anchor[1], p.scale, p.radius, rx0, wr,
                                   self.range_slot[(img, p.level, p.filt)], 0,
                                   *[float(v) for v in p.deformation]))
@@ -296,18 +304,40 @@ class Plan:
                     if not (0 <= ry0 and ry1 < rh and 0 <= rx0 and rx1 < rw):
                         raise ValidationError(f"assembly {ai}: rect {a.rect} outside the root "
                                               f"map {rh}x{rw}")
-                t_off = ta.take(hr * wr, align=4) if "totals" in self.outputs else -1
+                # the GDT kernel accumulates parts in the totals: always allocated
+                t_off = ta.take(hr * wr, align=4) if ("totals" in self.outputs or use_gdt) else -1
                 p_off = oa.take(len(a.parts) * hr * wr, align=4) if "positions" in self.outputs else -1
                 pl_off = pla.take(len(a.parts) * hr * wr, align=4) if "placed" in self.outputs else -1
                 self.asm_index[(img, ai)] = (t_off, p_off, pl_off, hr, wr)
                 asm_jobs.append((root_off, t_off, p_off, pl_off, root_pitch, ry0, ry1, rx0, rx1,
                                  first, len(a.parts), img, a.level_tag, a.component, 0, 0,
                                  float(a.bias)))
+                asm_gdt.append(use_gdt)
         self._place_jobs = np.array(place, dtype=_lib.PLACE_JOB) if place else np.zeros(0, _lib.PLACE_JOB)
         self._asm_jobs = np.array(asm_jobs, dtype=_lib.ASM_JOB) if asm_jobs else np.zeros(0, _lib.ASM_JOB)
         _lib.check(lib.dpm_place_prepare(_lib.table_ptr(self._place_jobs), len(self._place_jobs)),
                    "placement")
+        self._asm_gdt = np.array(asm_gdt, dtype=bool)
         self.total_size, self.pos_size, self.placed_size = ta.size, oa.size, pla.size
+        self.gdt_scratch = ga.size
+
+    def _gdt_eligible(self, a):
+        """Lower-envelope path: every part unbounded with positive quadratic
+        coefficients and every part centre of the rectangle inside its map
+        (the GDT root domain)."""
+        if not self.envelope or not a.parts:
+            return False
+        ry0, ry1, rx0, rx1 = a.rect
+        for p in a.parts:
+            cdx, cdy, cdxx, cdyy = (float(v) for v in p.deformation)
+            if p.radius >= 0 or cdxx <= 0 or cdyy <= 0:
+                return False
+            hp, wp = self.map_shape[(p.level, p.filt)]
+            s, (ay, ax) = p.scale, p.anchor
+            if not (s * ry0 + ay >= 0 and s * ry1 + ay < hp and s * rx0 + ax >= 0
+                    and s * rx1 + ax < wp):
+                return False
+        return True
 
     def _tc_eligible(self, fl):
         if not self.tensor_cores:
@@ -346,6 +376,8 @@ class Plan:
         self.totals = t.empty(max(self.total_size, 1), dtype=t.float64, device=dev)
         self.positions = t.empty(max(self.pos_size, 1), dtype=t.int32, device=dev)
         self.placed = t.empty(max(self.placed_size, 1), dtype=t.float64, device=dev)
+        self.gsv = t.empty(max(self.gdt_scratch, 1), dtype=t.float32, device=dev)
+        self.gdx = t.empty(max(self.gdt_scratch, 1), dtype=t.int16, device=dev)
         if self.max_dets > 0:
             self.dets = t.empty(self.max_dets * _lib.DETECTION.itemsize, dtype=t.uint8, device=dev)
             self.det_count = t.zeros(1, dtype=t.int32, device=dev)
@@ -371,11 +403,24 @@ class Plan:
         for h, nf, R, w_max, tiles in self._classes:
             sub = np.ascontiguousarray(tiles[keep[tiles["job"]]])
             tb["ffma"].append((h, nf, R, w_max, len(sub), upload_table(sub, dev)))
-        aj = np.ascontiguousarray(self._asm_jobs[np.isin(self._asm_jobs["image"], list(imgs))])
+        in_chunk = np.isin(self._asm_jobs["image"], list(imgs))
+        aj = np.ascontiguousarray(self._asm_jobs[in_chunk & ~self._asm_gdt])
         blocks = _lib.check(lib.dpm_assemble_prepare(
             _lib.table_ptr(aj), len(aj), _lib.table_ptr(self._place_jobs), len(self._place_jobs)),
             "assembly")
         tb["asm"] = (upload_table(aj, dev), len(aj), blocks)
+        # lower-envelope GDT: x-pass table (the chunk's placement jobs) and the
+        # y-pass/assembly table (indexing the full placement table)
+        gj = np.ascontiguousarray(self._asm_jobs[in_chunk & self._asm_gdt])
+        sel = np.concatenate([np.arange(j["part_job0"], j["part_job0"] + j["nparts"]) for j in gj]) \
+            if len(gj) else np.zeros(0, np.int64)
+        xj = np.ascontiguousarray(self._place_jobs[sel])
+        xblocks = _lib.check(lib.dpm_gdt_x_prepare(_lib.table_ptr(xj), len(xj)), "gdt x pass")
+        yblocks = _lib.check(lib.dpm_gdt_y_prepare(
+            _lib.table_ptr(gj), len(gj), _lib.table_ptr(self._place_jobs), len(self._place_jobs)),
+            "gdt y pass")
+        tb["gdt"] = (upload_table(xj, dev), len(xj), xblocks, upload_table(gj, dev), len(gj),
+                     yblocks)
         return tb
 
     def chunk(self, images):
@@ -436,12 +481,27 @@ class Plan:
                 _lib.check(lib.dpm_correlate(ptr(self.P), ptr(self.G), ptr(self.S),
                                              ptr(self.corr_jobs_d), ptr(tiles_d), n, h,
                                              nf, R, w_max, rng, s), "correlate")
-        if "place" in stages and tb["asm"][1]:
+        place = "place" in stages and (tb["asm"][1] or tb["gdt"][4])
+        if place and self.det_count is not None and reset_dets:
+            with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
+                self.det_count.zero_()
+        opt = lambda x, n: ptr(x) if n else None  # noqa: E731
+        dets = (ptr(self.dets) if self.dets is not None else None, self.max_dets,
+                ptr(self.det_count) if self.det_count is not None else None)
+        if place and tb["gdt"][4]:
+            xj_d, nxj, xblk, gj_d, ngj, yblk = tb["gdt"]
+            mark("k3x_gdt_rows")
+            _lib.check(lib.dpm_gdt_x(ptr(self.S), ptr(self.gsv), ptr(self.gdx), ptr(xj_d), nxj,
+                                     xblk, ptr(self.ranges), s), "gdt x pass")
+            mark("k3y_gdt_cols_assemble")
+            _lib.check(lib.dpm_gdt_y(ptr(self.S), ptr(self.gsv), ptr(self.gdx),
+                                     ptr(self.place_jobs_d), ptr(gj_d), ngj, yblk, ptr(self.ranges),
+                                     ptr(self.totals), opt(self.positions, self.pos_size),
+                                     opt(self.placed, self.placed_size), float(tau), *dets, s),
+                       "gdt y pass")
+        if place and tb["asm"][1]:
             mark("k3k4_place_assemble")
             rng = ptr(self.ranges)
-            if self.det_count is not None and reset_dets:
-                with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
-                    self.det_count.zero_()
             aj_d, naj, nblk = tb["asm"]
             _lib.check(lib.dpm_assemble(
                 ptr(self.S), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk, rng,
@@ -488,8 +548,10 @@ class Plan:
         """Kernels of libdpm_b200 one full run() launches."""
         n = 1 + len(self._tc_classes) + len(self._classes)  # K1, K2 classes
         n += 1 if self.n_ranges else 0
-        if len(self._asm_jobs):
+        if (~self._asm_gdt).any():
             n += 1
+        if self._asm_gdt.any():
+            n += 2
         return n
 
     def evals(self):

@@ -46,7 +46,7 @@ class PyramidScorer:
     """Device plan scoring ``n_images`` pyramids against a filter bank."""
 
     def __init__(self, bank, C, G, pyramid, n_images=1, radius=-1, domain="gdt",
-                 outputs=("totals", "positions"), max_dets=0, components=None):
+                 outputs=("totals", "positions"), max_dets=0, components=None, envelope=False):
         self.bank, self.pyramid = bank, pyramid
         self.cores = cores_from_stacked(bank, G)
         C = np.asarray(C, dtype=np.float32)
@@ -85,7 +85,7 @@ class PyramidScorer:
                                         level_tag=i, component=ci))
                 self.asm_keys.append((i, ci))
         self.plan = Plan(self.L, pyramid.levels, C, filters, assemblies=asms,
-                         n_images=n_images, outputs=outputs, max_dets=max_dets)
+                         n_images=n_images, outputs=outputs, max_dets=max_dets, envelope=envelope)
         self.n_images = n_images
 
     # inputs

@@ -100,3 +100,31 @@ def test_tile_shapes():
     assert th.value == 16
     assert lib.dpm_correlate_tile_shape(9, 2, ctypes.byref(tw), ctypes.byref(th)) < 0
     assert th.value == 8  # generic kernel tile
+
+
+def test_gdt_prepare_validates_domain_and_numbers_warps():
+    """Lower-envelope GDT tables: unbounded jobs only, centres inside the map,
+    block0 in units of 32-row (x) / 32-column (y) warps, 4 warps per CTA."""
+    lib = _lib.lib()
+    pj = np.zeros(2, dtype=_lib.PLACE_JOB)
+    pj["Hp"], pj["Wp"], pj["scale"], pj["radius"], pj["range_idx"] = 70, 40, 2, -1, 0
+    pj["rx0"], pj["wr"], pj["ay"], pj["ax"] = 1, 10, 1, 3
+    pj["cdxx"], pj["cdyy"] = 0.01, 0.01
+    pj["x_off"] = (0, 700)
+    assert lib.dpm_gdt_x_prepare(_lib.table_ptr(pj), 2) == 2  # 3 + 3 warps -> 2 CTAs
+    assert list(pj["block0"]) == [0, 3]
+    aj = np.zeros(1, dtype=_lib.ASM_JOB)
+    aj["ry0"], aj["ry1"], aj["rx0"], aj["rx1"], aj["nparts"], aj["part_job0"] = 0, 30, 1, 10, 2, 0
+    assert lib.dpm_gdt_y_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 2) == 1
+    aj["ry1"] = 40  # centre row 2*40 + 1 outside Hp = 70
+    with pytest.raises(Exception, match="outside"):
+        _lib.check(lib.dpm_gdt_y_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 2))
+    aj["ry1"], aj["total_off"] = 30, -1
+    with pytest.raises(Exception, match="totals"):
+        _lib.check(lib.dpm_gdt_y_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 2))
+    pj["radius"][1] = 3  # windowed jobs belong to dpm_assemble
+    with pytest.raises(Exception, match="unbounded"):
+        _lib.check(lib.dpm_gdt_x_prepare(_lib.table_ptr(pj), 2))
+    pj["radius"][1], pj["wr"][1] = -1, 20  # centre column 2*20 + 3 outside Wp = 40
+    with pytest.raises(Exception, match="outside"):
+        _lib.check(lib.dpm_gdt_x_prepare(_lib.table_ptr(pj), 2))
