@@ -188,10 +188,22 @@ typedef struct {
 int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs, const dpm_place_job* pjobs_host,
                              int npjobs);
 
+/* K3 prologue, once per run after K2: per placement job, the radius on each
+ * axis (the job's radius, or r* from its map range when radius < 0) and the
+ * FP32 screening bound E2 (see placement.cu). */
+typedef struct {
+  int32_t rx, ry;
+  float E2;
+  int32_t pad;
+} dpm_place_range;
+int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uint32_t* ranges,
+                     dpm_place_range* prep, void* stream);
+
 /* Placement of every part (x pass + y pass) fused with the assembly; one
- * CTA per 32 x 64 tile of roots.  Detections require the positions output. */
+ * CTA per 32 x 64 tile of roots.  `prep` is dpm_place_ranges' output for the
+ * same placement table.  Detections require the positions output. */
 int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
-                 int najobs, int64_t nblocks, const uint32_t* ranges, double* total,
+                 int najobs, int64_t nblocks, const dpm_place_range* prep, double* total,
                  uint32_t* pos, double* placed, double tau, dpm_detection* dets, int max_dets,
                  int* det_count, void* stream);
 

@@ -67,6 +67,7 @@ _SIGNATURES = {
     "dpm_correlate_tc": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "dpm_place_prepare": (_i64, [_vp, _i32]),
     "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
+    "dpm_place_ranges": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "dpm_assemble": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32, _vp,
                             _vp]),
     "dpm_gdt_x_prepare": (_i64, [_vp, _i32]),

@@ -22,12 +22,17 @@
 // are recomputed from the staged band.  Root + parts + bias are summed in
 // registers and written with the part positions; detections >= tau are
 // compacted with one atomic per warp.
-// Candidates are screened in FP32, branch free: the scan keeps the running
-// maximum m1 (first index on ties, strict '>') and the best value m2 of all
-// other candidates.  With E2 = 2^-19 * (max|S| + max pen_x + max pen_y) at
-// least twice the FP32 error of any candidate value, m2 < m1 - E2 proves the
-// FP32 winner is the unique exact winner; otherwise (ties, near ties) the
-// candidates within E2 of m1 are rescanned in FP64 in the reference's order.
+// Candidates are screened in FP32, branch free, by a loop fully unrolled for
+// the part's radius (switch over 0..RCAP): each candidate value carries its
+// window index in the low 6 mantissa bits, candidates are merged in pairs
+// (max/min), and the scan keeps the top value m1 (whose low bits name the
+// winner) and the best value m2 of all other candidates.  Encoding moves a
+// value by < 64 ulps; with E2 = 2^-15 * (max|S| + max pen_x + max pen_y) at
+// least twice the FP32 error plus the encoding error of any candidate,
+// m2 < m1 - E2 proves the decoded winner is the unique exact winner;
+// otherwise (ties, near ties) the candidates within E2 of m1 are rescanned
+// in FP64 in the reference's order.  Cells outside the map are staged as a
+// finite sentinel (-1e37) so encodings stay finite.
 //
 // radius < 0 selects the unbounded generalised distance transform, realised
 // as the window of radius r* computed from the map's
@@ -67,46 +72,82 @@ __device__ __forceinline__ int radius_of(const dpm_place_job& j, float vmax, flo
   return (int)floor((fabs(b) + sqrt(b * b + 4.0 * a * dprime)) / (2.0 * a)) + 1;
 }
 
-struct JobRange {
-  float vmax, vmin;
-  int rx, ry;
-  float E2;
-};
+using JobRange = dpm_place_range;
 
 __device__ __forceinline__ JobRange job_range(const dpm_place_job& pj, const uint32_t* ranges) {
   JobRange jr;
-  jr.vmax = key_float(ranges[2 * pj.range_idx]);
-  jr.vmin = key_float(ranges[2 * pj.range_idx + 1]);
-  jr.rx = radius_of(pj, jr.vmax, jr.vmin, true);
-  jr.ry = radius_of(pj, jr.vmax, jr.vmin, false);
-  const double mabs = fmax(fabs((double)jr.vmax), fabs((double)jr.vmin));
-  jr.E2 = (float)ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, jr.rx) + pen_absmax(pj.cdy, pj.cdyy, jr.ry),
-                       -19);
+  const float vmax = key_float(ranges[2 * pj.range_idx]);
+  const float vmin = key_float(ranges[2 * pj.range_idx + 1]);
+  jr.rx = radius_of(pj, vmax, vmin, true);
+  jr.ry = radius_of(pj, vmax, vmin, false);
+  const double mabs = fmax(fabs((double)vmax), fabs((double)vmin));
+  // floor: the index code of values near 0 lives in denormals (< 64 * 2^-149)
+  jr.E2 = (float)fmax(ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, jr.rx) +
+                                pen_absmax(pj.cdy, pj.cdyy, jr.ry), -15),
+                      0x1p-120);
+  jr.pad = 0;
   return jr;
+}
+
+// K3 prologue: r* and the screening bound of every placement job, once per
+// run (after K2 has filled the map ranges)
+__global__ void __launch_bounds__(256)
+place_ranges_kernel(const dpm_place_job* __restrict__ pjobs, int njobs,
+                    const uint32_t* __restrict__ ranges, dpm_place_range* __restrict__ prep) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < njobs) prep[i] = job_range(pjobs[i], ranges);
 }
 
 __device__ __forceinline__ uint32_t pack_pos(int y, int x) {
   return ((uint32_t)(uint16_t)(int16_t)y << 16) | (uint32_t)(uint16_t)(int16_t)x;
 }
 
-// Branch-free FP32 screen of one window (see file comment).
-struct Screen {
-  float m1, m2;
-  int i1;
-};
+constexpr float OUT_SENTINEL = -1.0e37f;  // staged cells outside the map
+constexpr float NONE_BELOW = -1.0e36f;    // m1 below this: no candidate inside the map
 
-__device__ __forceinline__ void screen_init(Screen& sc, int r) {
-  sc.m1 = -INFINITY;
-  sc.m2 = -INFINITY;
-  sc.i1 = -r;
+__device__ __forceinline__ float enc_idx(float v, int code) {
+  return __int_as_float((__float_as_int(v) & ~63) | code);
 }
 
-__device__ __forceinline__ void screen_add(Screen& sc, float v, int d) {
-  const bool gt = v > sc.m1;
-  sc.m2 = fmaxf(sc.m2, fminf(sc.m1, v));
-  sc.i1 = gt ? d : sc.i1;
-  sc.m1 = fmaxf(sc.m1, v);
+// Window of 2R+1 candidates src[d*STRIDE] + np[d], d = -R..R (pointers at
+// d = 0); m1 = top encoded value (code d + R in its low bits), m2 = best of
+// the others.
+template <int R, int STRIDE>
+__device__ __forceinline__ void screen_window(const float* __restrict__ src,
+                                              const float* __restrict__ np, float& m1, float& m2) {
+  m1 = -INFINITY;
+  m2 = -INFINITY;
+#pragma unroll
+  for (int d = -R; d < R; d += 2) {
+    const float a = enc_idx(src[d * STRIDE] + np[d], d + R);
+    const float b = enc_idx(src[(d + 1) * STRIDE] + np[d + 1], d + 1 + R);
+    const float hi = fmaxf(a, b), lo = fminf(a, b);
+    m2 = fmaxf(m2, fmaxf(lo, fminf(m1, hi)));
+    m1 = fmaxf(m1, hi);
+  }
+  const float c = enc_idx(src[R * STRIDE] + np[R], 2 * R);
+  m2 = fmaxf(m2, fminf(m1, c));
+  m1 = fmaxf(m1, c);
 }
+
+// runtime radius -> unrolled instantiation (radius <= RCAP on the staged path)
+template <int STRIDE>
+__device__ __forceinline__ void screen_dispatch(int r, const float* __restrict__ src,
+                                                const float* __restrict__ np, float& m1,
+                                                float& m2) {
+  switch (r) {
+#define DPM_SCREEN_CASE(R) \
+  case R: screen_window<R, STRIDE>(src, np, m1, m2); break;
+    DPM_SCREEN_CASE(0) DPM_SCREEN_CASE(1) DPM_SCREEN_CASE(2) DPM_SCREEN_CASE(3)
+    DPM_SCREEN_CASE(4) DPM_SCREEN_CASE(5) DPM_SCREEN_CASE(6) DPM_SCREEN_CASE(7)
+    DPM_SCREEN_CASE(8) DPM_SCREEN_CASE(9) DPM_SCREEN_CASE(10) DPM_SCREEN_CASE(11)
+    DPM_SCREEN_CASE(12) DPM_SCREEN_CASE(13) DPM_SCREEN_CASE(14) DPM_SCREEN_CASE(15)
+    DPM_SCREEN_CASE(16)
+#undef DPM_SCREEN_CASE
+    default: m1 = m2 = -INFINITY;
+  }
+}
+static_assert(2 * RCAP + 1 <= 63, "window index must fit the 6-bit code");
 
 // Placement of one part for one root via direct global loads (any radius).
 __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job& pj, int cy,
@@ -131,18 +172,18 @@ __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job
 }
 
 struct __align__(16) PlaceSmem {
-  float s[BAND_MAX * COLS_PITCH];  // staged S band (-inf outside the map)
+  float s[BAND_MAX * COLS_PITCH];  // staged S band (OUT_SENTINEL outside the map)
   float x32[BAND_MAX * PT_W];      // x-pass winners' FP32 screen values
+  float xsv[BAND_MAX * PT_W];      // x-pass winners' S values (exact y values)
   int8_t xdx[BAND_MAX * PT_W];     // x-pass winning dx
-  float npx[2 * RCAP + 1];         // -pen_x(dx) in FP32 (screening only)
-  float npy[2 * RCAP + 1];
-  JobRange jr;                     // r*, E2 of the current part (computed once per CTA)
+  float npx[2][2 * RCAP + 4];      // -pen_x(dx) in FP32 (screening only), by part parity
+  float npy[2][2 * RCAP + 4];
 };
 
 __global__ void __launch_bounds__(PT_THREADS, 2)
 place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restrict__ pjobs,
                       const dpm_asm_job* __restrict__ ajobs, int najobs,
-                      const uint32_t* __restrict__ ranges, double* __restrict__ total,
+                      const dpm_place_range* __restrict__ prep, double* __restrict__ total,
                       uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
                       dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -171,20 +212,61 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       tot[k] = (double)__ldg(S + aj.root_off + (int64_t)(aj.ry0 + iy) * aj.root_pitch + rx);
   }
 
-  for (int p = 0; p < aj.nparts; ++p) {
-    const dpm_place_job pj = pjobs[aj.part_job0 + p];
-    __syncthreads();  // previous part done with the shared band and parameters
-    if (threadIdx.x == 0) sh.jr = job_range(pj, ranges);
-    if (threadIdx.x >= 32 && threadIdx.x <= 32 + 2 * RCAP) {
-      const int d = threadIdx.x - 32 - RCAP;
-      sh.npx[d + RCAP] = (float)(-pen(pj.cdx, pj.cdxx, d));
-      sh.npy[d + RCAP] = (float)(-pen(pj.cdy, pj.cdyy, d));
+  // Per part: [band p resident] x pass -> sync -> async copy of band p+1 into
+  // the same buffer (the y pass only reads x32/xdx/xsv) overlapped with the
+  // y pass of part p.  Penalty tables are double buffered by part parity.
+  auto staged_ok = [&](const dpm_place_job& pj, const JobRange& jr) {
+    return jr.rx <= RCAP && jr.ry <= RCAP && pj.scale <= 2;
+  };
+  auto stage_issue = [&](const dpm_place_job& pj, const JobRange& jr, int buf) {
+    const float* sm = S + pj.s_off;
+    const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
+    const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
+    const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
+    const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * jr.rx;
+    for (int r = warp; r < nrows; r += PT_WARPS) {
+      const int y = yb0 + r;
+      const bool yok = y >= 0 && y < pj.Hp;
+      const float* srow = sm + (int64_t)(yok ? y : 0) * pj.Wp;
+      float* drow = sh.s + r * COLS_PITCH;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int c = lane + 32 * q, x = xb0 + c;
+        if (c >= ncols) continue;
+        if (yok && x >= 0 && x < pj.Wp) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(drow + c);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(srow + x));
+        } else {
+          drow[c] = OUT_SENTINEL;
+        }
+      }
     }
-    __syncthreads();
-    const JobRange jr = sh.jr;
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (threadIdx.x >= PT_THREADS - 2 * (2 * RCAP + 1)) {  // last warps: penalty tables
+      const int t = threadIdx.x - (PT_THREADS - 2 * (2 * RCAP + 1));
+      const int d = (t % (2 * RCAP + 1)) - RCAP;
+      if (t < 2 * RCAP + 1) sh.npx[buf][d + RCAP] = (float)(-pen(pj.cdx, pj.cdxx, d));
+      else sh.npy[buf][d + RCAP] = (float)(-pen(pj.cdy, pj.cdyy, d));
+    }
+  };
+
+  // r*/E2 of every part come from the prologue (dpm_place_ranges)
+  auto issue_part = [&](int q, int buf) {  // band + tables of part q (if staged)
+    const dpm_place_job pn = pjobs[aj.part_job0 + q];
+    const JobRange jn = prep[aj.part_job0 + q];
+    if (staged_ok(pn, jn)) stage_issue(pn, jn, buf);
+  };
+  if (aj.nparts > 0) issue_part(0, 0);
+  for (int p = 0; p < aj.nparts; ++p) {
+    const int buf = p & 1;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();  // band p and its penalty tables resident; part p-1 finished
+    const dpm_place_job pj = pjobs[aj.part_job0 + p];
+    const JobRange jr = prep[aj.part_job0 + p];
     const float* sm = S + pj.s_off;
     const int cx = pj.scale * rx + pj.ax;
-    if (!(jr.rx <= RCAP && jr.ry <= RCAP && pj.scale <= 2)) {
+    const bool have_next = p + 1 < aj.nparts;
+    if (!staged_ok(pj, jr)) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         const int iy = ty0 + warp + PT_WARPS * k;
@@ -198,47 +280,26 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
         if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bdy, cx + bdx);
         if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
       }
+      if (have_next) issue_part(p + 1, buf ^ 1);
       continue;
     }
-    // band: map rows / cols the windows of this tile reach
     const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
-    const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
-    const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * jr.rx;
-
-    // stage the band: warp per row, up to 3 loads in flight per lane, -inf outside
-    for (int r = warp; r < nrows; r += PT_WARPS) {
-      const int y = yb0 + r;
-      const bool yok = y >= 0 && y < pj.Hp;
-      const float* srow = sm + (int64_t)(yok ? y : 0) * pj.Wp;
-      float v[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int c = lane + 32 * q, x = xb0 + c;
-        v[q] = (yok && c < ncols && x >= 0 && x < pj.Wp) ? __ldg(srow + x) : -INFINITY;
-      }
-      float* drow = sh.s + r * COLS_PITCH;
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (lane + 32 * q < ncols) drow[lane + 32 * q] = v[q];
-    }
-    __syncthreads();
 
     // x pass: band row r (warp-strided), centre column = lane
-    const float* npx = sh.npx + RCAP;
+    const float* npx = sh.npx[buf] + RCAP;
     for (int r = warp; r < nrows; r += PT_WARPS) {
       const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
-      Screen sc;
-      screen_init(sc, jr.rx);
-      for (int dx = -jr.rx; dx <= jr.rx; ++dx) screen_add(sc, srow[dx] + npx[dx], dx);
-      // the y-pass screen only needs the winner's value to FP32 accuracy
-      // (the FP32 screen max is within 2^-22 M of it); exact values are
-      // recomputed from the band for y winners and ties
-      int xi = sc.i1;
-      if (sc.m1 == -INFINITY) {  // no candidate inside the map: reference gives (-inf, -r)
+      float m1, m2;
+      screen_dispatch<1>(jr.rx, srow, npx, m1, m2);
+      // the y-pass screen only needs the winner's value to the screening
+      // accuracy; exact values are recomputed from xsv for y winners and ties
+      int xi = (__float_as_int(m1) & 63) - jr.rx;
+      if (m1 < NONE_BELOW) {  // no candidate inside the map: reference gives (-inf, -r)
         xi = -jr.rx;
-      } else if (sc.m2 >= sc.m1 - jr.E2) {  // tie or near tie: exact rescan, reference order
-        const float lo = sc.m1 - jr.E2;
+        m1 = OUT_SENTINEL;
+      } else if (m2 >= m1 - jr.E2) {  // tie or near tie: exact rescan, reference order
+        const float lo = m1 - jr.E2;
         double xv = -INFINITY;
         xi = -jr.rx;
         for (int dx = -jr.rx; dx <= jr.rx; ++dx) {
@@ -248,14 +309,15 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
           }
         }
       }
-      sh.x32[r * PT_W + lane] = sc.m1;
+      sh.x32[r * PT_W + lane] = m1;
+      sh.xsv[r * PT_W + lane] = srow[xi];
       sh.xdx[r * PT_W + lane] = (int8_t)xi;
     }
-    __syncthreads();
+    __syncthreads();  // x pass done: the band buffer is free for part p+1
+    if (have_next) issue_part(p + 1, buf ^ 1);
 
-    // y pass for this thread's roots; exact values from the staged band
-    const float* npy = sh.npy + RCAP;
-    const float* scol = sh.s + pj.scale * lane + jr.rx;  // band column of the centre
+    // y pass for this thread's roots; exact values from the x winners
+    const float* npy = sh.npy[buf] + RCAP;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
       const int iy = ty0 + warp + PT_WARPS * k;
@@ -264,22 +326,21 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       const int cy = pj.scale * ry + pj.ay;
       const int r0 = cy - yb0;  // band row of dy = 0
       const float* xcol = sh.x32 + r0 * PT_W + lane;
-      Screen sc;
-      screen_init(sc, jr.ry);
-      for (int dy = -jr.ry; dy <= jr.ry; ++dy) screen_add(sc, xcol[dy * PT_W] + npy[dy], dy);
+      float m1, m2;
+      screen_dispatch<PT_W>(jr.ry, xcol, npy, m1, m2);
       auto exact = [&](int dy) -> double {
-        const int row = r0 + dy;
-        const int dx = sh.xdx[row * PT_W + lane];
-        const double xv = __dadd_rn((double)scol[row * COLS_PITCH + dx], -pen(pj.cdx, pj.cdxx, dx));
+        const int row = (r0 + dy) * PT_W + lane;
+        const int dx = sh.xdx[row];
+        const double xv = __dadd_rn((double)sh.xsv[row], -pen(pj.cdx, pj.cdxx, dx));
         return __dadd_rn(xv, -pen(pj.cdy, pj.cdyy, dy));
       };
       double best;
-      int bi = sc.i1;
-      if (sc.m1 == -INFINITY) {
+      int bi = (__float_as_int(m1) & 63) - jr.ry;
+      if (m1 < NONE_BELOW) {
         best = -INFINITY;
         bi = -jr.ry;
-      } else if (sc.m2 >= sc.m1 - jr.E2) {
-        const float lo = sc.m1 - jr.E2;
+      } else if (m2 >= m1 - jr.E2) {
+        const float lo = m1 - jr.E2;
         best = -INFINITY;
         bi = -jr.ry;
         for (int dy = -jr.ry; dy <= jr.ry; ++dy) {
@@ -396,11 +457,22 @@ extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_
   return b;
 }
 
+extern "C" int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uint32_t* ranges,
+                                dpm_place_range* prep, void* stream) {
+  DPM_REQUIRE(njobs >= 0 && (njobs == 0 || (pjobs && ranges && prep)),
+              "dpm_place_ranges: null pointer");
+  if (njobs == 0) return DPM_OK;
+  place_ranges_kernel<<<(unsigned)((njobs + 255) / 256), 256, 0, as_stream(stream)>>>(pjobs, njobs,
+                                                                                    ranges, prep);
+  DPM_LAUNCHED("place_ranges_kernel");
+  return DPM_OK;
+}
+
 extern "C" int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
-                            int najobs, int64_t nblocks, const uint32_t* ranges, double* total,
+                            int najobs, int64_t nblocks, const dpm_place_range* prep, double* total,
                             uint32_t* pos, double* placed, double tau, dpm_detection* dets,
                             int max_dets, int* det_count, void* stream) {
-  DPM_REQUIRE(S && pjobs && ajobs && ranges, "dpm_assemble: null pointer");
+  DPM_REQUIRE(S && pjobs && ajobs && prep, "dpm_assemble: null pointer");
   DPM_REQUIRE(!dets || (det_count && pos), "dpm_assemble: detections need a counter and positions");
   DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_assemble: nblocks");
   if (najobs == 0 || nblocks == 0) return DPM_OK;
@@ -408,7 +480,7 @@ extern "C" int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dp
   DPM_CUDA(cudaFuncSetAttribute(place_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   place_assemble_kernel<<<(unsigned)nblocks, PT_THREADS, smem, as_stream(stream)>>>(
-      S, pjobs, ajobs, najobs, ranges, total, pos, placed, tau, dets, max_dets, det_count);
+      S, pjobs, ajobs, najobs, prep, total, pos, placed, tau, dets, max_dets, det_count);
   DPM_LAUNCHED("place_assemble_kernel");
   return DPM_OK;
 }

@@ -376,6 +376,7 @@ class Plan:
         self.totals = t.empty(max(self.total_size, 1), dtype=t.float64, device=dev)
         self.positions = t.empty(max(self.pos_size, 1), dtype=t.int32, device=dev)
         self.placed = t.empty(max(self.placed_size, 1), dtype=t.float64, device=dev)
+        self.prep = t.empty(max(4 * len(self._place_jobs), 4), dtype=t.int32, device=dev)
         self.gsv = t.empty(max(self.gdt_scratch, 1), dtype=t.float32, device=dev)
         self.gdx = t.empty(max(self.gdt_scratch, 1), dtype=t.int16, device=dev)
         if self.max_dets > 0:
@@ -500,11 +501,13 @@ class Plan:
                                      opt(self.placed, self.placed_size), float(tau), *dets, s),
                        "gdt y pass")
         if place and tb["asm"][1]:
+            mark("k3_place_ranges")
+            _lib.check(lib.dpm_place_ranges(ptr(self.place_jobs_d), len(self._place_jobs),
+                                            ptr(self.ranges), ptr(self.prep), s), "place ranges")
             mark("k3k4_place_assemble")
-            rng = ptr(self.ranges)
             aj_d, naj, nblk = tb["asm"]
             _lib.check(lib.dpm_assemble(
-                ptr(self.S), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk, rng,
+                ptr(self.S), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk, ptr(self.prep),
                 ptr(self.totals) if self.total_size else None,
                 ptr(self.positions) if self.pos_size else None,
                 ptr(self.placed) if self.placed_size else None,
@@ -549,7 +552,7 @@ class Plan:
         n = 1 + len(self._tc_classes) + len(self._classes)  # K1, K2 classes
         n += 1 if self.n_ranges else 0
         if (~self._asm_gdt).any():
-            n += 1
+            n += 2  # prologue + placement/assembly
         if self._asm_gdt.any():
             n += 2
         return n
