@@ -429,6 +429,8 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
        : N <= 32 ? corr_tc_kernel<32, 6, 6>
        : N <= 48 ? corr_tc_kernel<48, 6, 6>
                  : corr_tc_kernel<64, 6, 6>;
+  else if (h == 6 && w == 11 && R == 8 && N <= 16)  // DPM root filters (3 mirrored pairs)
+    fn = corr_tc_kernel<16, 6, 11>;
   DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = nstrips < sms ? nstrips : sms;
   fn<<<grid, TC_THREADS, smem, as_stream(stream)>>>(a);

@@ -343,7 +343,8 @@ class Plan:
         if not self.tensor_cores:
             return False
         fd = self.filters[fl[0]]
-        if fd.R % 8 or not (9 <= len(fl) <= 64) or fd.h + 2 > 16:
+        if fd.R % 8 or not (1 <= len(fl) <= 64) or fd.h + 2 > 16 or \
+                (fd.R // 4) * (128 + fd.w - 1) > 320:
             return False
         return _lib.lib().dpm_correlate_tc_smem(fd.h, fd.w, fd.R, len(fl)) <= 227 * 1024
 

@@ -395,7 +395,8 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
 
     rng = np.random.default_rng(11)
     for H, W, nf, h, w, R in [(40, 300, 48, 6, 6, 8), (23, 130, 16, 6, 6, 8),
-                              (17, 200, 33, 5, 7, 8), (12, 70, 64, 3, 4, 8)]:
+                              (17, 200, 33, 5, 7, 8), (12, 70, 64, 3, 4, 8),
+                              (30, 150, 6, 6, 11, 8), (9, 90, 1, 2, 3, 8)]:
         level = rng.random((H, W, 32)).astype(np.float32)
         C = rng.normal(size=(32, R)).astype(np.float32)
         cores = [rng.normal(0, 0.05, (h, w, R)).astype(np.float32) for _ in range(nf)]
