@@ -235,6 +235,32 @@ int dpm_gdt_y(const float* S, const float* sv, const int16_t* dx, const dpm_plac
               double* total, uint32_t* pos, double* placed, double tau, dpm_detection* dets,
               int max_dets, int* det_count, void* stream);
 
+/* ------------------------------------------ pruned detection (Algorithm 1)
+ * First failing rank of every root hypothesis of a rectangle, from the
+ * rank-prefix maps (cp_partial_stack order).  Replaces the per-rank root
+ * checks (detection.py:452-460) and the per-rank part window-max checks
+ * (detection.py:471-503) of detect(pruning=True).  Job = one (level, filter)
+ * role: radius < 0 is the root (value at the root position); radius >= 0 a
+ * part (max over the (2*radius+1)^2 window around scale*root + anchor, cells
+ * outside the map ignored).  map_offs[offs0 + r] is the float offset in S of
+ * prefix r (r < R), thr[thr0 + r] its threshold; out[out_off + iy*wr + ix]
+ * receives r + 1 for the first r with value < thr[r], or 0. */
+typedef struct {
+  int64_t out_off;   /* byte offset of the job's [hr][wr] uint8 ranks       */
+  int32_t offs0;     /* first entry in map_offs                             */
+  int32_t thr0;      /* first entry in thr                                  */
+  int32_t R;         /* ranks checked                                       */
+  int32_t Hp, Wp;    /* prefix map extent                                   */
+  int32_t ry0, ry1, rx0, rx1;
+  int32_t ay, ax, scale;
+  int32_t radius;    /* < 0: root job                                       */
+  int32_t block0;    /* first CTA; set by dpm_prune_prepare                 */
+} dpm_prune_job;
+int64_t dpm_prune_prepare(dpm_prune_job* jobs_host, int njobs);
+int dpm_prune_ranks(const float* S, const int64_t* map_offs, const double* thr,
+                    const dpm_prune_job* jobs, int njobs, int64_t nblocks, uint8_t* out,
+                    void* stream);
+
 /* ----------------------------------------------------- micro-benchmark
  * FP32 FFMA peak probe used by bench.py for the K2 roofline denominator:
  * `iters` dependent-chain-free FFMA blocks on every SM; returns via

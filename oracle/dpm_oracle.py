@@ -44,6 +44,11 @@ __all__ = [
     "r_star",
     "place_gathered",
     "score_pyramid",
+    "dilate_any",
+    "covered_count",
+    "window_max",
+    "detect_pruned",
+    "calibrate_thresholds",
 ]
 
 
@@ -405,3 +410,168 @@ def _gdt_rect(root_support, part_supports, anchors, scale):
     if ry0 > ry1 or rx0 > rx1:
         return None
     return ry0, ry1, rx0, rx1
+
+
+# ------------------------------------------------- pruned detection (Alg. 1)
+
+def dilate_any(mask, radius):
+    """Box dilation onto a grid extended by ``radius`` on every side
+    (detection.py:302-317): out[Y, X] is set when some mask cell lies within
+    the (2r+1)^2 box centred at mask coordinate (Y - r, X - r)."""
+    h, w = mask.shape
+    out = np.zeros((h + 2 * radius, w + 2 * radius), dtype=bool)
+    ys, xs = np.nonzero(mask)
+    width = 2 * radius + 1
+    for y, x in zip(ys, xs):
+        out[y:y + width, x:x + width] = True
+    return out
+
+
+def covered_count(covered, rect, anchor, radius, support):
+    """Part-map positions inside the union of alive search windows
+    (detection.py:545-567)."""
+    ry0, ry1, rx0, rx1 = rect
+    ay, ax = anchor
+    sy, sx = support
+    py0, py1 = max(0, ry0 + ay - radius), min(sy - 1, ry1 + ay + radius)
+    px0, px1 = max(0, rx0 + ax - radius), min(sx - 1, rx1 + ax + radius)
+    if py0 > py1 or px0 > px1:
+        return 0
+    oy, ox = py0 - ay - (ry0 - radius), px0 - ax - (rx0 - radius)
+    return int(covered[oy:oy + py1 - py0 + 1, ox:ox + px1 - px0 + 1].sum())
+
+
+def window_max(stack_r, centres_y, centres_x, radius):
+    """Max of a map over (2r+1)^2 windows at the given centres, -inf outside
+    (detection.py:484-490)."""
+    pad = np.pad(stack_r, radius, constant_values=-np.inf)
+    from numpy.lib.stride_tricks import sliding_window_view
+    win = sliding_window_view(pad, (2 * radius + 1, 2 * radius + 1))
+    hp, wp = stack_r.shape
+    out = np.full(centres_y.shape, -np.inf)
+    ok = (centres_y + radius >= 0) & (centres_y - radius < hp) & \
+         (centres_x + radius >= 0) & (centres_x - radius < wp)
+    cy = np.clip(centres_y, 0, hp - 1)
+    cx = np.clip(centres_x, 0, wp - 1)
+    vals = win[cy, cx].max(axis=(-2, -1))
+    # centres off the map: clip moved them; recompute those exactly
+    off = ok & ((cy != centres_y) | (cx != centres_x))
+    out[ok & ~off] = vals[ok & ~off]
+    for i in np.flatnonzero(off):
+        y, x = centres_y.flat[i], centres_x.flat[i]
+        y0, y1 = max(y - radius, 0), min(y + radius, hp - 1)
+        x0, x1 = max(x - radius, 0), min(x + radius, wp - 1)
+        out.flat[i] = stack_r[y0:y1 + 1, x0:x1 + 1].max()
+    return out
+
+
+def detect_pruned(dec, pyramid, tau, part_prune_mode="kill", stacks=None):
+    """``detect(..., pruning=True)`` (detection.py:386-542, pruning branches
+    433-503): root positions die at the first rank whose prefix partial is
+    below the root threshold; a part whose window-max prefix partial drops
+    below its threshold kills the hypothesis ("kill") or contributes nothing
+    ("lenient").  ``stacks(level_idx, level)`` may supply the rank-prefix
+    maps (root_stack, [part_stacks]); default: ``cp_partial_stack``.
+
+    Returns (detections, stats, prune_maps) with the reference's counters."""
+    dets = []
+    st = {"positions_examined": 0, "positions_pruned_at_rank": {}, "part_pruned_at_rank": {},
+          "positions_killed_by_parts": 0, "multiplications": 0}
+    maps = []
+
+    def bump(table, r, n):
+        if n:
+            table[r] = table.get(r, 0) + int(n)
+
+    for li, level in enumerate(pyramid):
+        level = np.asarray(level, dtype=np.float64)
+        rect = hypothesis_rect(level.shape, dec.root_cp.dims, [p.cp.dims for p in dec.parts],
+                               [p.anchor for p in dec.parts],
+                               [p.search_radius for p in dec.parts])
+        lm = {"rect": rect}
+        maps.append(lm)
+        if rect is None:
+            continue
+        ry0, ry1, rx0, rx1 = rect
+        hr, wr = ry1 - ry0 + 1, rx1 - rx0 + 1
+        st["positions_examined"] += hr * wr
+        if stacks is None:
+            root_stack = cp_partial_stack(level, dec.root_cp)
+            part_stacks = [cp_partial_stack(level, p.cp) for p in dec.parts]
+        else:
+            root_stack, part_stacks = stacks(li, level)
+        root_rect = root_stack[:, ry0:ry1 + 1, rx0:rx1 + 1]
+        alive = np.ones((hr, wr), dtype=bool)
+        prune_rank = np.zeros((hr, wr), dtype=np.int64)
+        n0, m0, l0 = dec.root_cp.dims
+        for r in range(dec.root_cp.rank):
+            st["multiplications"] += int(alive.sum()) * (n0 + m0 + l0)
+            newly = alive & (root_rect[r] < dec.root_thresholds[r])
+            bump(st["positions_pruned_at_rank"], r + 1, newly.sum())
+            prune_rank[newly] = r + 1
+            alive &= ~newly
+        lm["root_prune_rank"] = prune_rank
+        scores = root_rect[-1].copy()
+        part_rank = np.zeros((len(dec.parts), hr, wr), dtype=np.int64)
+        placements = []
+        gy = np.arange(ry0, ry1 + 1)[:, None] + 0 * np.arange(wr)[None, :]
+        gx = np.arange(rx0, rx1 + 1)[None, :] + 0 * np.arange(hr)[:, None]
+        for pi, part in enumerate(dec.parts):
+            if part_prune_mode == "kill" and not alive.any():
+                break
+            pstack = part_stacks[pi]
+            n, m, l = part.cp.dims
+            rad = part.search_radius
+            ay, ax = part.anchor
+            support = (level.shape[0] - n + 1, level.shape[1] - m + 1)
+            part_alive = alive.copy()
+            for r in range(part.cp.rank):
+                if not part_alive.any():
+                    break
+                cov = covered_count(dilate_any(part_alive, rad), rect, (ay, ax), rad, support)
+                st["multiplications"] += cov * (n + m + l)
+                wmax = window_max(pstack[r], gy + ay, gx + ax, rad)
+                newly = part_alive & (wmax < part.thresholds[r])
+                if newly.any():
+                    bump(st["part_pruned_at_rank"], r + 1, newly.sum())
+                    part_rank[pi][newly] = r + 1
+                    part_alive &= ~newly
+                    if part_prune_mode == "kill":
+                        st["positions_killed_by_parts"] += int((alive & newly).sum())
+                        alive &= ~newly
+            placed, py, px = placement_grid(pstack[-1], part.anchor, part.deformation, rad, rect)
+            placements.append((part_alive, placed, py, px, part.anchor))
+            contrib = np.where(part_alive, placed, 0.0) if part_prune_mode == "lenient" else placed
+            scores = scores + contrib
+        lm["part_prune_rank"] = part_rank
+        scores = scores + dec.bias
+        for iy, ix in zip(*np.nonzero(alive & (scores >= tau))):
+            gyy, gxx = ry0 + iy, rx0 + ix
+            pp = []
+            for pa, _, py, px, anc in placements:
+                if part_prune_mode == "lenient" and not pa[iy, ix]:
+                    pp.append((int(gyy + anc[0]), int(gxx + anc[1])))
+                else:
+                    pp.append((int(py[iy, ix]), int(px[iy, ix])))
+            dets.append((li, (int(gyy), int(gxx)), tuple(pp), float(scores[iy, ix])))
+    dets.sort(key=lambda d: (d[0], d[1]))
+    return dets, st, maps
+
+
+def calibrate_thresholds(dec, positives, stacks=None):
+    """Per-rank floors = min over positives of the prefix partials at the
+    positive positions (detection.py:262-299).  Returns (root_thr, [part_thr])."""
+    root_min, part_min = None, [None] * len(dec.parts)
+    for level, hyp in positives:
+        level = np.asarray(level, dtype=np.float64)
+        if stacks is None:
+            rs = cp_partial_stack(level, dec.root_cp)
+            ps = [cp_partial_stack(level, p.cp) for p in dec.parts]
+        else:
+            rs, ps = stacks(level)
+        v = rs[:, hyp.root[0], hyp.root[1]]
+        root_min = v.copy() if root_min is None else np.minimum(root_min, v)
+        for i, (s, pos) in enumerate(zip(ps, hyp.parts)):
+            v = s[:, pos[0], pos[1]]
+            part_min[i] = v.copy() if part_min[i] is None else np.minimum(part_min[i], v)
+    return root_min, part_min

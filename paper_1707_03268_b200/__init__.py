@@ -16,8 +16,9 @@ per kernel.  There is no CPU fallback.
 from .correlation import (ScoreMap, correlate3_cp, correlate3_full, cp_multiplications,
                           cp_partial_stack, full_multiplications, theoretical_gain,
                           valid_support)
-from .detection import (_placement_grid, best_part_placement, cp_score_hypothesis,
-                        deformation_penalty, dense_detect, detect, score_hypothesis, validate)
+from .detection import (_placement_grid, best_part_placement, calibrate_thresholds,
+                        cp_score_hypothesis, deformation_penalty, dense_detect, detect,
+                        score_hypothesis, validate)
 from .errors import CpdetectError, DeviceError, FormatError, NumericError, ValidationError
 from .pipeline import PyramidScorer, cores_from_stacked
 from .types import (CPModel, DecomposedModel, DecomposedPart, Detection, DetectStats,
@@ -31,6 +32,7 @@ __all__ = [
     "PartSpec", "PyramidScorer", "ScoreMap", "ValidationError", "_placement_grid",
     "best_part_placement", "cores_from_stacked", "correlate3_cp", "correlate3_full",
     "cp_multiplications", "cp_partial_stack", "cp_score_hypothesis", "deformation_penalty",
-    "dense_detect", "detect", "full_multiplications", "score_hypothesis", "theoretical_gain",
+    "dense_detect", "detect",
+    "calibrate_thresholds", "full_multiplications", "score_hypothesis", "theoretical_gain",
     "valid_support", "validate",
 ]

@@ -7,8 +7,13 @@ and assembly in FP64 with the reference's exact expression order, so for a
 given response map the placed values and argmaxes are bit-identical to
 ``_placement_grid``.
 
-``detect(..., pruning=True)`` (Algorithm 1, convolution shortening) is the
-next tier and raises NotImplementedError here.
+``detect(..., pruning=True)`` (Algorithm 1, convolution shortening) runs its
+rank-prefix maps (K2), the per-rank root / part-window checks
+(``dpm_prune_ranks``), placement and assembly on the GPU; which hypotheses
+are alive when each part is checked, the lenient-mode sums and the
+reference's work counters are composed on the host from the returned ranks.
+``calibrate_thresholds`` reads its per-rank floors from the GPU's own prefix
+maps, so a model calibrated here never prunes its own positives.
 """
 
 import time
@@ -31,6 +36,7 @@ __all__ = [
     "cp_score_hypothesis",
     "validate",
     "require_valid",
+    "calibrate_thresholds",
 ]
 
 
@@ -185,10 +191,9 @@ def detect(dec, pyramid, tau, pruning=False, part_prune_mode="kill", model_id="m
         raise ValidationError(f"unknown part_prune_mode {part_prune_mode!r}")
     if pruning and not dec.calibrated:
         raise ValidationError("pruning requires calibrated thresholds")
-    if pruning:
-        raise NotImplementedError("pruned detection (Algorithm 1) is the next tier of the "
-                                  "B200 path; call with pruning=False")
     levels = _require_pyramid(pyramid, dec.channels)
+    if pruning:
+        return _detect_pruned(dec, levels, tau, part_prune_mode, model_id, collect_maps)
     start = time.perf_counter()
     stats = DetectStats()
     # per-filter CP: each filter projects onto its own c columns
@@ -285,3 +290,254 @@ def cp_score_hypothesis(dec, level, hypothesis):
         score += float(m[pos[0], pos[1]])
         score -= deformation_penalty(part.deformation, dy, dx)
     return score + dec.bias
+
+
+# ------------------------------------------------- pruned detection (Alg. 1)
+
+def _prefix_filters(cps):
+    """Every rank prefix of every CP filter over its own basis columns:
+    prefix k keeps ranks <= k (the cp_partial_stack order, bit-identical
+    prefixes).  Returns (C, filters, pref) with pref[i] the filter indices of
+    CP i's prefixes 1..R_i."""
+    C = np.concatenate([np.asarray(cp.factors_c, dtype=np.float32) for cp in cps], axis=1)
+    filters, pref, off = [], [], 0
+    for cp in cps:
+        idx = []
+        for k in range(cp.rank):
+            filters.append(FilterDef(cp_core(cp, keep=k + 1), chan_off=off))
+            idx.append(len(filters) - 1)
+        pref.append(idx)
+        off += cp.rank
+    return C, filters, pref
+
+
+def _dilate_any(mask, radius):
+    """Box dilation onto a grid extended by ``radius`` on every side
+    (detection.py:302-317): cell (Y, X) is set when a mask cell lies in the
+    (2r+1)^2 box centred at mask coordinate (Y - r, X - r)."""
+    from numpy.lib.stride_tricks import sliding_window_view
+
+    width = 2 * radius + 1
+    return sliding_window_view(np.pad(mask, 2 * radius), (width, width)).any(axis=(-2, -1))
+
+
+def _covered_count(covered, rect, anchor, radius, support):
+    """Part positions inside the union of alive windows (detection.py:545-567)."""
+    ry0, ry1, rx0, rx1 = rect
+    ay, ax = anchor
+    sy, sx = support
+    py0, py1 = max(0, ry0 + ay - radius), min(sy - 1, ry1 + ay + radius)
+    px0, px1 = max(0, rx0 + ax - radius), min(sx - 1, rx1 + ax + radius)
+    if py0 > py1 or px0 > px1:
+        return 0
+    oy, ox = py0 - ay - (ry0 - radius), px0 - ax - (rx0 - radius)
+    return int(covered[oy:oy + py1 - py0 + 1, ox:ox + px1 - px0 + 1].sum())
+
+
+def _bump(table, rank, count):
+    if count:
+        table[rank] = table.get(rank, 0) + int(count)
+
+
+def _detect_pruned(dec, levels, tau, mode, model_id, collect_maps):
+    """detect(..., pruning=True) (detection.py:386-542 with the pruning
+    branches 433-503)."""
+    from . import _lib
+    from .device import stream_handle, upload_table
+
+    t = _t()
+    start = time.perf_counter()
+    stats = DetectStats()
+    stats.prune_maps = [] if collect_maps else None
+    cps = [dec.root_cp] + [p.cp for p in dec.parts]
+    C, filters, pref = _prefix_filters(cps)
+    root_f, part_fs = pref[0][-1], [pr[-1] for pr in pref[1:]]
+    asms, rects = _detect_plan(levels, C, filters, root_f, part_fs, dec.parts, dec.bias)
+    detections = []
+    if not asms:
+        for rect in rects:
+            if collect_maps:
+                stats.prune_maps.append({"rect": rect})
+        stats.wall_time = time.perf_counter() - start
+        return detections, stats
+    L = levels[0].shape[2]
+    apps = [(a.level_tag, f) for a in asms for f in range(len(filters))]
+    plan = Plan(L, [lv.shape[:2] for lv in levels], C, filters, apps=apps, assemblies=asms,
+                outputs=("totals", "positions", "placed"))
+    for k, lv in enumerate(levels):
+        plan.x_view(0, k).copy_(t.from_numpy(lv.astype(np.float32)))
+    plan.run()
+
+    # per-rank checks on the device: one job per (level, filter role)
+    thr = np.concatenate([np.asarray(dec.root_thresholds, dtype=np.float64)] +
+                         [np.asarray(p.thresholds, dtype=np.float64) for p in dec.parts])
+    thr0 = np.cumsum([0] + [cp.rank for cp in cps])[:-1]
+    jobs, offs, out_at = [], [], {}
+    cursor = 0
+    for ai, a in enumerate(asms):
+        k = a.level_tag
+        ry0, ry1, rx0, rx1 = a.rect
+        n = (ry1 - ry0 + 1) * (rx1 - rx0 + 1)
+        for role, cp in enumerate(cps):
+            hp, wp = plan.map_shape[(k, pref[role][0])]
+            o0 = len(offs)
+            offs.extend(plan.map_off[(0, k, f)] for f in pref[role])
+            if role == 0:
+                ay = ax = 0
+                radius = -1
+            else:
+                part = dec.parts[role - 1]
+                (ay, ax), radius = part.anchor, int(part.search_radius)
+            jobs.append((cursor, o0, int(thr0[role]), cp.rank, hp, wp, ry0, ry1, rx0, rx1,
+                         int(ay), int(ax), 1, radius, 0))
+            out_at[(ai, role)] = cursor
+            cursor += n
+    jobs = np.array(jobs, dtype=_lib.PRUNE_JOB)
+    lib = _lib.lib()
+    nblk = _lib.check(lib.dpm_prune_prepare(_lib.table_ptr(jobs), len(jobs)), "prune")
+    dev = plan.device
+    jobs_d = upload_table(jobs, dev)
+    offs_d = t.tensor(offs, dtype=t.int64, device=dev)
+    thr_d = t.from_numpy(thr).to(dev)
+    ranks_d = t.empty(max(cursor, 1), dtype=t.uint8, device=dev)
+    _lib.check(lib.dpm_prune_ranks(plan.S.data_ptr(), offs_d.data_ptr(), thr_d.data_ptr(),
+                                   jobs_d.data_ptr(), len(jobs), nblk, ranks_d.data_ptr(),
+                                   stream_handle(None)), "prune")
+    ranks = ranks_d.cpu().numpy()
+
+    ai_of = {a.level_tag: ai for ai, a in enumerate(asms)}
+    for li, (lv, rect) in enumerate(zip(levels, rects)):
+        lm = {"rect": rect} if collect_maps else None
+        if collect_maps:
+            stats.prune_maps.append(lm)
+        if rect is None:
+            continue
+        ai = ai_of[li]
+        ry0, ry1, rx0, rx1 = rect
+        hr, wr = ry1 - ry0 + 1, rx1 - rx0 + 1
+        stats.positions_examined += hr * wr
+        rank_of = {role: ranks[out_at[(ai, role)]:out_at[(ai, role)] + hr * wr].reshape(hr, wr)
+                   .astype(np.int64) for role in range(len(cps))}
+        # root: first failing rank (detection.py:452-460)
+        rr = rank_of[0]
+        n0, m0, l0 = dec.root_cp.dims
+        for r in range(dec.root_cp.rank):
+            alive_r = (rr == 0) | (rr > r)
+            stats.multiplications += int(alive_r.sum()) * (n0 + m0 + l0)
+            _bump(stats.positions_pruned_at_rank, r + 1, (rr == r + 1).sum())
+        alive = rr == 0
+        if collect_maps:
+            lm["root_prune_rank"] = rr.copy()
+        out = plan.assembly_outputs(0, ai)
+        placed = out["placed"].cpu().numpy()
+        py, px = unpack_positions(out["positions"].cpu().numpy())
+        part_rank = np.zeros((len(dec.parts), hr, wr), dtype=np.int64)
+        part_alive = []
+        for pi, part in enumerate(dec.parts):
+            if mode == "kill" and not alive.any():
+                break
+            pr = rank_of[pi + 1]
+            n, m, l = part.cp.dims
+            rad = int(part.search_radius)
+            support = (lv.shape[0] - n + 1, lv.shape[1] - m + 1)
+            pa0 = alive.copy()
+            for r in range(part.cp.rank):
+                pa_r = pa0 & ~((pr >= 1) & (pr <= r))
+                if not pa_r.any():
+                    break
+                stats.multiplications += _covered_count(_dilate_any(pa_r, rad), rect,
+                                                        part.anchor, rad, support) * (n + m + l)
+                newly = pa_r & (pr == r + 1)
+                if newly.any():
+                    _bump(stats.part_pruned_at_rank, r + 1, newly.sum())
+                    part_rank[pi][newly] = r + 1
+                    if mode == "kill":
+                        stats.positions_killed_by_parts += int((alive & newly).sum())
+                        alive &= ~newly
+            part_alive.append(pa0 & (pr == 0))
+        if collect_maps:
+            lm["part_prune_rank"] = part_rank
+        if mode == "lenient":
+            # root + sum_i (alive_i ? placed_i : 0) + bias, reference order
+            scores = plan.map(0, li, root_f).double().cpu().numpy()[ry0:ry1 + 1, rx0:rx1 + 1]
+            for pi in range(len(part_alive)):
+                scores = scores + np.where(part_alive[pi], placed[pi], 0.0)
+            scores = scores + dec.bias
+        else:
+            scores = out["totals"].cpu().numpy()
+        for iy, ix in zip(*np.nonzero(alive & (scores >= tau))):
+            gy, gx = ry0 + int(iy), rx0 + int(ix)
+            pp = []
+            for pi, part in enumerate(dec.parts):
+                if mode == "lenient" and not part_alive[pi][iy, ix]:
+                    pp.append((gy + int(part.anchor[0]), gx + int(part.anchor[1])))
+                else:
+                    pp.append((int(py[pi, iy, ix]), int(px[pi, iy, ix])))
+            score = float(scores[iy, ix])
+            hyp = Hypothesis(level=li, root=(gy, gx), parts=tuple(pp), score=score)
+            detections.append(Detection(hyp, model_id=model_id, score=score, tau=tau))
+    detections.sort(key=lambda d: (d.hypothesis.level, d.hypothesis.root))
+    stats.wall_time = time.perf_counter() - start
+    return detections, stats
+
+
+def _check_positive(dec, level, hyp):
+    # detection.py:238-259
+    H, W, _ = level.shape
+    n0, m0, _ = dec.root_cp.dims
+    ry, rx = hyp.root
+    if not (0 <= ry <= H - n0 and 0 <= rx <= W - m0):
+        raise ValidationError(f"positive root position {hyp.root} out of support")
+    if len(hyp.parts) != len(dec.parts):
+        raise ValidationError(f"positive has {len(hyp.parts)} part positions, model has "
+                              f"{len(dec.parts)} parts")
+    for i, (part, pos) in enumerate(zip(dec.parts, hyp.parts)):
+        n, m, _ = part.cp.dims
+        if not (0 <= pos[0] <= H - n and 0 <= pos[1] <= W - m):
+            raise ValidationError(f"positive part {i} position {pos} out of support")
+        dy = pos[0] - ry - part.anchor[0]
+        dx = pos[1] - rx - part.anchor[1]
+        if max(abs(dy), abs(dx)) > part.search_radius:
+            raise ValidationError(f"positive part {i} displaced by ({dy}, {dx}), outside its "
+                                  f"search radius {part.search_radius}")
+
+
+def calibrate_thresholds(dec, positives):
+    """Tightest per-rank floors keeping every positive (detection.py:262-299),
+    read from the GPU's prefix maps.  Returns a copy of ``dec`` with
+    ``root_thresholds`` and per-part ``thresholds`` set."""
+    from dataclasses import replace
+
+    if not positives:
+        raise ValidationError("cannot calibrate thresholds from zero positives")
+    cps = [dec.root_cp] + [p.cp for p in dec.parts]
+    C, filters, pref = _prefix_filters(cps)
+    mins = [None] * len(cps)
+    cache = {}
+    for level, hyp in positives:
+        level = np.asarray(level)
+        _check_positive(dec, level, hyp)
+        key = id(level)
+        if key not in cache:
+            checked = check_feature_map(level, channels=dec.channels)
+            cache[key] = _maps_at(checked, C, filters)
+        maps = cache[key]
+        for role, pos in enumerate((hyp.root,) + tuple(hyp.parts)):
+            vec = np.array([maps[f][pos[0], pos[1]] for f in pref[role]])
+            mins[role] = vec if mins[role] is None else np.minimum(mins[role], vec)
+    parts = tuple(_with(p, thresholds=m) for p, m in zip(dec.parts, mins[1:]))
+    return _with(dec, parts=parts, root_thresholds=mins[0])
+
+
+def _with(obj, **kw):
+    """dataclasses.replace for our types and the reference's (duck typed)."""
+    from dataclasses import is_dataclass, replace
+
+    if is_dataclass(obj):
+        return replace(obj, **kw)
+    import copy
+
+    new = copy.copy(obj)
+    for k, v in kw.items():
+        setattr(new, k, v)
+    return new

@@ -285,7 +285,63 @@ def gen_cfg2_sample():
     save("cfg2_sample.npz", **out)
 
 
+def gen_detect_pruned():
+    """calibrate_thresholds + detect(pruning=True) in both part modes on the
+    reference test fixtures (pkg/tests/test_detection.py:48-53 setup)."""
+    out = {}
+    fast = AlsOptions(max_iterations=100, restarts=1, seed=0)
+    cases = [(0, 1, 2, 2, 0.0), (7, 8, 2, 3, -np.inf), (11, 12, None, 2, 0.5)]
+    for k, (mseed, sseed, low_rank, ranks, tau) in enumerate(cases):
+        model = gen_model(root_size=(3, 4), part_size=(4, 4), n_parts=2, channels=6,
+                          low_rank=low_rank, search_radius=2, bias=0.1, seed=mseed)
+        scene = gen_scene(model, n_objects=2, noise=0.05, level_shapes=((30, 34), (26, 28)),
+                          seed=sseed)
+        dec = decompose_model(model, ranks=ranks, opts=fast)
+        positives = [(scene.pyramid[lvl], hyp) for lvl, hyp in scene.planted]
+        cal = D.calibrate_thresholds(dec, positives)
+        pre = f"q{k}"
+        for li, lv in enumerate(scene.pyramid):
+            out[f"{pre}_level{li}"] = lv
+        out[f"{pre}_nlevels"] = np.int64(len(scene.pyramid))
+        out[f"{pre}_planted"] = np.array([[lvl, *hyp.root, *[c for pp in hyp.parts for c in pp]]
+                                          for lvl, hyp in scene.planted])
+        for pi, prt in enumerate(cal.parts):
+            out[f"{pre}_part{pi}_anchor"] = np.array(prt.anchor)
+            out[f"{pre}_part{pi}_def"] = np.array(prt.deformation)
+            out[f"{pre}_part{pi}_r"] = np.int64(prt.search_radius)
+            out[f"{pre}_part{pi}_thr"] = np.asarray(prt.thresholds)
+            out.update(cp_arrays(f"{pre}_pcp{pi}", prt.cp))
+        out[f"{pre}_nparts"] = np.int64(len(cal.parts))
+        out[f"{pre}_bias"] = np.float64(cal.bias)
+        out[f"{pre}_root_thr"] = np.asarray(cal.root_thresholds)
+        out.update(cp_arrays(f"{pre}_rcp", cal.root_cp))
+        out[f"{pre}_tau"] = np.float64(tau)
+        for mode in ("kill", "lenient"):
+            dets, stats = D.detect(cal, scene.pyramid, tau, pruning=True, part_prune_mode=mode,
+                                   collect_maps=True)
+            m = f"{pre}_{mode}"
+            out[f"{m}_dets"] = np.array([[d.hypothesis.level, *d.hypothesis.root,
+                                          *[c for pp in d.hypothesis.parts for c in pp], d.score]
+                                         for d in dets]).reshape(-1, 3 + 2 * len(cal.parts) + 1)
+            R = max(cal.root_cp.rank, *[p.cp.rank for p in cal.parts])
+            out[f"{m}_stats"] = np.array([stats.positions_examined, stats.positions_killed_by_parts,
+                                          stats.multiplications])
+            out[f"{m}_root_pruned"] = np.array([stats.positions_pruned_at_rank.get(r, 0)
+                                                for r in range(1, R + 1)])
+            out[f"{m}_part_pruned"] = np.array([stats.part_pruned_at_rank.get(r, 0)
+                                                for r in range(1, R + 1)])
+            for li, lm in enumerate(stats.prune_maps):
+                if lm["rect"] is None:
+                    continue
+                out[f"{m}_rect{li}"] = np.array(lm["rect"])
+                out[f"{m}_rootrank{li}"] = lm["root_prune_rank"]
+                out[f"{m}_partrank{li}"] = lm["part_prune_rank"]
+    out["n"] = np.int64(len(cases))
+    save("detect_pruned.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["correlation", "placement", "detect_compact", "cfg1", "cfg2_sample"]
+    which = sys.argv[1:] or ["correlation", "placement", "detect_compact", "cfg1", "cfg2_sample",
+                             "detect_pruned"]
     for w in which:
         globals()["gen_" + w]()

@@ -46,6 +46,9 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
         "dpm_place_job": ("s_off", "x_off", "Hp", "rx0", "block0", "cdx", "cdyy"),
         "dpm_asm_job": ("root_off", "placed_off", "root_pitch", "block0", "bias"),
         "dpm_detection": ("image", "score", "parts"),
+        "dpm_place_range": ("rx", "ry", "E2", "pad"),
+        "dpm_prune_job": ("out_off", "offs0", "thr0", "R", "Hp", "ry0", "rx1", "scale", "radius",
+                          "block0"),
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dpm_b200.h"', "int main(){"]
     for st, fs in fields.items():
@@ -61,7 +64,8 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
     out = dict(line.rsplit(" ", 1) for line in os.popen(str(exe)).read().split("\n") if line)
     dts = {"dpm_proj_job": _lib.PROJ_JOB, "dpm_corr_job": _lib.CORR_JOB,
            "dpm_place_job": _lib.PLACE_JOB, "dpm_asm_job": _lib.ASM_JOB,
-           "dpm_detection": _lib.DETECTION}
+           "dpm_detection": _lib.DETECTION, "dpm_place_range": _lib.PLACE_RANGE,
+           "dpm_prune_job": _lib.PRUNE_JOB}
     for st, fs in fields.items():
         assert int(out[st]) == dts[st].itemsize, st
         for f in fs:

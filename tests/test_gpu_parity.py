@@ -468,3 +468,128 @@ def test_gdt_envelope_matches_windowed_rstar_kernel():
         scale = np.abs(wa["totals"]).max()
         assert np.abs(ga["totals"] - wa["totals"]).max() <= 1e-12 * scale
     assert ties <= 1e-4 * n, (ties, n)
+
+
+def _pruned_case(k):
+    from conftest import golden_pruned
+
+    g = load_golden("detect_pruned.npz")
+    dec, pyr, planted, tau = golden_pruned(g, k)
+    hyps = [(pyr[int(p[0])], B.Hypothesis(level=int(p[0]), root=(int(p[1]), int(p[2])),
+                                           parts=tuple((int(p[3 + 2 * i]), int(p[4 + 2 * i]))
+                                                       for i in range(len(dec.parts)))))
+            for p in planted]
+    return g, dec, pyr, hyps, tau
+
+
+def _gpu_stacks(dec):
+    def stacks(li, level):
+        return (B.cp_partial_stack(level, dec.root_cp),
+                [B.cp_partial_stack(level, p.cp) for p in dec.parts])
+    return stacks
+
+
+def _stats_tuple(st):
+    return (st.positions_examined, dict(st.positions_pruned_at_rank), dict(st.part_pruned_at_rank),
+            st.positions_killed_by_parts, st.multiplications)
+
+
+@pytest.mark.parametrize("mode", ["kill", "lenient"])
+def test_pruned_detect_kernel_isolated_exact(mode):
+    """GPU detect(pruning=True) vs the oracle's restatement run on the GPU's own
+    FP32 prefix maps: prune ranks, counters, detections and scores identical."""
+    for k in range(3):
+        g, dec, pyr, hyps, tau = _pruned_case(k)
+        dets, st = B.detect(dec, pyr, tau, pruning=True, part_prune_mode=mode, collect_maps=True)
+        odets, ost, omaps = O.detect_pruned(dec, pyr, tau, part_prune_mode=mode,
+                                            stacks=_gpu_stacks(dec))
+        assert _stats_tuple(st) == (ost["positions_examined"], ost["positions_pruned_at_rank"],
+                                    ost["part_pruned_at_rank"], ost["positions_killed_by_parts"],
+                                    ost["multiplications"]), (k, mode)
+        for lm, om in zip(st.prune_maps, omaps):
+            assert lm["rect"] == om["rect"]
+            if lm["rect"] is not None:
+                assert np.array_equal(lm["root_prune_rank"], om["root_prune_rank"])
+                assert np.array_equal(lm["part_prune_rank"], om["part_prune_rank"])
+        assert len(dets) == len(odets)
+        for d, o in zip(dets, odets):
+            h = d.hypothesis
+            assert (h.level, tuple(h.root), tuple(map(tuple, h.parts))) == (o[0], o[1], o[2])
+            assert d.score == o[3]
+
+
+@pytest.mark.parametrize("mode", ["kill", "lenient"])
+def test_pruned_detect_matches_reference_golden(mode):
+    """GPU pruned detection vs the reference run (FP64 maps, FP64 calibration).
+    Prune ranks may differ only where the deciding comparison is within the
+    FP32 map tolerance of its threshold (calibrated thresholds sit exactly on
+    positives' FP64 values); everything else -- detections, scores to 1e-5,
+    part positions up to ties -- agrees."""
+    for k in range(3):
+        g, dec, pyr, hyps, tau = _pruned_case(k)
+        m = f"q{k}_{mode}"
+        dets, st = B.detect(dec, pyr, tau, pruning=True, part_prune_mode=mode, collect_maps=True)
+        flips = np.zeros(0, dtype=bool)
+        affected = set()
+        for li, lm in enumerate(st.prune_maps):
+            if lm["rect"] is None:
+                continue
+            rr, gr = lm["root_prune_rank"], g[f"{m}_rootrank{li}"]
+            pr, gp = lm["part_prune_rank"], g[f"{m}_partrank{li}"]
+            level = np.asarray(pyr[li], dtype=np.float64)
+            ry0, ry1, rx0, rx1 = lm["rect"]
+            rs = O.cp_partial_stack(level, dec.root_cp)
+            scale = np.abs(rs).max()
+            for iy, ix in zip(*np.nonzero(rr != gr)):
+                r = min(v for v in (rr[iy, ix], gr[iy, ix]) if v) - 1
+                gap = abs(rs[r, ry0 + iy, rx0 + ix] - dec.root_thresholds[r])
+                assert gap <= 1e-5 * scale, (k, mode, li, iy, ix, gap)
+                affected.add((li, ry0 + iy, rx0 + ix))
+            for pi, part in enumerate(dec.parts):
+                ps = O.cp_partial_stack(level, part.cp)
+                pscale = np.abs(ps).max()
+                for iy, ix in zip(*np.nonzero(pr[pi] != gp[pi])):
+                    cands = [v for v in (pr[pi][iy, ix], gp[pi][iy, ix]) if v]
+                    if not cands:
+                        continue
+                    r = min(cands) - 1
+                    wm = O.window_max(ps[r], np.array([ry0 + iy + part.anchor[0]]),
+                                      np.array([rx0 + ix + part.anchor[1]]), part.search_radius)
+                    gap = abs(wm[0] - part.thresholds[r])
+                    # a root pruned / killed earlier on one side leaves the part unchecked
+                    assert gap <= 1e-5 * pscale or (li, ry0 + iy, rx0 + ix) in affected, \
+                        (k, mode, li, pi, iy, ix, gap)
+                    affected.add((li, ry0 + iy, rx0 + ix))
+        ref = g[f"{m}_dets"]
+        got = {(d.hypothesis.level, *d.hypothesis.root): d for d in dets}
+        want = {(int(r[0]), int(r[1]), int(r[2])): r for r in ref}
+        for key in set(got) ^ set(want):
+            assert key in affected, (k, mode, key)
+        for key in (set(got) & set(want)) - affected:
+            d, r = got[key], want[key]
+            assert abs(d.score - r[-1]) <= 1e-5 * max(1.0, abs(r[-1])), (k, mode, key)
+        if not affected:
+            assert [st.positions_examined, st.positions_killed_by_parts, st.multiplications] == \
+                list(g[f"{m}_stats"])
+
+
+def test_gpu_calibration_never_prunes_its_positives():
+    """calibrate_thresholds on the GPU's prefix maps: thresholds within 1e-5 of
+    the reference's FP64 calibration, and zero false pruning of the positives
+    (the reference's acceptance criterion 4)."""
+    for k in range(3):
+        g, dec, pyr, hyps, tau = _pruned_case(k)
+        cal = B.calibrate_thresholds(dec, hyps)
+        scale = max(np.abs(dec.root_thresholds).max(), 1.0)
+        assert np.abs(cal.root_thresholds - dec.root_thresholds).max() <= 1e-5 * scale
+        for a, b in zip(cal.parts, dec.parts):
+            assert np.abs(a.thresholds - b.thresholds).max() <= 1e-5 * scale
+        for mode in ("kill", "lenient"):
+            _, st = B.detect(cal, pyr, -np.inf, pruning=True, part_prune_mode=mode,
+                             collect_maps=True)
+            for lvl, hyp in hyps:
+                li = hyp.level
+                lm = st.prune_maps[li]
+                iy, ix = hyp.root[0] - lm["rect"][0], hyp.root[1] - lm["rect"][2]
+                assert lm["root_prune_rank"][iy, ix] == 0
+                assert not lm["part_prune_rank"][:, iy, ix].any()

@@ -97,6 +97,8 @@ def test_validation_errors_mirror_reference_before_any_device_work():
         B.detect(dec, [], 0.0, pruning=True)
     with pytest.raises(B.ValidationError, match="pyramid level 0"):
         B.detect(dec, [np.zeros((5, 5, 4))], 0.0)
+    with pytest.raises(B.ValidationError, match="zero positives"):
+        B.calibrate_thresholds(dec, [])
     bad = B.PartModel(np.zeros((2, 2, 3)), (B.PartSpec(np.zeros((2, 2, 3)), (0, 0),
                                                         (0, 0, -1.0, 0), 0),))
     with pytest.raises(B.ValidationError, match="c_dxx"):

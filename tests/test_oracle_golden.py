@@ -232,3 +232,48 @@ def test_r_star_window_equals_unbounded():
     b = O.placement_grid(s, (0, 0), de, 60, rect)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_oracle_pruned_detect_matches_reference_golden(oracle):
+    """detect(pruning=True) restatement vs the reference itself, both part
+    modes: detections, prune-rank maps and every counter identical; the
+    calibration restatement reproduces the reference's thresholds."""
+    from conftest import golden_pruned
+
+    g = load_golden("detect_pruned.npz")
+    pruned_any = 0
+    for k in range(int(g["n"])):
+        dec, pyr, planted, tau = golden_pruned(g, k)
+        from paper_1707_03268_b200.types import Hypothesis
+
+        pos = [(pyr[int(p[0])], Hypothesis(level=int(p[0]), root=(int(p[1]), int(p[2])),
+                                           parts=tuple((int(p[3 + 2 * i]), int(p[4 + 2 * i]))
+                                                       for i in range(len(dec.parts)))))
+               for p in planted]
+        rt, pt = oracle.calibrate_thresholds(dec, pos)
+        assert np.array_equal(rt, dec.root_thresholds)
+        for a, p in zip(pt, dec.parts):
+            assert np.array_equal(a, p.thresholds)
+        for mode in ("kill", "lenient"):
+            m = f"q{k}_{mode}"
+            dets, st, maps = oracle.detect_pruned(dec, pyr, tau, part_prune_mode=mode)
+            ref = g[f"{m}_dets"]
+            assert len(dets) == ref.shape[0], (k, mode)
+            for d, r in zip(dets, ref):
+                assert (d[0], *d[1]) == tuple(int(v) for v in r[:3])
+                assert [c for pp in d[2] for c in pp] == [int(v) for v in r[3:-1]]
+                assert d[3] == r[-1]
+            assert [st["positions_examined"], st["positions_killed_by_parts"],
+                    st["multiplications"]] == list(g[f"{m}_stats"])
+            R = g[f"{m}_root_pruned"].size
+            assert [st["positions_pruned_at_rank"].get(r, 0) for r in range(1, R + 1)] == \
+                list(g[f"{m}_root_pruned"])
+            assert [st["part_pruned_at_rank"].get(r, 0) for r in range(1, R + 1)] == \
+                list(g[f"{m}_part_pruned"])
+            for li, lm in enumerate(maps):
+                if lm["rect"] is None:
+                    continue
+                assert np.array_equal(lm["root_prune_rank"], g[f"{m}_rootrank{li}"])
+                assert np.array_equal(lm["part_prune_rank"], g[f"{m}_partrank{li}"])
+            pruned_any += sum(st["positions_pruned_at_rank"].values())
+    assert pruned_any > 0  # the fixtures exercise pruning
