@@ -19,6 +19,7 @@ from .correlation import (ScoreMap, correlate3_cp, correlate3_full, cp_multiplic
 from .detection import (_placement_grid, best_part_placement, calibrate_thresholds,
                         cp_score_hypothesis, deformation_penalty, dense_detect, detect,
                         score_hypothesis, validate)
+from .evaluation import RocPoint, match_detections, nms, nms_records, roc_eval
 from .errors import CpdetectError, DeviceError, FormatError, NumericError, ValidationError
 from .pipeline import PyramidScorer, cores_from_stacked
 from .types import (CPModel, DecomposedModel, DecomposedPart, Detection, DetectStats,
@@ -33,6 +34,7 @@ __all__ = [
     "best_part_placement", "cores_from_stacked", "correlate3_cp", "correlate3_full",
     "cp_multiplications", "cp_partial_stack", "cp_score_hypothesis", "deformation_penalty",
     "dense_detect", "detect",
-    "calibrate_thresholds", "full_multiplications", "score_hypothesis", "theoretical_gain",
+    "calibrate_thresholds", "nms", "nms_records", "match_detections", "roc_eval",
+    "RocPoint", "full_multiplications", "score_hypothesis", "theoretical_gain",
     "valid_support", "validate",
 ]

@@ -340,8 +340,49 @@ def gen_detect_pruned():
     save("detect_pruned.npz", **out)
 
 
+def gen_roc():
+    """roc_eval (evaluation.py:102-162) on three compact scenes: dense model,
+    decomposed (full rank 2 of a rank-2 model) and calibrated pruning."""
+    from cpdetect.evaluation import roc_eval
+
+    out = {}
+    fast = AlsOptions(max_iterations=100, restarts=1, seed=0)
+    model = gen_model(root_size=(3, 4), part_size=(4, 4), n_parts=2, channels=6, low_rank=2,
+                      search_radius=2, bias=0.1, seed=21)
+    scenes = [gen_scene(model, n_objects=2, noise=0.05, level_shapes=((30, 34),), seed=31 + i)
+              for i in range(3)]
+    dec = decompose_model(model, ranks=2, opts=fast)
+    positives = [(sc.pyramid[lvl], hyp) for sc in scenes for lvl, hyp in sc.planted]
+    cal = D.calibrate_thresholds(dec, positives)
+    taus = np.linspace(-2.0, 6.0, 9)
+    out["taus"] = taus
+    for si, sc in enumerate(scenes):
+        out[f"s{si}_level0"] = sc.pyramid[0]
+        out[f"s{si}_planted"] = np.array([[lvl, *hyp.root, *[c for pp in hyp.parts for c in pp]]
+                                          for lvl, hyp in sc.planted])
+    out["root"] = model.root
+    for pi, p in enumerate(model.parts):
+        out[f"part{pi}"] = p.filter
+        out[f"part{pi}_anchor"] = np.array(p.anchor)
+        out[f"part{pi}_def"] = np.array(p.deformation)
+        out[f"part{pi}_r"] = np.int64(p.search_radius)
+        out[f"part{pi}_thr"] = np.asarray(cal.parts[pi].thresholds)
+        out.update(cp_arrays(f"pcp{pi}", dec.parts[pi].cp))
+    out["bias"] = np.float64(model.bias)
+    out["root_thr"] = np.asarray(cal.root_thresholds)
+    out.update(cp_arrays("rcp", dec.root_cp))
+
+    def pts(points):
+        return np.array([[p.tau, p.misdetection_rate, p.false_positives_per_scene,
+                          p.false_positives_per_window] for p in points])
+    out["roc_dense"] = pts(roc_eval(model, scenes, taus))
+    out["roc_cp"] = pts(roc_eval(dec, scenes, taus))
+    out["roc_pruned"] = pts(roc_eval(cal, scenes, taus, pruning=True))
+    save("roc.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["correlation", "placement", "detect_compact", "cfg1", "cfg2_sample",
-                             "detect_pruned"]
+                             "detect_pruned", "roc"]
     for w in which:
         globals()["gen_" + w]()

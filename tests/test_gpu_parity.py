@@ -593,3 +593,39 @@ def test_gpu_calibration_never_prunes_its_positives():
                 iy, ix = hyp.root[0] - lm["rect"][0], hyp.root[1] - lm["rect"][2]
                 assert lm["root_prune_rank"][iy, ix] == 0
                 assert not lm["part_prune_rank"][:, iy, ix].any()
+
+
+def test_roc_eval_matches_reference_golden():
+    """roc_eval over the GPU detectors equals the reference's sweep: dense,
+    decomposed, and pruned with thresholds calibrated on the GPU maps."""
+    from types import SimpleNamespace
+
+    from conftest import _Dec, _Part
+    from paper_1707_03268_b200.evaluation import roc_eval
+
+    g = load_golden("roc.npz")
+    nparts = 2
+    scenes = []
+    for si in range(3):
+        pl = g[f"s{si}_planted"]
+        planted = [(int(p[0]), B.Hypothesis(level=int(p[0]), root=(int(p[1]), int(p[2])),
+                                            parts=tuple((int(p[3 + 2 * i]), int(p[4 + 2 * i]))
+                                                        for i in range(nparts))))
+                   for p in pl]
+        scenes.append(SimpleNamespace(pyramid=[g[f"s{si}_level0"]], planted=planted))
+    dense = B.PartModel(g["root"], tuple(
+        B.PartSpec(g[f"part{i}"], tuple(g[f"part{i}_anchor"]), tuple(g[f"part{i}_def"]),
+                   int(g[f"part{i}_r"])) for i in range(nparts)), float(g["bias"]))
+    parts = [_Part(golden_cp(g, f"pcp{i}"), g[f"part{i}_anchor"], g[f"part{i}_def"],
+                   g[f"part{i}_r"], None) for i in range(nparts)]
+    dec = _Dec(golden_cp(g, "rcp"), parts, g["bias"], None)
+    taus = g["taus"]
+
+    def pts(points):
+        return np.array([[p.tau, p.misdetection_rate, p.false_positives_per_scene,
+                          p.false_positives_per_window] for p in points])
+    assert np.array_equal(pts(roc_eval(dense, scenes, taus)), g["roc_dense"])
+    assert np.array_equal(pts(roc_eval(dec, scenes, taus)), g["roc_cp"])
+    positives = [(sc.pyramid[lvl], hyp) for sc in scenes for lvl, hyp in sc.planted]
+    cal = B.calibrate_thresholds(dec, positives)
+    assert np.array_equal(pts(roc_eval(cal, scenes, taus, pruning=True)), g["roc_pruned"])
