@@ -261,6 +261,25 @@ int dpm_prune_ranks(const float* S, const int64_t* map_offs, const double* thr,
                     const dpm_prune_job* jobs, int njobs, int64_t nblocks, uint8_t* out,
                     void* stream);
 
+/* ------------------------------------------------------- mixture max
+ * SURVEY.md §8(f) row 3 (the reference has no combination rule; SPEC asks
+ * for a max).  Job = one (image, root level): the union rectangle of its
+ * component assemblies (listed as indices into `ajobs` at
+ * members[member0 .. member0+nmembers)); for every root position, best =
+ * max over the components whose rectangle holds it of their totals (ties to
+ * the lowest component), comp = that component, or (-inf, -1). */
+typedef struct {
+  int64_t out_off;   /* offset of the job's [hu][wu] outputs                */
+  int32_t ry0, ry1, rx0, rx1;
+  int32_t member0, nmembers;
+  int32_t block0;    /* set by dpm_mixture_prepare                          */
+  int32_t pad;
+} dpm_mix_job;
+int64_t dpm_mixture_prepare(dpm_mix_job* jobs_host, int njobs);
+int dpm_mixture_max(const double* total, const dpm_asm_job* ajobs, const int32_t* members,
+                    const dpm_mix_job* jobs, int njobs, int64_t nblocks, double* best,
+                    int32_t* comp, void* stream);
+
 /* ----------------------------------------------------- micro-benchmark
  * FP32 FFMA peak probe used by bench.py for the K2 roofline denominator:
  * `iters` dependent-chain-free FFMA blocks on every SM; returns via

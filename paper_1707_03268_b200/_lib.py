@@ -13,7 +13,7 @@ import numpy as np
 from .errors import DeviceError, NumericError, ValidationError
 
 __all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "ASM_JOB",
-           "DETECTION", "PLACE_RANGE", "PRUNE_JOB", "LIB_PATH", "MAX_PARTS", "table_ptr"]
+           "DETECTION", "PLACE_RANGE", "PRUNE_JOB", "MIX_JOB", "LIB_PATH", "MAX_PARTS", "table_ptr"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdpm_b200.so")
 MAX_PARTS = 16
@@ -50,8 +50,13 @@ PRUNE_JOB = np.dtype([("out_off", "<i8"), ("offs0", "<i4"), ("thr0", "<i4"), ("R
                       ("rx0", "<i4"), ("rx1", "<i4"), ("ay", "<i4"), ("ax", "<i4"),
                       ("scale", "<i4"), ("radius", "<i4"), ("block0", "<i4")], align=True)
 
+MIX_JOB = np.dtype([("out_off", "<i8"), ("ry0", "<i4"), ("ry1", "<i4"), ("rx0", "<i4"),
+                    ("rx1", "<i4"), ("member0", "<i4"), ("nmembers", "<i4"), ("block0", "<i4"),
+                    ("pad", "<i4")], align=True)
+
 _SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 88, "ASM_JOB": 88,
-          "DETECTION": 96, "PLACE_RANGE": 16, "PRUNE_JOB": 64}
+          "DETECTION": 96, "PLACE_RANGE": 16, "PRUNE_JOB": 64,
+          "MIX_JOB": 40}
 for _n, _s in _SIZES.items():
     assert globals()[_n].itemsize == _s, (_n, globals()[_n].itemsize)
 
@@ -83,6 +88,8 @@ _SIGNATURES = {
                          _vp, _vp]),
     "dpm_prune_prepare": (_i64, [_vp, _i32]),
     "dpm_prune_ranks": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
+    "dpm_mixture_prepare": (_i64, [_vp, _i32]),
+    "dpm_mixture_max": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
     "dpm_ffma_probe": (_i32, [_vp, _i32, _vp, _vp]),
 }
 

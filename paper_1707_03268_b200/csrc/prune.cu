@@ -84,3 +84,62 @@ extern "C" int dpm_prune_ranks(const float* S, const int64_t* map_offs, const do
   DPM_LAUNCHED("prune_ranks_kernel");
   return DPM_OK;
 }
+
+// ------------------------------------------------------------ mixture max
+// Per (image, root level): for every root position of the union rectangle
+// of the level's component assemblies, the max over components of their
+// totals at that position (components whose rectangle holds it), ties to the
+// lowest component index (the reference defines no
+// combination, SPEC.md:358 asks for a max).
+namespace dpm {
+__global__ void __launch_bounds__(256)
+mixture_max_kernel(const double* __restrict__ total, const dpm_asm_job* __restrict__ ajobs,
+                   const int32_t* __restrict__ members, const dpm_mix_job* __restrict__ jobs,
+                   int njobs, double* __restrict__ best, int32_t* __restrict__ comp) {
+  const int jid = find_job(jobs, njobs, blockIdx.x);
+  const dpm_mix_job j = jobs[jid];
+  const int hu = j.ry1 - j.ry0 + 1, wu = j.rx1 - j.rx0 + 1;
+  const int64_t e = (int64_t)(blockIdx.x - j.block0) * 256 + threadIdx.x;
+  if (e >= (int64_t)hu * wu) return;
+  const int ry = j.ry0 + (int)(e / wu), rx = j.rx0 + (int)(e % wu);
+  double b = -INFINITY;
+  int bc = -1;
+  for (int m = 0; m < j.nmembers; ++m) {
+    const dpm_asm_job a = ajobs[members[j.member0 + m]];
+    if (ry < a.ry0 || ry > a.ry1 || rx < a.rx0 || rx > a.rx1) continue;
+    const double v = total[a.total_off + (int64_t)(ry - a.ry0) * (a.rx1 - a.rx0 + 1) + (rx - a.rx0)];
+    if (bc < 0 || v > b || (v == b && a.component < bc)) {
+      b = v;
+      bc = a.component;
+    }
+  }
+  best[j.out_off + e] = b;
+  comp[j.out_off + e] = bc;
+}
+}  // namespace dpm
+
+extern "C" int64_t dpm_mixture_prepare(dpm_mix_job* jobs, int njobs) {
+  DPM_REQUIRE(njobs >= 0 && (njobs == 0 || jobs), "dpm_mixture_prepare: bad table");
+  int64_t blocks = 0;
+  for (int i = 0; i < njobs; ++i) {
+    dpm_mix_job& j = jobs[i];
+    DPM_REQUIRE(j.ry1 >= j.ry0 && j.rx1 >= j.rx0 && j.nmembers >= 0 && j.member0 >= 0 &&
+                    j.out_off >= 0,
+                "dpm_mixture_prepare: job %d has a bad rectangle / member range", i);
+    j.block0 = (int32_t)blocks;
+    blocks += ((int64_t)(j.ry1 - j.ry0 + 1) * (j.rx1 - j.rx0 + 1) + 255) / 256;
+  }
+  return blocks;
+}
+
+extern "C" int dpm_mixture_max(const double* total, const dpm_asm_job* ajobs,
+                               const int32_t* members, const dpm_mix_job* jobs, int njobs,
+                               int64_t nblocks, double* best, int32_t* comp, void* stream) {
+  DPM_REQUIRE(total && ajobs && members && jobs && best && comp, "dpm_mixture_max: null pointer");
+  DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_mixture_max: nblocks");
+  if (njobs == 0 || nblocks == 0) return DPM_OK;
+  mixture_max_kernel<<<(unsigned)nblocks, 256, 0, as_stream(stream)>>>(total, ajobs, members, jobs,
+                                                                       njobs, best, comp);
+  DPM_LAUNCHED("mixture_max_kernel");
+  return DPM_OK;
+}

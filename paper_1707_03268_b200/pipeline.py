@@ -171,6 +171,57 @@ class PyramidScorer:
     def detections(self):
         return self.plan.detections()
 
+    def mixture(self, stream=None):
+        """Per-root max over mixture components on
+        the device (``dpm_mixture_max``), after ``run()`` / ``score_batch()``.
+
+        For every (image, root level) the union rectangle of its components'
+        root rectangles; at each root position the best total among the
+        components whose rectangle holds it (ties to the lowest component,
+        -inf / -1 where none does).  Returns {(image, root_level): (rect,
+        best float64 [hu][wu], component int32 [hu][wu])} as device tensors."""
+        from . import _lib
+        from .device import stream_handle, upload_table
+
+        plan = self.plan
+        if plan.total_size == 0:
+            raise ValidationError("mixture() needs the totals output")
+        t = plan.torch
+        if not hasattr(self, "_mix"):
+            aj = plan._asm_jobs
+            groups = {}
+            for idx in range(len(aj)):
+                key = (int(aj["image"][idx]), int(aj["level"][idx]))
+                groups.setdefault(key, []).append(idx)
+            jobs, members, keys, off = [], [], [], 0
+            for key, idxs in sorted(groups.items()):
+                ry0 = int(min(aj["ry0"][idxs])); ry1 = int(max(aj["ry1"][idxs]))
+                rx0 = int(min(aj["rx0"][idxs])); rx1 = int(max(aj["rx1"][idxs]))
+                jobs.append((off, ry0, ry1, rx0, rx1, len(members), len(idxs), 0, 0))
+                members.extend(idxs)
+                keys.append((key, (ry0, ry1, rx0, rx1), off))
+                off += (ry1 - ry0 + 1) * (rx1 - rx0 + 1)
+            jobs = np.array(jobs, dtype=_lib.MIX_JOB)
+            nblk = _lib.check(_lib.lib().dpm_mixture_prepare(_lib.table_ptr(jobs), len(jobs)),
+                              "mixture")
+            dev = plan.device
+            self._mix = dict(jobs=upload_table(jobs, dev), njobs=len(jobs), nblk=nblk,
+                             members=t.tensor(members, dtype=t.int32, device=dev),
+                             ajobs=upload_table(np.ascontiguousarray(aj), dev), keys=keys,
+                             best=t.empty(max(off, 1), dtype=t.float64, device=dev),
+                             comp=t.empty(max(off, 1), dtype=t.int32, device=dev))
+        m = self._mix
+        _lib.check(_lib.lib().dpm_mixture_max(
+            plan.totals.data_ptr(), m["ajobs"].data_ptr(), m["members"].data_ptr(),
+            m["jobs"].data_ptr(), m["njobs"], m["nblk"], m["best"].data_ptr(),
+            m["comp"].data_ptr(), stream_handle(stream)), "mixture")
+        out = {}
+        for (img, lvl), rect, off in m["keys"]:
+            hu, wu = rect[1] - rect[0] + 1, rect[3] - rect[2] + 1
+            out[(img, lvl)] = (rect, m["best"][off:off + hu * wu].view(hu, wu),
+                               m["comp"][off:off + hu * wu].view(hu, wu))
+        return out
+
     # accounting (BASELINE.md §3)
     def evals_per_image(self):
         return self.plan.evals()

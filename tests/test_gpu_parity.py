@@ -629,3 +629,33 @@ def test_roc_eval_matches_reference_golden():
     positives = [(sc.pyramid[lvl], hyp) for sc in scenes for lvl, hyp in sc.planted]
     cal = B.calibrate_thresholds(dec, positives)
     assert np.array_equal(pts(roc_eval(cal, scenes, taus, pruning=True)), g["roc_pruned"])
+
+
+def test_mixture_max_matches_host_composition():
+    """dpm_mixture_max (per-root max over components, ties to the lowest
+    component) equals the same rule applied to the per-component totals, on
+    config 5 (components with different root shapes) at sampled levels."""
+    wl = synth.workload(5)
+    C, G = _shared(5, 8)
+    sc = PyramidScorer(wl.bank, C, G, wl.pyramid, n_images=1)
+    sc.load_image(0, synth.hog_pyramid(5, 0, wl.pyramid))
+    sc.run()
+    mix = sc.mixture()
+    res = sc.results(0)
+    by_level = {}
+    for r in res:
+        by_level.setdefault(r["root_level"], []).append(r)
+    assert set(k[1] for k in mix) == set(by_level)
+    for lvl, recs in by_level.items():
+        rect, best, comp = mix[(0, lvl)]
+        best, comp = best.cpu().numpy(), comp.cpu().numpy()
+        ry0, ry1, rx0, rx1 = rect
+        want = np.full(best.shape, -np.inf)
+        wcomp = np.full(best.shape, -1)
+        for r in sorted(recs, key=lambda r: r["component"]):
+            a0, a1, b0, b1 = r["rect"]
+            sub = (slice(a0 - ry0, a1 - ry0 + 1), slice(b0 - rx0, b1 - rx0 + 1))
+            better = (wcomp[sub] < 0) | (r["scores"] > want[sub])
+            want[sub] = np.where(better, r["scores"], want[sub])
+            wcomp[sub] = np.where(better, r["component"], wcomp[sub])
+        assert np.array_equal(best, want) and np.array_equal(comp, wcomp), lvl
