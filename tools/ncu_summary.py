@@ -35,6 +35,9 @@ KEYS = {
 
 SHORT = {
     "place_assemble_kernel": "place_assemble_kernel",
+    "place_ranges_kernel": "place_ranges_kernel",
+    "gdt_x_kernel": "gdt_x_kernel",
+    "gdt_y_kernel": "gdt_y_kernel",
     "corr_tc_kernel": "corr_tc_kernel",
     "corr_kernel": "corr_kernel",
     "project_kernel": "project_kernel",
