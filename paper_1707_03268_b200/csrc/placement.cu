@@ -105,27 +105,40 @@ __device__ __forceinline__ uint32_t pack_pos(int y, int x) {
 constexpr float OUT_SENTINEL = -1.0e37f;  // staged cells outside the map
 constexpr float NONE_BELOW = -1.0e36f;    // m1 below this: no candidate inside the map
 
-__device__ __forceinline__ float enc_idx(float v, int code) {
-  return __int_as_float((__float_as_int(v) & ~63) | code);
+// (bits(v) & mask) | code in ONE lop3 (LUT 0xEA = (a & b) | c): the mask
+// lives in a register so the code can be the instruction's immediate
+template <int CODE>
+__device__ __forceinline__ float enc_idx(float v, uint32_t mask) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(__float_as_uint(v)), "r"(mask), "n"(CODE));
+  return __uint_as_float(r);
 }
 
 // Window of 2R+1 candidates src[d*STRIDE] + np[d], d = -R..R (pointers at
 // d = 0); m1 = top encoded value (code d + R in its low bits), m2 = best of
 // the others.
-template <int R, int STRIDE>
-__device__ __forceinline__ void screen_window(const float* __restrict__ src,
-                                              const float* __restrict__ np, float& m1, float& m2) {
-  m1 = -INFINITY;
-  m2 = -INFINITY;
-#pragma unroll
-  for (int d = -R; d < R; d += 2) {
-    const float a = enc_idx(src[d * STRIDE] + np[d], d + R);
-    const float b = enc_idx(src[(d + 1) * STRIDE] + np[d + 1], d + 1 + R);
+template <int R, int STRIDE, int D>
+__device__ __forceinline__ void screen_pairs(const float* __restrict__ src,
+                                             const float* __restrict__ np, uint32_t mask,
+                                             float& m1, float& m2) {
+  if constexpr (D < R) {
+    const float a = enc_idx<D + R>(src[D * STRIDE] + np[D], mask);
+    const float b = enc_idx<D + 1 + R>(src[(D + 1) * STRIDE] + np[D + 1], mask);
     const float hi = fmaxf(a, b), lo = fminf(a, b);
     m2 = fmaxf(m2, fmaxf(lo, fminf(m1, hi)));
     m1 = fmaxf(m1, hi);
+    screen_pairs<R, STRIDE, D + 2>(src, np, mask, m1, m2);
   }
-  const float c = enc_idx(src[R * STRIDE] + np[R], 2 * R);
+}
+
+template <int R, int STRIDE>
+__device__ __forceinline__ void screen_window(const float* __restrict__ src,
+                                              const float* __restrict__ np, uint32_t mask,
+                                              float& m1, float& m2) {
+  m1 = -INFINITY;
+  m2 = -INFINITY;
+  screen_pairs<R, STRIDE, -R>(src, np, mask, m1, m2);
+  const float c = enc_idx<2 * R>(src[R * STRIDE] + np[R], mask);
   m2 = fmaxf(m2, fminf(m1, c));
   m1 = fmaxf(m1, c);
 }
@@ -133,11 +146,11 @@ __device__ __forceinline__ void screen_window(const float* __restrict__ src,
 // runtime radius -> unrolled instantiation (radius <= RCAP on the staged path)
 template <int STRIDE>
 __device__ __forceinline__ void screen_dispatch(int r, const float* __restrict__ src,
-                                                const float* __restrict__ np, float& m1,
-                                                float& m2) {
+                                                const float* __restrict__ np, uint32_t mask,
+                                                float& m1, float& m2) {
   switch (r) {
 #define DPM_SCREEN_CASE(R) \
-  case R: screen_window<R, STRIDE>(src, np, m1, m2); break;
+  case R: screen_window<R, STRIDE>(src, np, mask, m1, m2); break;
     DPM_SCREEN_CASE(0) DPM_SCREEN_CASE(1) DPM_SCREEN_CASE(2) DPM_SCREEN_CASE(3)
     DPM_SCREEN_CASE(4) DPM_SCREEN_CASE(5) DPM_SCREEN_CASE(6) DPM_SCREEN_CASE(7)
     DPM_SCREEN_CASE(8) DPM_SCREEN_CASE(9) DPM_SCREEN_CASE(10) DPM_SCREEN_CASE(11)
@@ -202,6 +215,9 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   const int ry_lo = aj.ry0 + ty0;
   const int ry_hi = aj.ry0 + min(ty0 + PT_H, hr) - 1;
   const int rx_lo = aj.rx0 + tx0;
+  // ~63 from a value the compiler cannot fold (najobs > 0), so the index
+  // code, not the mask, is each encoding lop3's immediate
+  const uint32_t code_mask = ~63u | ((uint32_t)najobs >> 31);
 
   double tot[RPT];
 #pragma unroll
@@ -291,7 +307,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     for (int r = warp; r < nrows; r += PT_WARPS) {
       const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
       float m1, m2;
-      screen_dispatch<1>(jr.rx, srow, npx, m1, m2);
+      screen_dispatch<1>(jr.rx, srow, npx, code_mask, m1, m2);
       // the y-pass screen only needs the winner's value to the screening
       // accuracy; exact values are recomputed from xsv for y winners and ties
       int xi = (__float_as_int(m1) & 63) - jr.rx;
@@ -327,7 +343,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       const int r0 = cy - yb0;  // band row of dy = 0
       const float* xcol = sh.x32 + r0 * PT_W + lane;
       float m1, m2;
-      screen_dispatch<PT_W>(jr.ry, xcol, npy, m1, m2);
+      screen_dispatch<PT_W>(jr.ry, xcol, npy, code_mask, m1, m2);
       auto exact = [&](int dy) -> double {
         const int row = (r0 + dy) * PT_W + lane;
         const int dx = sh.xdx[row];
