@@ -50,7 +50,8 @@ constexpr int PT_H = 64;                                  // root rows per tile
 constexpr int PT_THREADS = 512;
 constexpr int PT_WARPS = PT_THREADS / 32;
 constexpr int BAND_MAX = 2 * (PT_H - 1) + 1 + 2 * RCAP;   // 159 (scale <= 2)
-constexpr int COLS_PITCH = 2 * (PT_W - 1) + 1 + 2 * RCAP + 2;  // 97
+// even, so band rows start 8-byte aligned (packed pairs in the x pass)
+constexpr int COLS_PITCH = 2 * (PT_W - 1) + 1 + 2 * RCAP + 3;  // 98
 
 __device__ __forceinline__ double pen(double c1, double c2, int d) {
   const double dd = (double)d;
@@ -131,26 +132,58 @@ __device__ __forceinline__ void screen_pairs(const float* __restrict__ src,
   }
 }
 
-template <int R, int STRIDE>
+// Contiguous candidates (x pass at scale 2): src + D and np + D are 8-byte
+// aligned for every pair start D = -R, -R+2, ..., so each pair is one
+// 64-bit load per operand and one packed add.f32x2.
+template <int R, int D>
+__device__ __forceinline__ void screen_pairs_packed(const float* __restrict__ src,
+                                                    const float* __restrict__ np, uint32_t mask,
+                                                    float& m1, float& m2) {
+  if constexpr (D < R) {
+    const unsigned long long s2 = *reinterpret_cast<const unsigned long long*>(src + D);
+    const unsigned long long p2 = *reinterpret_cast<const unsigned long long*>(np + D);
+    unsigned long long v2;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v2) : "l"(s2), "l"(p2));
+    float va, vb;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(va), "=f"(vb) : "l"(v2));
+    const float a = enc_idx<D + R>(va, mask);
+    const float b = enc_idx<D + 1 + R>(vb, mask);
+    const float hi = fmaxf(a, b), lo = fminf(a, b);
+    m2 = fmaxf(m2, fmaxf(lo, fminf(m1, hi)));
+    m1 = fmaxf(m1, hi);
+    screen_pairs_packed<R, D + 2>(src, np, mask, m1, m2);
+  }
+}
+
+// np_odd: the same table shifted by one element, so that for odd R the pair
+// starts are 8-byte aligned too (packed path only)
+template <int R, int STRIDE, bool PACKED>
 __device__ __forceinline__ void screen_window(const float* __restrict__ src,
-                                              const float* __restrict__ np, uint32_t mask,
+                                              const float* __restrict__ np,
+                                              const float* __restrict__ np_odd, uint32_t mask,
                                               float& m1, float& m2) {
   m1 = -INFINITY;
   m2 = -INFINITY;
-  screen_pairs<R, STRIDE, -R>(src, np, mask, m1, m2);
+  if constexpr (PACKED) {
+    const float* npp = (R & 1) ? np_odd : np;
+    screen_pairs_packed<R, -R>(src, npp, mask, m1, m2);
+  } else {
+    screen_pairs<R, STRIDE, -R>(src, np, mask, m1, m2);
+  }
   const float c = enc_idx<2 * R>(src[R * STRIDE] + np[R], mask);
   m2 = fmaxf(m2, fminf(m1, c));
   m1 = fmaxf(m1, c);
 }
 
 // runtime radius -> unrolled instantiation (radius <= RCAP on the staged path)
-template <int STRIDE>
+template <int STRIDE, bool PACKED>
 __device__ __forceinline__ void screen_dispatch(int r, const float* __restrict__ src,
-                                                const float* __restrict__ np, uint32_t mask,
+                                                const float* __restrict__ np,
+                                                const float* __restrict__ np_odd, uint32_t mask,
                                                 float& m1, float& m2) {
   switch (r) {
 #define DPM_SCREEN_CASE(R) \
-  case R: screen_window<R, STRIDE>(src, np, mask, m1, m2); break;
+  case R: screen_window<R, STRIDE, PACKED>(src, np, np_odd, mask, m1, m2); break;
     DPM_SCREEN_CASE(0) DPM_SCREEN_CASE(1) DPM_SCREEN_CASE(2) DPM_SCREEN_CASE(3)
     DPM_SCREEN_CASE(4) DPM_SCREEN_CASE(5) DPM_SCREEN_CASE(6) DPM_SCREEN_CASE(7)
     DPM_SCREEN_CASE(8) DPM_SCREEN_CASE(9) DPM_SCREEN_CASE(10) DPM_SCREEN_CASE(11)
@@ -190,6 +223,7 @@ struct __align__(16) PlaceSmem {
   float xsv[BAND_MAX * PT_W];      // x-pass winners' S values (exact y values)
   int8_t xdx[BAND_MAX * PT_W];     // x-pass winning dx
   float npx[2][2 * RCAP + 4];      // -pen_x(dx) in FP32 (screening only), by part parity
+  float npx_odd[2][2 * RCAP + 4];  // the same, shifted by one element (packed pairs, odd r)
   float npy[2][2 * RCAP + 4];
 };
 
@@ -261,7 +295,11 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     if (threadIdx.x >= PT_THREADS - 2 * (2 * RCAP + 1)) {  // last warps: penalty tables
       const int t = threadIdx.x - (PT_THREADS - 2 * (2 * RCAP + 1));
       const int d = (t % (2 * RCAP + 1)) - RCAP;
-      if (t < 2 * RCAP + 1) sh.npx[buf][d + RCAP] = (float)(-pen(pj.cdx, pj.cdxx, d));
+      if (t < 2 * RCAP + 1) {
+        const float v = (float)(-pen(pj.cdx, pj.cdxx, d));
+        sh.npx[buf][d + RCAP] = v;
+        sh.npx_odd[buf][d + RCAP + 1] = v;
+      }
       else sh.npy[buf][d + RCAP] = (float)(-pen(pj.cdy, pj.cdyy, d));
     }
   };
@@ -304,10 +342,14 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
 
     // x pass: band row r (warp-strided), centre column = lane
     const float* npx = sh.npx[buf] + RCAP;
+    const float* npx_odd = sh.npx_odd[buf] + RCAP + 1;
     for (int r = warp; r < nrows; r += PT_WARPS) {
       const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
       float m1, m2;
-      screen_dispatch<1>(jr.rx, srow, npx, code_mask, m1, m2);
+      if (pj.scale == 2)  // 2*lane + even row base: pair starts are 8-byte aligned
+        screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
+      else
+        screen_dispatch<1, false>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
       // the y-pass screen only needs the winner's value to the screening
       // accuracy; exact values are recomputed from xsv for y winners and ties
       int xi = (__float_as_int(m1) & 63) - jr.rx;
@@ -343,7 +385,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       const int r0 = cy - yb0;  // band row of dy = 0
       const float* xcol = sh.x32 + r0 * PT_W + lane;
       float m1, m2;
-      screen_dispatch<PT_W>(jr.ry, xcol, npy, code_mask, m1, m2);
+      screen_dispatch<PT_W, false>(jr.ry, xcol, npy, npy, code_mask, m1, m2);
       auto exact = [&](int dy) -> double {
         const int row = (r0 + dy) * PT_W + lane;
         const int dx = sh.xdx[row];
