@@ -391,11 +391,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
 
 using namespace dpm;
 
+// Input-row ring depth: at least h + 2 (the h rows of an output row plus
+// slack), then as deep as shared memory allows (up to TC_MAX_RING), so the
+// producers run further ahead of the MMA warp and hide row-load latency.
+static int tc_ring(int h, int w, int R, int nf) {
+  const int N = (nf + 15) & ~15;
+  const int nq = R / 4;
+  const size_t b = ((size_t)h * w * nq * 2 * N * 16 + 1023) & ~(size_t)1023;
+  const size_t slot = 2ull * nq * (TC_M + w - 1) * 16;
+  const size_t fixed = b + (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16 + 15;
+  int ring = h + 2 <= TC_MAX_RING ? h + 2 : TC_MAX_RING;
+  while (ring < TC_MAX_RING && fixed + (ring + 1) * slot <= 227 * 1024) ++ring;
+  return ring;
+}
+
 extern "C" size_t dpm_correlate_tc_smem(int h, int w, int R, int nf) {
   const int N = (nf + 15) & ~15;
   const int nq = R / 4;
   const size_t b = (size_t)h * w * nq * 2 * N * 16;
-  const int ring = h + 2 <= TC_MAX_RING ? h + 2 : TC_MAX_RING;
+  const int ring = tc_ring(h, w, R, nf);
   const size_t slot = 2ull * nq * (TC_M + w - 1) * 16;
   return ((b + 1023) & ~(size_t)1023) + ((ring * slot + 15) & ~(size_t)15) +
          (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
@@ -417,7 +431,7 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
   int dev = 0, sms = 148;
   DPM_CUDA(cudaGetDevice(&dev));
   DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  TcArgs a{P, Gtc, S, jobs, strips, nstrips, h, w, R, N, h + 2, 0, 0, ranges};
+  TcArgs a{P, Gtc, S, jobs, strips, nstrips, h, w, R, N, tc_ring(h, w, R, nf), 0, 0, ranges};
   a.acc_cols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
   void (*fn)(const TcArgs) = N <= 16 ? corr_tc_kernel<16, 0, 0>
