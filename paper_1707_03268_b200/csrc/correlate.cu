@@ -71,6 +71,7 @@ struct CorrArgs {
   int nwf, nwy;
   int w_max;
   int R_max;
+  int nf_max;
   uint32_t* ranges;
 };
 
@@ -123,11 +124,150 @@ __device__ __forceinline__ void stage_g(float* sG, const CorrArgs& a, const dpm_
   }
 }
 
+// One rank chunk of a tile: every warp accumulates its MP output rows x NF
+// filters over the staged P chunk (nr ranks) and core chunk.
+template <int FH, int NF>
+__device__ __forceinline__ void chunk_fma(unsigned long long (&acc)[K2_MP][NF / 2],
+                                          const float* sP, const float* sG, int wy, int wf,
+                                          int lane, int nr, int w, int nfp, int TROWS,
+                                          int TPITCH) {
+  constexpr int MP = K2_MP;
+  constexpr int COL = MP + FH - 1;
+  constexpr int NP = NF / 2;
+  const float* pw = sP + (wy * MP) * TPITCH + lane;
+  const float* gw = sG + wf * NF;
+  const int gstride_i = w * nr * nfp;
+  for (int j = 0; j < w; ++j) {
+    for (int r = 0; r < nr; ++r) {
+      const float* pc = pw + r * TROWS * TPITCH + j;
+      float col[COL];
+#pragma unroll
+      for (int q = 0; q < COL; ++q) col[q] = pc[q * TPITCH];
+      const float* gp = gw + (j * nr + r) * nfp;
+#pragma unroll
+      for (int i = 0; i < FH; ++i) {
+        float g[NF];
+        load_g<NF>(g, gp + i * gstride_i);
+        unsigned long long g2[NP];
+#pragma unroll
+        for (int f = 0; f < NP; ++f) g2[f] = pack2(g[2 * f], g[2 * f + 1]);
+#pragma unroll
+        for (int p = 0; p < MP; ++p)
+#pragma unroll
+          for (int f = 0; f < NP; ++f) ffma2(acc[p][f], col[p + i], g2[f]);
+      }
+    }
+  }
+}
+
+// epilogue: coalesced stores (lane = x), optional per-map range fold
+template <int FH, int NF>
+__device__ __forceinline__ void tile_epilogue(unsigned long long (&acc)[K2_MP][NF / 2],
+                                              const CorrArgs& a, const dpm_corr_job& job, int x0,
+                                              int y0, int wy, int wf, int lane) {
+  constexpr int MP = K2_MP;
+  constexpr int NP = NF / 2;
+  const int ho = job.H - FH + 1, wo = job.W - job.w + 1;
+  const int x = x0 + lane;
+  const int yb = y0 + wy * MP;
+  float out[MP][NF];
+#pragma unroll
+  for (int p = 0; p < MP; ++p)
+#pragma unroll
+    for (int f = 0; f < NP; ++f) unpack2(acc[p][f], out[p][2 * f], out[p][2 * f + 1]);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int fg = wf * NF + f;
+    float vmax = -INFINITY, vmin = INFINITY;
+    if (fg < job.nf) {
+      float* dst = a.S + job.s_off + (int64_t)fg * ho * wo;
+#pragma unroll
+      for (int p = 0; p < MP; ++p) {
+        const int y = yb + p;
+        if (x < wo && y < ho) {
+          dst[(int64_t)y * wo + x] = out[p][f];
+          vmax = fmaxf(vmax, out[p][f]);
+          vmin = fminf(vmin, out[p][f]);
+        }
+      }
+    }
+    if (a.ranges != nullptr && job.range_idx >= 0 && wf * NF + f < job.nf)
+      fold_range(a.ranges, job.range_idx + fg, vmax, vmin);
+  }
+}
+
+// Core chunk (ranks rc .. rc+nr of every tap) with 16-byte cp.async (cores
+// are 16-byte aligned, nf_pad % 8 == 0).
+__device__ __forceinline__ void stage_g_async(float* sG, const CorrArgs& a,
+                                              const dpm_corr_job& job, int FH, int rc, int nr) {
+  const int nfp = job.nf_pad;
+  const int per_ij4 = (nr * nfp) >> 2;
+  const int total4 = FH * job.w * per_ij4;
+  for (int e = threadIdx.x; e < total4; e += blockDim.x) {
+    const int ij = e / per_ij4, rem = e - ij * per_ij4;
+    const float* src = a.G + job.g_off + ((int64_t)ij * job.R + rc) * nfp + 4 * rem;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sG + ij * (nr * nfp) + 4 * rem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+  }
+}
+
+// Rank-chunk pipeline for R > K2_RCH: a step is (tile, rank chunk); the P and
+// core chunks of step s+1 are copied (cp.async) while step s computes, into
+// the other half of double buffers; accumulators live across a tile's chunks.
+template <int FH, int NF>
+__device__ __forceinline__ void corr_chunked(const CorrArgs& a, float* smem, int PBUF, int GBUF,
+                                             int TY, int TROWS, int TPITCH) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wf = warp % a.nwf, wy = warp / a.nwf;
+  float* sG0 = smem + 2 * PBUF;
+  auto issue = [&](int t, int rc, int buf) {
+    const dpm_corr_tile tl = a.tiles[t];
+    const dpm_corr_job jb = a.jobs[tl.job];
+    const int nr = min(K2_RCH, jb.R - rc);
+    stage_g_async(sG0 + buf * GBUF, a, jb, FH, rc, nr);  // joins stage_p's commit group
+    stage_p(smem + buf * PBUF, a, jb, rc, nr, tl.ty * TY, tl.tx * 32, TROWS, TPITCH);
+  };
+  int t = blockIdx.x, rc = 0, buf = 0;
+  if (t < a.ntiles) issue(t, 0, 0);
+  unsigned long long acc[K2_MP][NF / 2];
+  while (t < a.ntiles) {
+    const dpm_corr_tile tile = a.tiles[t];
+    const dpm_corr_job job = a.jobs[tile.job];
+    if (rc == 0) {
+#pragma unroll
+      for (int p = 0; p < K2_MP; ++p)
+#pragma unroll
+        for (int f = 0; f < NF / 2; ++f) acc[p][f] = 0ull;
+    }
+    int nt = t, nrc = rc + K2_RCH;
+    if (nrc >= job.R) {
+      nt = t + gridDim.x;
+      nrc = 0;
+    }
+    __syncthreads();  // every warp is done with buffer buf ^ 1 (step s-1)
+    if (nt < a.ntiles) {
+      issue(nt, nrc, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();  // step s resident for every warp
+    const int nr = min(K2_RCH, job.R - rc);
+    chunk_fma<FH, NF>(acc, smem + buf * PBUF, sG0 + buf * GBUF, wy, wf, lane, nr, job.w,
+                      job.nf_pad, TROWS, TPITCH);
+    if (nrc == 0 || nt != t)  // last chunk of this tile
+      tile_epilogue<FH, NF>(acc, a, job, tile.tx * 32, tile.ty * TY, wy, wf, lane);
+    t = nt;
+    rc = nrc;
+    buf ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 template <int FH, int NF>
 __global__ void __launch_bounds__(32 * K2_MAX_WARPS)
 corr_kernel(const CorrArgs a) {
   constexpr int MP = K2_MP;
-  constexpr int COL = MP + FH - 1;
   extern __shared__ __align__(16) float smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wf = warp % a.nwf, wy = warp / a.nwf;
@@ -135,6 +275,11 @@ corr_kernel(const CorrArgs a) {
   const int TROWS = TY + FH - 1;
   const int TPITCH = 32 + a.w_max - 1;
   const int PBUF = (K2_RCH * TROWS * TPITCH + 3) & ~3;
+  if (a.R_max > K2_RCH) {  // several rank chunks per tile: chunk pipeline
+    const int GBUF = (FH * a.w_max * K2_RCH * ((a.nf_max + 7) & ~7) + 3) & ~3;
+    corr_chunked<FH, NF>(a, smem, PBUF, GBUF, TY, TROWS, TPITCH);
+    return;
+  }
   // P double buffer [2][RCH][TROWS][TPITCH] at smem, core [FH][w][RCH][nf_pad] after it
   float* sG = smem + 2 * PBUF;
   // one rank chunk per tile: prefetch the next tile's P during this one
@@ -151,7 +296,6 @@ corr_kernel(const CorrArgs a) {
   for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
     const dpm_corr_tile tile = a.tiles[t];
     const dpm_corr_job job = a.jobs[tile.job];
-    const int ho = job.H - FH + 1, wo = job.W - job.w + 1;
     const int y0 = tile.ty * TY, x0 = tile.tx * 32;
     const int w = job.w, nfp = job.nf_pad;
 
@@ -188,59 +332,10 @@ corr_kernel(const CorrArgs a) {
       }
       __syncthreads();
 
-      const float* pw = sP + (wy * MP) * TPITCH + lane;
-      const float* gw = sG + wf * NF;
-      const int gstride_i = w * nr * nfp;
-      for (int j = 0; j < w; ++j) {
-        for (int r = 0; r < nr; ++r) {
-          const float* pc = pw + r * TROWS * TPITCH + j;
-          float col[COL];
-#pragma unroll
-          for (int q = 0; q < COL; ++q) col[q] = pc[q * TPITCH];
-          const float* gp = gw + (j * nr + r) * nfp;
-#pragma unroll
-          for (int i = 0; i < FH; ++i) {
-            float g[NF];
-            load_g<NF>(g, gp + i * gstride_i);
-            unsigned long long g2[NP];
-#pragma unroll
-            for (int f = 0; f < NP; ++f) g2[f] = pack2(g[2 * f], g[2 * f + 1]);
-#pragma unroll
-            for (int p = 0; p < MP; ++p)
-#pragma unroll
-              for (int f = 0; f < NP; ++f) ffma2(acc[p][f], col[p + i], g2[f]);
-          }
-        }
-      }
+      chunk_fma<FH, NF>(acc, sP, sG, wy, wf, lane, nr, w, nfp, TROWS, TPITCH);
     }
 
-    // epilogue: coalesced stores (lane = x), optional per-map range fold
-    const int x = x0 + lane;
-    const int yb = y0 + wy * MP;
-    float out[MP][NF];
-#pragma unroll
-    for (int p = 0; p < MP; ++p)
-#pragma unroll
-      for (int f = 0; f < NP; ++f) unpack2(acc[p][f], out[p][2 * f], out[p][2 * f + 1]);
-#pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      const int fg = wf * NF + f;
-      float vmax = -INFINITY, vmin = INFINITY;
-      if (fg < job.nf) {
-        float* dst = a.S + job.s_off + (int64_t)fg * ho * wo;
-#pragma unroll
-        for (int p = 0; p < MP; ++p) {
-          const int y = yb + p;
-          if (x < wo && y < ho) {
-            dst[(int64_t)y * wo + x] = out[p][f];
-            vmax = fmaxf(vmax, out[p][f]);
-            vmin = fminf(vmin, out[p][f]);
-          }
-        }
-      }
-      if (a.ranges != nullptr && job.range_idx >= 0 && wf * NF + f < job.nf)
-        fold_range(a.ranges, job.range_idx + fg, vmax, vmin);
-    }
+    tile_epilogue<FH, NF>(acc, a, job, x0, y0, wy, wf, lane);
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
 }
@@ -366,7 +461,7 @@ extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm
   int dev = 0, sms = 148;
   DPM_CUDA(cudaGetDevice(&dev));
   DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CorrArgs a{P, G, S, jobs, tiles, ntiles, 1, 1, w_max, R, ranges};
+  CorrArgs a{P, G, S, jobs, tiles, ntiles, 1, 1, w_max, R, nf, ranges};
   Shape s;
   if (!pick(h, nf, &s)) {
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 8);
@@ -379,8 +474,10 @@ extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm
   const int TROWS = s.nwy * K2_MP + h - 1;
   const int TPITCH = 32 + w_max - 1;
   const int nfp = (nf + 7) & ~7;  // core filter stride (dpm_corr_job.nf_pad)
+  // P double buffer + one core chunk; R > K2_RCH double-buffers the core chunk too
+  const size_t gbuf = (((size_t)h * w_max * K2_RCH * nfp) + 3) & ~(size_t)3;
   const size_t smem = sizeof(float) * (2 * ((((size_t)K2_RCH * TROWS * TPITCH) + 3) & ~(size_t)3) +
-                                       (size_t)h * w_max * K2_RCH * nfp);
+                                       (R > K2_RCH ? 2 : 1) * gbuf);
   DPM_REQUIRE(smem <= 227 * 1024, "dpm_correlate: h=%d w=%d nf=%d needs %zu B shared memory",
               h, w_max, nf, smem);
   corr_fn fn = kernel_for(h, s.nf_kernel);
