@@ -276,7 +276,7 @@ def run_ours(args):
 
     # ---- end to end through the public API: pinned H2D + run + D2H detections
     for _ in range(max(1, args.warmup // 2)):
-        sc.score_batch(host, tau)
+        sc.score_batch(host, tau, chunk_images=args.chunk)
     barrier()
     e2e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ndets = []
@@ -284,7 +284,7 @@ def run_ours(args):
         barrier()
         e2e_ev[0].record(stream)
         for _ in range(args.steps):
-            d = sc.score_batch(host, tau)
+            d = sc.score_batch(host, tau, chunk_images=args.chunk)
             if dist_on:
                 d = gather_detections(d, device="cuda")
             ndets.append(len(d))
@@ -480,6 +480,8 @@ def main():
     ap.add_argument("--tau", type=float, default=None)
     ap.add_argument("--max-dets", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--chunk", type=int, default=2,
+                    help="images per H2D/compute pipeline chunk of the e2e score_batch call")
     ap.add_argument("--k3", choices=("window", "envelope"), default="window",
                     help="K3 placement kernel: windowed r* (default, faster at the benchmark's "
                          "r*) or the Felzenszwalb lower envelope")

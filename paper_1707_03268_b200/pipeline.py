@@ -108,7 +108,7 @@ class PyramidScorer:
         """Feature bytes one batch moves host -> device (excluding arena padding)."""
         return 4 * self.plan.L * self.n_images * sum(h * w for h, w in self.plan.levels)
 
-    def score_batch(self, host_arena, tau, stream=None, chunk_images=8):
+    def score_batch(self, host_arena, tau, stream=None, chunk_images=2):
         """Public end-to-end call: host pyramids (arena layout, pinned) in,
         detections (structured numpy array of DETECTION records with
         score >= tau) out.
