@@ -19,6 +19,7 @@ from .correlation import (ScoreMap, correlate3_cp, correlate3_full, cp_multiplic
 from .detection import (_placement_grid, best_part_placement, calibrate_thresholds,
                         cp_score_hypothesis, deformation_penalty, dense_detect, detect,
                         score_hypothesis, validate)
+from . import formats  # noqa: F401
 from .evaluation import RocPoint, match_detections, nms, nms_records, roc_eval
 from .errors import CpdetectError, DeviceError, FormatError, NumericError, ValidationError
 from .pipeline import PyramidScorer, cores_from_stacked

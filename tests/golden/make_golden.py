@@ -381,8 +381,44 @@ def gen_roc():
     save("roc.npz", **out)
 
 
+def gen_formats():
+    """Files written by the reference's own savers (save_model dense and
+    decomposed+calibrated, save_scene) plus the arrays its loaders return,
+    for the format readers."""
+    from cpdetect.model import load_model, save_model
+    from cpdetect.synthetic import load_scene, save_scene
+
+    d = os.path.join(HERE, "formats")
+    os.makedirs(d, exist_ok=True)
+    fast = AlsOptions(max_iterations=100, restarts=1, seed=0)
+    model = gen_model(root_size=(3, 4), part_size=(4, 4), n_parts=2, channels=6, low_rank=2,
+                      search_radius=2, bias=0.25, seed=5)
+    scene = gen_scene(model, n_objects=2, noise=0.05, level_shapes=((20, 24), (16, 18)), seed=6)
+    dec = decompose_model(model, ranks=2, opts=fast)
+    cal = D.calibrate_thresholds(dec, [(scene.pyramid[l], h) for l, h in scene.planted])
+    save_model(os.path.join(d, "dense.json"), model)
+    save_model(os.path.join(d, "dec.json"), cal)
+    save_scene(os.path.join(d, "scene.json"), scene)
+    m = load_model(os.path.join(d, "dense.json"))
+    c = load_model(os.path.join(d, "dec.json"))
+    sc = load_scene(os.path.join(d, "scene.json"))
+    out = {"dense_root": m.root, "dense_bias": m.bias,
+           "dec_root_thr": c.root_thresholds, "dec_bias": c.bias,
+           "scene_truth": np.array([[l, *h.root, *[v for p in h.parts for v in p], h.score]
+                                    for l, h in sc.planted])}
+    for i, p in enumerate(m.parts):
+        out[f"dense_part{i}"] = p.filter
+    out.update(cp_arrays("dec_root", c.root_cp))
+    for i, p in enumerate(c.parts):
+        out.update(cp_arrays(f"dec_part{i}", p.cp))
+        out[f"dec_part{i}_thr"] = p.thresholds
+    for i, lv in enumerate(sc.pyramid):
+        out[f"scene_level{i}"] = lv
+    save("formats/expected.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["correlation", "placement", "detect_compact", "cfg1", "cfg2_sample",
-                             "detect_pruned", "roc"]
+                             "detect_pruned", "roc", "formats"]
     for w in which:
         globals()["gen_" + w]()

@@ -659,3 +659,29 @@ def test_mixture_max_matches_host_composition():
             want[sub] = np.where(better, r["scores"], want[sub])
             wcomp[sub] = np.where(better, r["component"], wcomp[sub])
         assert np.array_equal(best, want) and np.array_equal(comp, wcomp), lvl
+
+
+def test_pinned_pyramid_loader_feeds_score_batch(tmp_path):
+    """T3F feature levels read straight into the pinned arena equal fill_host's
+    arena, and score_batch from it gives the same detections."""
+    from paper_1707_03268_b200 import formats as F
+
+    wl = synth.workload(2)
+    C, G = _shared(2, 8)
+    sc = PyramidScorer(wl.bank, C, G, wl.pyramid, n_images=2, max_dets=1 << 16)
+    a = sc.host_arena(pinned=True)
+    b = sc.host_arena(pinned=True)
+    a.zero_()
+    b.zero_()
+    for img in range(2):
+        lv = synth.hog_pyramid(2, img, wl.pyramid)
+        sc.fill_host(a, img, lv)
+        paths = []
+        for k, l in enumerate(lv):
+            paths.append(str(tmp_path / f"i{img}_l{k}.t3f"))
+            F.write_t3f(paths[-1], l)
+        F.load_pyramid_pinned(sc, b, img, paths)
+    assert np.array_equal(a.numpy(), b.numpy())
+    da, db = sc.score_batch(a, 2.0), sc.score_batch(b, 2.0)
+    key = lambda d: np.sort(d, order=["image", "level", "component", "ry", "rx"])  # noqa: E731
+    assert np.array_equal(key(da), key(db)) and len(da) > 0
