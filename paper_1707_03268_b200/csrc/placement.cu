@@ -345,6 +345,13 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const float* npx_odd = sh.npx_odd[buf] + RCAP + 1;
     for (int r = warp; r < nrows; r += PT_WARPS) {
       const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
+      const int ymap = yb0 + r;
+      if (ymap < 0 || ymap >= pj.Hp) {  // row outside the map: no candidate (warp uniform)
+        sh.x32[r * PT_W + lane] = OUT_SENTINEL;
+        sh.xsv[r * PT_W + lane] = OUT_SENTINEL;
+        sh.xdx[r * PT_W + lane] = (int8_t)(-jr.rx);
+        continue;
+      }
       float m1, m2;
       if (pj.scale == 2)  // 2*lane + even row base: pair starts are 8-byte aligned
         screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
