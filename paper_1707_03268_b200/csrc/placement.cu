@@ -274,16 +274,17 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
     const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
     const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * jr.rx;
-    for (int r = warp; r < nrows; r += PT_WARPS) {
+    // only band rows inside the map are staged (the x pass never reads the others)
+    const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
+    for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
       const int y = yb0 + r;
-      const bool yok = y >= 0 && y < pj.Hp;
-      const float* srow = sm + (int64_t)(yok ? y : 0) * pj.Wp;
+      const float* srow = sm + (int64_t)y * pj.Wp;
       float* drow = sh.s + r * COLS_PITCH;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int c = lane + 32 * q, x = xb0 + c;
         if (c >= ncols) continue;
-        if (yok && x >= 0 && x < pj.Wp) {
+        if (x >= 0 && x < pj.Wp) {
           const uint32_t sa = (uint32_t)__cvta_generic_to_shared(drow + c);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(srow + x));
         } else {
@@ -343,15 +344,18 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     // x pass: band row r (warp-strided), centre column = lane
     const float* npx = sh.npx[buf] + RCAP;
     const float* npx_odd = sh.npx_odd[buf] + RCAP + 1;
-    for (int r = warp; r < nrows; r += PT_WARPS) {
+    // band rows outside the map have no candidate (reference: (-inf, -r))
+    const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
+    const int n_out = r_lo + (nrows - r_hi);
+    for (int i = threadIdx.x; i < n_out * PT_W; i += PT_THREADS) {
+      const int k = i / PT_W, l = i - k * PT_W;
+      const int r = k < r_lo ? k : r_hi + (k - r_lo);
+      sh.x32[r * PT_W + l] = OUT_SENTINEL;
+      sh.xsv[r * PT_W + l] = OUT_SENTINEL;
+      sh.xdx[r * PT_W + l] = (int8_t)(-jr.rx);
+    }
+    for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {  // in-map rows only
       const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
-      const int ymap = yb0 + r;
-      if (ymap < 0 || ymap >= pj.Hp) {  // row outside the map: no candidate (warp uniform)
-        sh.x32[r * PT_W + lane] = OUT_SENTINEL;
-        sh.xsv[r * PT_W + lane] = OUT_SENTINEL;
-        sh.xdx[r * PT_W + lane] = (int8_t)(-jr.rx);
-        continue;
-      }
       float m1, m2;
       if (pj.scale == 2)  // 2*lane + even row base: pair starts are 8-byte aligned
         screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
