@@ -243,9 +243,18 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   const int ty0 = (tile / ntx) * PT_H, tx0 = (tile % ntx) * PT_W;  // offsets inside the rect
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int RPT = PT_H / PT_WARPS;  // roots per thread (4)
-  const int ix = tx0 + lane;
-  const bool col_ok = ix < wr;
-  const int rx = aj.rx0 + ix;
+  // Narrow tiles pack: lpr = lanes per band row / per root row (power of two
+  // >= the tile's valid columns), so a warp screens 32 / lpr rows at once and
+  // the roots map compactly onto threads.
+  const int wt = min(PT_W, wr - tx0), h_tile = min(PT_H, hr - ty0);
+  const int lpr_log = wt > 16 ? 5 : wt > 8 ? 4 : wt > 4 ? 3 : wt > 2 ? 2 : wt > 1 ? 1 : 0;
+  const int lpr = 1 << lpr_log;
+  auto root_of = [&](int k, int& iyr, int& ixr) -> bool {  // k-th root of this thread
+    const int e = threadIdx.x + PT_THREADS * k;
+    iyr = e >> lpr_log;
+    ixr = e & (lpr - 1);
+    return iyr < h_tile && ixr < wt;
+  };
   const int ry_lo = aj.ry0 + ty0;
   const int ry_hi = aj.ry0 + min(ty0 + PT_H, hr) - 1;
   const int rx_lo = aj.rx0 + tx0;
@@ -256,10 +265,10 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   double tot[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    const int iy = ty0 + warp + PT_WARPS * k;
+    int iyr, ixr;
     tot[k] = 0.0;
-    if (aj.root_off >= 0 && col_ok && iy < hr)
-      tot[k] = (double)__ldg(S + aj.root_off + (int64_t)(aj.ry0 + iy) * aj.root_pitch + rx);
+    if (aj.root_off >= 0 && root_of(k, iyr, ixr))
+      tot[k] = (double)__ldg(S + aj.root_off + (int64_t)(ry_lo + iyr) * aj.root_pitch + rx_lo + ixr);
   }
 
   // Per part: [band p resident] x pass -> sync -> async copy of band p+1 into
@@ -273,7 +282,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
     const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
-    const int ncols = pj.scale * (PT_W - 1) + 1 + 2 * jr.rx;
+    const int ncols = pj.scale * (lpr - 1) + 1 + 2 * jr.rx;
     // only band rows inside the map are staged (the x pass never reads the others)
     const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
     for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
@@ -319,14 +328,15 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const dpm_place_job pj = pjobs[aj.part_job0 + p];
     const JobRange jr = prep[aj.part_job0 + p];
     const float* sm = S + pj.s_off;
-    const int cx = pj.scale * rx + pj.ax;
     const bool have_next = p + 1 < aj.nparts;
     if (!staged_ok(pj, jr)) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
-        const int iy = ty0 + warp + PT_WARPS * k;
-        if (!col_ok || iy >= hr) continue;
+        int iyr, ixr;
+        if (!root_of(k, iyr, ixr)) continue;
+        const int iy = ty0 + iyr, ix = tx0 + ixr;
         const int cy = pj.scale * (aj.ry0 + iy) + pj.ay;
+        const int cx = pj.scale * (aj.rx0 + ix) + pj.ax;
         double best;
         int bdy, bdx;
         place_unstaged(sm, pj, cy, cx, jr.rx, jr.ry, best, bdy, bdx);
@@ -354,8 +364,12 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       sh.xsv[r * PT_W + l] = OUT_SENTINEL;
       sh.xdx[r * PT_W + l] = (int8_t)(-jr.rx);
     }
-    for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {  // in-map rows only
-      const float* srow = sh.s + r * COLS_PITCH + pj.scale * lane + jr.rx;  // dx = 0
+    const int xsub = lane >> lpr_log, xc = lane & (lpr - 1);
+    const int rpw = PT_W >> lpr_log;  // band rows per warp step
+    for (int rb = r_lo + warp * rpw; rb < r_hi; rb += PT_WARPS * rpw) {  // in-map rows only
+      const int r = rb + xsub;
+      if (r >= r_hi) continue;
+      const float* srow = sh.s + r * COLS_PITCH + pj.scale * xc + jr.rx;  // dx = 0
       float m1, m2;
       if (pj.scale == 2)  // 2*lane + even row base: pair starts are 8-byte aligned
         screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
@@ -378,9 +392,9 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
           }
         }
       }
-      sh.x32[r * PT_W + lane] = m1;
-      sh.xsv[r * PT_W + lane] = srow[xi];
-      sh.xdx[r * PT_W + lane] = (int8_t)xi;
+      sh.x32[r * PT_W + xc] = m1;
+      sh.xsv[r * PT_W + xc] = srow[xi];
+      sh.xdx[r * PT_W + xc] = (int8_t)xi;
     }
     __syncthreads();  // x pass done: the band buffer is free for part p+1
     if (have_next) issue_part(p + 1, buf ^ 1);
@@ -389,16 +403,18 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const float* npy = sh.npy[buf] + RCAP;
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
-      const int iy = ty0 + warp + PT_WARPS * k;
-      if (!col_ok || iy >= hr) continue;
+      int iyr, ixr;
+      if (!root_of(k, iyr, ixr)) continue;
+      const int iy = ty0 + iyr, ix = tx0 + ixr;
       const int ry = aj.ry0 + iy;
       const int cy = pj.scale * ry + pj.ay;
+      const int cx = pj.scale * (aj.rx0 + ix) + pj.ax;
       const int r0 = cy - yb0;  // band row of dy = 0
-      const float* xcol = sh.x32 + r0 * PT_W + lane;
+      const float* xcol = sh.x32 + r0 * PT_W + ixr;
       float m1, m2;
       screen_dispatch<PT_W, false>(jr.ry, xcol, npy, npy, code_mask, m1, m2);
       auto exact = [&](int dy) -> double {
-        const int row = (r0 + dy) * PT_W + lane;
+        const int row = (r0 + dy) * PT_W + ixr;
         const int dx = sh.xdx[row];
         const double xv = __dadd_rn((double)sh.xsv[row], -pen(pj.cdx, pj.cdxx, dx));
         return __dadd_rn(xv, -pen(pj.cdy, pj.cdyy, dy));
@@ -421,7 +437,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       } else {
         best = exact(bi);
       }
-      const int bdx = sh.xdx[(r0 + bi) * PT_W + lane];
+      const int bdx = sh.xdx[(r0 + bi) * PT_W + ixr];
       tot[k] = __dadd_rn(tot[k], best);
       const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
       if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bi, cx + bdx);
@@ -432,8 +448,9 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   // bias, totals, tau compaction (part positions read back from `pos`)
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    const int iy = ty0 + warp + PT_WARPS * k;
-    const bool live = col_ok && iy < hr;
+    int iyr, ixr;
+    const bool live = root_of(k, iyr, ixr);
+    const int iy = ty0 + iyr, ix = tx0 + ixr;
     if (live) {
       tot[k] = __dadd_rn(tot[k], aj.bias);
       if (aj.total_off >= 0) total[aj.total_off + (int64_t)iy * wr + ix] = tot[k];
@@ -454,7 +471,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     dd.level = aj.level;
     dd.component = aj.component;
     dd.ry = aj.ry0 + iy;
-    dd.rx = rx;
+    dd.rx = aj.rx0 + ix;
     dd.nparts = aj.nparts;
     dd.score = tot[k];
     for (int q = 0; q < DPM_MAX_PARTS; ++q)
