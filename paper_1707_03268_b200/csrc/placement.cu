@@ -225,6 +225,8 @@ struct __align__(16) PlaceSmem {
   float npx[2][2 * RCAP + 4];      // -pen_x(dx) in FP32 (screening only), by part parity
   float npx_odd[2][2 * RCAP + 4];  // the same, shifted by one element (packed pairs, odd r)
   float npy[2][2 * RCAP + 4];
+  alignas(16) JobRange jr[2];      // r*, E2 of the current / next part (16-B cp.async)
+  alignas(16) dpm_place_job pj[2]; // placement job of the current / next part
 };
 
 __global__ void __launch_bounds__(PT_THREADS, 2)
@@ -315,20 +317,43 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   };
 
   // r*/E2 of every part come from the prologue (dpm_place_ranges)
-  auto issue_part = [&](int q, int buf) {  // band + tables of part q (if staged)
-    const dpm_place_job pn = pjobs[aj.part_job0 + q];
-    const JobRange jn = prep[aj.part_job0 + q];
+  // The placement job and r*/E2 record of part q are cp.async-copied into
+  // shared slot q & 1 one part ahead (warp 0), so no thread waits on their
+  // global loads at a part boundary.
+  auto fetch_job = [&](int q, int buf) {
+    if (warp != 0) return;
+    if (lane < (int)(sizeof(dpm_place_job) / 8)) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(
+          reinterpret_cast<unsigned char*>(&sh.pj[buf]) + 8 * lane);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                   "l"(reinterpret_cast<const unsigned char*>(pjobs + aj.part_job0 + q) + 8 * lane));
+    } else if (lane == 31) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&sh.jr[buf]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                   "l"(prep + aj.part_job0 + q));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto issue_part = [&](int buf) {  // band + tables of the part whose job is in slot buf
+    const dpm_place_job pn = sh.pj[buf];
+    const JobRange jn = sh.jr[buf];
     if (staged_ok(pn, jn)) stage_issue(pn, jn, buf);
   };
-  if (aj.nparts > 0) issue_part(0, 0);
+  if (aj.nparts > 0) {
+    fetch_job(0, 0);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    issue_part(0);
+  }
   for (int p = 0; p < aj.nparts; ++p) {
     const int buf = p & 1;
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();  // band p and its penalty tables resident; part p-1 finished
-    const dpm_place_job pj = pjobs[aj.part_job0 + p];
-    const JobRange jr = prep[aj.part_job0 + p];
+    const dpm_place_job pj = sh.pj[buf];
+    const JobRange jr = sh.jr[buf];
     const float* sm = S + pj.s_off;
     const bool have_next = p + 1 < aj.nparts;
+    if (have_next) fetch_job(p + 1, buf ^ 1);
     if (!staged_ok(pj, jr)) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
@@ -345,7 +370,11 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
         if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bdy, cx + bdx);
         if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
       }
-      if (have_next) issue_part(p + 1, buf ^ 1);
+      if (have_next) {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();  // job p+1 visible
+        issue_part(buf ^ 1);
+      }
       continue;
     }
     const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
@@ -396,8 +425,9 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       sh.xsv[r * PT_W + xc] = srow[xi];
       sh.xdx[r * PT_W + xc] = (int8_t)xi;
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);  // job p+1 (warp 0's copies)
     __syncthreads();  // x pass done: the band buffer is free for part p+1
-    if (have_next) issue_part(p + 1, buf ^ 1);
+    if (have_next) issue_part(buf ^ 1);
 
     // y pass for this thread's roots; exact values from the x winners
     const float* npy = sh.npy[buf] + RCAP;
