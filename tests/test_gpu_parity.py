@@ -685,3 +685,103 @@ def test_pinned_pyramid_loader_feeds_score_batch(tmp_path):
     da, db = sc.score_batch(a, 2.0), sc.score_batch(b, 2.0)
     key = lambda d: np.sort(d, order=["image", "level", "component", "ry", "rx"])  # noqa: E731
     assert np.array_equal(key(da), key(db)) and len(da) > 0
+
+
+# ---------------------------------------------- reference test-suite mirrors
+# (pkg/tests/test_correlation.py:71-116, test_detection.py:169-240, 318-590)
+
+def test_correlation_known_answers():
+    rng = np.random.default_rng(0)
+    img = rng.normal(size=(4, 5, 1))
+    sm = B.correlate3_full(img, np.full((1, 1, 1), 2.0))
+    assert_map_close(sm.scores, 2.0 * img[:, :, 0], "scalar filter")
+    assert sm.multiplications == 4 * 5
+    img = rng.normal(size=(5, 6, 3))
+    filt = np.zeros((2, 2, 3))
+    filt[0, 0, 0] = 1.0
+    assert_map_close(B.correlate3_full(img, filt).scores, img[0:4, 0:5, 0], "delta filter")
+    # rank-1 CP == dense correlation with the reconstructed filter
+    img = rng.normal(size=(7, 6, 3))
+    a, b, c = rng.normal(size=3), rng.normal(size=2), rng.normal(size=3)
+    cp = B.CPModel.from_factors(a[:, None], b[:, None], c[:, None])
+    dense = np.einsum("r,ir,jr,kr->ijk", cp.weights, cp.factors_a, cp.factors_b, cp.factors_c)
+    assert_map_close(B.correlate3_cp(img, cp).scores, B.correlate3_full(img, dense).scores,
+                     "rank-1 separable")
+
+
+def _rand_dec(rng, root=(3, 4), parts=((4, 4), (4, 4)), L=6, R=2):
+    from conftest import CP, _Dec, _Part
+
+    def cp(n, m):
+        return CP(np.abs(rng.normal(size=R)) + 0.5, rng.normal(size=(n, R)) / np.sqrt(n),
+                  rng.normal(size=(m, R)) / np.sqrt(m), rng.normal(size=(L, R)) / np.sqrt(L))
+    ps = [_Part(cp(*d), (i, 2 * i), (0.0, 0.0, 0.05, 0.05), 2, None)
+          for i, d in enumerate(parts)]
+    return _Dec(cp(*root), ps, 0.1, None)
+
+
+def test_detect_root_only_model_and_degenerate_pyramids():
+    rng = np.random.default_rng(50)
+    dec = _rand_dec(rng, parts=())
+    level = rng.normal(size=(20, 24, 6))
+    root = O.cp_partial_stack(level, dec.root_cp)[-1] + dec.bias
+    tau = float(np.quantile(root, 0.9))
+    dets, st = B.detect(dec, [level], tau)
+    got = {d.hypothesis.root for d in dets}
+    want = {(int(y), int(x)) for y, x in zip(*np.nonzero(root >= tau))}
+    near = {(int(y), int(x)) for y, x in zip(*np.nonzero(np.abs(root - tau) <= 1e-5 * abs(root).max()))}
+    assert got ^ want <= near and all(d.hypothesis.parts == () for d in dets)
+    # calibrated on its own top hypothesis, pruning keeps it and prunes others
+    iy, ix = np.unravel_index(np.argmax(root), root.shape)
+    cal = B.calibrate_thresholds(dec, [(level, B.Hypothesis(level=0, root=(int(iy), int(ix))))])
+    pdets, pst = B.detect(cal, [level], tau, pruning=True)
+    assert (int(iy), int(ix)) in {d.hypothesis.root for d in pdets}
+    assert pst.positions_pruned > 0
+    # degenerate pyramids (test_detection.py:522-530)
+    dec2 = _rand_dec(rng)
+    none, st0 = B.detect(dec2, [], -np.inf)
+    assert none == [] and st0.positions_examined == 0
+    dec3 = _rand_dec(rng, parts=((6, 6),))  # level fits the root, not the part
+    found, st1 = B.detect(dec3, [np.zeros((5, 6, 6))], -np.inf)
+    assert found == [] and st1.positions_examined == 0
+    with pytest.raises(B.ValidationError, match="channel"):
+        B.detect(dec2, [np.zeros((20, 20, 3))], 0.0)
+
+
+def test_pruned_subset_identical_scores_invariants_determinism():
+    for k in range(3):
+        g, dec, pyr, hyps, tau = _pruned_case(k)
+        cal = B.calibrate_thresholds(dec, hyps)
+        tau = min(float(h.score) for _, h in hyps if h.score is not None) - 20.0 \
+            if all(h.score is not None for _, h in hyps) else 0.0
+        off, soff = B.detect(cal, pyr, tau, pruning=False)
+        on, son = B.detect(cal, pyr, tau, pruning=True)
+        offi = {(d.hypothesis.level, d.hypothesis.root): d.score for d in off}
+        oni = {(d.hypothesis.level, d.hypothesis.root): d.score for d in on}
+        assert set(oni) <= set(offi)
+        assert all(oni[key] == offi[key] for key in oni)  # survivors: identical full sums
+        assert son.multiplications <= soff.multiplications
+        assert son.positions_pruned + son.positions_surviving == son.positions_examined
+        on2, son2 = B.detect(cal, pyr, tau, pruning=True)
+        assert [(d.hypothesis.level, d.hypothesis.root, d.score) for d in on] == \
+            [(d.hypothesis.level, d.hypothesis.root, d.score) for d in on2]
+        assert son.positions_pruned_at_rank == son2.positions_pruned_at_rank
+        assert son.multiplications == son2.multiplications
+
+
+def test_calibration_known_answers():
+    g, dec, pyr, hyps, tau = _pruned_case(0)
+    level, hyp = hyps[0]
+    one = B.calibrate_thresholds(dec, [(level, hyp)])
+    rs = B.cp_partial_stack(level, dec.root_cp)
+    assert np.array_equal(one.root_thresholds, rs[:, hyp.root[0], hyp.root[1]])
+    for p, (py, px) in zip(one.parts, hyp.parts):
+        ps = B.cp_partial_stack(level, p.cp)
+        assert np.array_equal(p.thresholds, ps[:, py, px])
+    once = B.calibrate_thresholds(dec, hyps)
+    twice = B.calibrate_thresholds(dec, hyps + hyps)
+    assert np.array_equal(once.root_thresholds, twice.root_thresholds)
+    bad = B.Hypothesis(level=0, root=hyp.root,
+                       parts=((hyp.parts[0][0] + 9, hyp.parts[0][1]),) + tuple(hyp.parts[1:]))
+    with pytest.raises(B.ValidationError, match="search radius|out of support"):
+        B.calibrate_thresholds(dec, [(level, bad)])
