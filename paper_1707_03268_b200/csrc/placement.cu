@@ -288,19 +288,34 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     // only band rows inside the map are staged (the x pass never reads the others)
     const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(sh.s);
-    for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
-      const int y = yb0 + r;
-      const float* srow = sm + (int64_t)y * pj.Wp + xb0;
-      const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
+    const int Wp = pj.Wp;
+    const float* sbase = sm + (int64_t)yb0 * Wp + xb0;
+    if (xb0 >= 0 && xb0 + ncols <= Wp) {  // every band column inside the map (uniform)
+      for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
+        const float* srow = sbase + (int64_t)r * Wp;
+        const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int c = lane + 32 * q, x = xb0 + c;
-        if (c >= ncols) continue;
-        if (x >= 0 && x < pj.Wp) {
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(drow + 4u * c),
-                       "l"(srow + c));
-        } else {
-          sh.s[r * COLS_PITCH + c] = OUT_SENTINEL;
+        for (int q = 0; q < 3; ++q) {
+          const int c = lane + 32 * q;
+          if (c < ncols)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(drow + 4u * c),
+                         "l"(srow + c));
+        }
+      }
+    } else {
+      for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
+        const float* srow = sbase + (int64_t)r * Wp;
+        const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int c = lane + 32 * q, x = xb0 + c;
+          if (c >= ncols) continue;
+          if (x >= 0 && x < Wp) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(drow + 4u * c),
+                         "l"(srow + c));
+          } else {
+            sh.s[r * COLS_PITCH + c] = OUT_SENTINEL;
+          }
         }
       }
     }
