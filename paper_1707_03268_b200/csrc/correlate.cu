@@ -392,7 +392,7 @@ static bool pick(int h, int nf, Shape* s) {
     s->nf_kernel = 8;
     s->nwf = (nf + 7) / 8;
     if (s->nwf > 6) return false;
-    s->nwy = s->nwf >= 3 ? 1 : 2;
+    s->nwy = 2;  // <= K2_MAX_WARPS (12) warps per CTA
   }
   switch (h) {
     case 2: case 3: case 4: case 5: case 6: case 7: case 8: case 11: case 15: return true;

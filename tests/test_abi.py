@@ -98,8 +98,9 @@ def test_prepare_validates_and_numbers_blocks():
 def test_tile_shapes():
     lib = _lib.lib()
     tw, th = ctypes.c_int(), ctypes.c_int()
-    assert lib.dpm_correlate_tile_shape(6, 48, ctypes.byref(tw), ctypes.byref(th)) == 6
-    assert (tw.value, th.value) == (32, 8)
+    # 6 filter warps x 2 row warps (32 x 16 positions, 12 warps)
+    assert lib.dpm_correlate_tile_shape(6, 48, ctypes.byref(tw), ctypes.byref(th)) == 12
+    assert (tw.value, th.value) == (32, 16)
     assert lib.dpm_correlate_tile_shape(6, 6, ctypes.byref(tw), ctypes.byref(th)) == 2
     assert th.value == 16
     assert lib.dpm_correlate_tile_shape(9, 2, ctypes.byref(tw), ctypes.byref(th)) < 0
