@@ -120,6 +120,12 @@ int dpm_correlate(const float* P, const float* G, float* S, const dpm_corr_job* 
  * Requirements: R % 8 == 0, 1 <= nf <= 64, h + 2 <= 16 and the returned
  * shared-memory size <= 227 KB. */
 size_t dpm_correlate_tc_smem(int h, int w, int R, int nf);
+/* Floats of the `Gtc` block for (h, w, R, nf): the tf32 hi|lo layout above,
+ * followed -- for the compile-time DPM shapes (R = 8, h = 6, w in {6, 11}),
+ * whose kernel runs the correction MMA in bf16 over tap pairs -- by the bf16
+ * block [h][ceil(w/2)][2][N][8] of the tf32-truncated values (tap 2p then
+ * 2p+1; zeros past w). */
+size_t dpm_correlate_tc_core_floats(int h, int w, int R, int nf);
 int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
                      const dpm_corr_tile* strips, int nstrips, int h, int w, int R, int nf,
                      uint32_t* ranges, void* stream);

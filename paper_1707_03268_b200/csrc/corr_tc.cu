@@ -16,6 +16,14 @@
 //   MMA2: D[:, 0:N]  += A_lo x  B_hi
 // and the epilogue adds D[:, f] + D[:, N+f]; the dropped A_lo*B_lo term is
 // ~2^-22 relative, far inside the 1e-5 parity bar.
+// The compile-time DPM shapes (R == 8) run the correction MMA2 in bf16
+// (kind::f16) over two taps at once: A_lo is staged as bf16, 16 bytes per
+// position, so a K-major descriptor with LBO = 16 B reads position m + j for
+// K = 0..7 and position m + j + 1 for K = 8..15, i.e. taps j and j + 1,
+// against a host-built bf16 [B_hi(j); B_hi(j+1)] block.  That halves MMA2's
+// instructions and its shared-memory operand bytes (the tensor pipe here is
+// bound by operand bandwidth); the added error (bf16 rounding of the ~2^-11
+// correction) is ~2^-19 relative per product.
 //
 // Warp roles (256 threads, one persistent CTA per SM):
 //   warp 0      : TMEM allocation; one elected lane issues tcgen05.mma
@@ -115,6 +123,28 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// kind::f16 with bf16 A/B, f32 D, K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(TC_M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc));
+}
+
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -152,10 +182,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
   const int nq = a.R >> 2;                       // rank quads
   const int taps = a.h * a.w;
   const int tcols = TC_M + a.w - 1;
+  constexpr bool BF = FH > 0;  // bf16 correction MMA (compile-time shapes, R == 8)
   const uint32_t b_bytes = (uint32_t)taps * nq * (2 * a.N) * 16u;
-  const uint32_t slot_bytes = 2u * nq * tcols * 16u;  // hi then lo
+  const uint32_t npairs = (uint32_t)(a.w + 1) / 2;
+  const uint32_t b2_bytes = BF ? (uint32_t)a.h * npairs * 2u * a.N * 16u : 0u;
+  const uint32_t hi_bytes = (uint32_t)nq * tcols * 16u;
+  const uint32_t slot_bytes = BF ? ((hi_bytes + (tcols + 1u) * 16u + 127u) & ~127u)
+                                 : 2u * hi_bytes;  // hi then lo
   unsigned char* sB = smem;
-  unsigned char* sA = smem + ((b_bytes + 1023u) & ~1023u);
+  unsigned char* sB2 = smem + ((b_bytes + 1023u) & ~1023u);
+  unsigned char* sA = sB2 + ((b2_bytes + 1023u) & ~1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sA + ((a.ring * slot_bytes + 15u) & ~15u));
   uint64_t* full = bars;
   uint64_t* empty = bars + TC_MAX_RING;
@@ -168,6 +204,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
     const float4* src = reinterpret_cast<const float4*>(a.Gtc);
     float4* dst = reinterpret_cast<float4*>(sB);
     for (uint32_t e = threadIdx.x; e < b_bytes / 16u; e += TC_THREADS) dst[e] = __ldg(src + e);
+    if constexpr (BF) {  // bf16 tap-pair block follows the tf32 block in Gtc
+      const float4* src2 = src + b_bytes / 16u;
+      float4* dst2 = reinterpret_cast<float4*>(sB2);
+      for (uint32_t e = threadIdx.x; e < b2_bytes / 16u; e += TC_THREADS) dst2[e] = __ldg(src2 + e);
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.ring; ++s) {
@@ -206,6 +247,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
     const uint32_t slot_step = slot_bytes >> 4;
     const uint32_t tap_step = (uint32_t)nq * lboB >> 4;
     const uint32_t kcA = 2u * lboA >> 4, kcB = 2u * lboB >> 4;
+    // bf16 correction operands: A_lo [position][8 ranks] after the hi planes
+    // (LBO 16 B: K-chunk 1 = next position), B2 [h][pair][2][N][8] (LBO = N*16 B)
+    const uint64_t dAlo0 = umma_desc(smem_u32(sA) + hi_bytes, 16u, 128u);
+    const uint64_t dB2 = umma_desc(smem_u32(sB2), (uint32_t)a.N * 16u, 128u);
+    const uint32_t b2_pair = (2u * a.N * 16u) >> 4;
+    const uint32_t idescbf = idesc_bf16(a.N);
     uint32_t q_glob = 0, row_glob = 0;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
@@ -221,9 +268,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
         const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
         if constexpr (FH > 0) {
           // compile-time taps: every descriptor is a row base + immediate
-          uint64_t da_row[FH];
+          uint64_t da_row[FH], da_lo[FH];
 #pragma unroll
-          for (int i = 0; i < FH; ++i) da_row[i] = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
+          for (int i = 0; i < FH; ++i) {
+            da_row[i] = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
+            da_lo[i] = dAlo0 + ((q_glob + y + i) % a.ring) * slot_step;
+          }
           if (elect_one()) {
 #pragma unroll
             for (int i = 0; i < FH; ++i)
@@ -232,7 +282,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
                 const uint64_t ahi = da_row[i] + (uint32_t)j;
                 const uint64_t bb = dB0 + (uint32_t)((i * FW + j) * 2) * (uint32_t)(lboB >> 4);
                 mma_tf32(d, ahi, bb, idesc1, (i | j) != 0);
-                mma_tf32(d, ahi + lo_step, bb, idesc2, 1);
+              }
+            // bf16 correction over tap pairs: A_lo rows at +16 B per position
+#pragma unroll
+            for (int i = 0; i < FH; ++i)
+#pragma unroll
+              for (int jp = 0; jp < (FW + 1) / 2; ++jp) {
+                const uint64_t alo = da_lo[i] + (uint32_t)(2 * jp);
+                const uint64_t b2 = dB2 + (uint32_t)((i * ((FW + 1) / 2) + jp) * b2_pair);
+                mma_bf16(d, alo, b2, idescbf);
               }
           }
           __syncwarp();
@@ -287,6 +345,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
         float4* hi = reinterpret_cast<float4*>(sA + slot * slot_bytes);
         float4* lo = hi + nelem;
         const float* prow = pbase + (int64_t)q * job.pitch;
+        if constexpr (BF) {
+          // R == 8: lane handles positions c = lane + 32k; hi as two tf32 quads,
+          // lo as 8 bf16 (16 B) per position, one zero position past the row
+          uint4* lo16 = reinterpret_cast<uint4*>(sA + slot * slot_bytes + hi_bytes);
+          constexpr int PP = (TC_M + (FW > 0 ? FW : 1) + 31) / 32;
+          float v8[PP][8];
+#pragma unroll
+          for (int k = 0; k < PP; ++k) {
+            const int c = lane + 32 * k, x = x0 + c;
+            const bool ok = c < tcols && x < job.W;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v8[k][r] = ok ? __ldg(prow + (int64_t)r * plane + x) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < PP; ++k) {
+            const int c = lane + 32 * k;
+            if (c > tcols) continue;
+            float h8[8], l8[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              h8[r] = tf32_hi(v8[k][r]);
+              l8[r] = v8[k][r] - h8[r];
+            }
+            if (c < tcols) {
+              hi[c] = make_float4(h8[0], h8[1], h8[2], h8[3]);
+              hi[tcols + c] = make_float4(h8[4], h8[5], h8[6], h8[7]);
+            }
+            lo16[c] = make_uint4(bf16x2_rn(l8[0], l8[1]), bf16x2_rn(l8[2], l8[3]),
+                                 bf16x2_rn(l8[4], l8[5]), bf16x2_rn(l8[6], l8[7]));
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(full + slot);
+          continue;
+        }
         float4 v[PQ];
 #pragma unroll
         for (int k = 0; k < PQ; ++k) {
@@ -394,12 +487,29 @@ using namespace dpm;
 // Input-row ring depth: at least h + 2 (the h rows of an output row plus
 // slack), then as deep as shared memory allows (up to TC_MAX_RING), so the
 // producers run further ahead of the MMA warp and hide row-load latency.
+// compile-time shapes of the launcher (DPM part / root filters at R = 8):
+// they use the bf16 correction MMA and its smem layout
+static bool tc_bf16(int h, int w, int R) { return R == 8 && h == 6 && (w == 6 || w == 11); }
+
+static size_t tc_b2_bytes(int h, int w, int R, int nf) {
+  if (!tc_bf16(h, w, R)) return 0;
+  const int N = (nf + 15) & ~15;
+  return ((size_t)h * ((w + 1) / 2) * 2 * N * 16 + 1023) & ~(size_t)1023;
+}
+
+static size_t tc_slot(int h, int w, int R) {
+  const int nq = R / 4, tcols = TC_M + w - 1;
+  if (tc_bf16(h, w, R))
+    return ((size_t)nq * tcols * 16 + (size_t)(tcols + 1) * 16 + 127) & ~(size_t)127;
+  return 2ull * nq * tcols * 16;
+}
+
 static int tc_ring(int h, int w, int R, int nf) {
   const int N = (nf + 15) & ~15;
   const int nq = R / 4;
   const size_t b = ((size_t)h * w * nq * 2 * N * 16 + 1023) & ~(size_t)1023;
-  const size_t slot = 2ull * nq * (TC_M + w - 1) * 16;
-  const size_t fixed = b + (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16 + 15;
+  const size_t slot = tc_slot(h, w, R);
+  const size_t fixed = b + tc_b2_bytes(h, w, R, nf) + (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16 + 15;
   int ring = h + 2 <= TC_MAX_RING ? h + 2 : TC_MAX_RING;
   while (ring < TC_MAX_RING && fixed + (ring + 1) * slot <= 227 * 1024) ++ring;
   return ring;
@@ -410,9 +520,16 @@ extern "C" size_t dpm_correlate_tc_smem(int h, int w, int R, int nf) {
   const int nq = R / 4;
   const size_t b = (size_t)h * w * nq * 2 * N * 16;
   const int ring = tc_ring(h, w, R, nf);
-  const size_t slot = 2ull * nq * (TC_M + w - 1) * 16;
-  return ((b + 1023) & ~(size_t)1023) + ((ring * slot + 15) & ~(size_t)15) +
-         (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
+  const size_t slot = tc_slot(h, w, R);
+  return ((b + 1023) & ~(size_t)1023) + tc_b2_bytes(h, w, R, nf) +
+         ((ring * slot + 15) & ~(size_t)15) + (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
+}
+
+extern "C" size_t dpm_correlate_tc_core_floats(int h, int w, int R, int nf) {
+  const int N = (nf + 15) & ~15;
+  size_t f = (size_t)h * w * (R / 4) * 2 * N * 4;
+  if (tc_bf16(h, w, R)) f += (size_t)h * ((w + 1) / 2) * 2 * N * 8 / 2;  // bf16 block
+  return f;
 }
 
 extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,

@@ -593,9 +593,18 @@ class Plan:
         return sum(4 * (self.L + self.Rtot) * H * W for H, W in self.levels)
 
 
+def _bf16_rn(x):
+    """float32 -> bf16 bit patterns (uint16), round to nearest even."""
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
 def _tc_core(cores):
     """Cores of one group in the tcgen05 B layout [h*w][R/4][2N][4]: rows < N
-    the tf32-truncated values, rows >= N the exact fp32 remainders."""
+    the tf32-truncated values, rows >= N the exact fp32 remainders.  For the
+    shapes whose kernel runs the bf16 correction MMA
+    (dpm_correlate_tc_core_floats larger than that block), the bf16 tap-pair
+    block [h][ceil(w/2)][2][N][8] of the truncated values follows."""
     core = np.stack([np.asarray(c, np.float32) for c in cores], axis=-1)  # (h, w, R, nf)
     h, w, R, nf = core.shape
     N = _round_up(nf, 16)
@@ -605,6 +614,16 @@ def _tc_core(cores):
     for src, base in ((hi, 0), (lo, N)):
         t = src.reshape(h * w, R // 4, 4, nf).transpose(0, 1, 3, 2)  # (tap, quad, nf, 4)
         out[:, :, base:base + nf, :] = t
+    out = out.ravel()
+    total = int(_lib.lib().dpm_correlate_tc_core_floats(h, w, R, nf))
+    if total > out.size:
+        npairs = (w + 1) // 2
+        b2 = np.zeros((h, npairs, 2, N, 8), dtype=np.uint16)
+        bits = _bf16_rn(hi)  # (h, w, R, nf)
+        for j in range(w):
+            b2[:, j // 2, j % 2, :nf, :] = bits[:, j, :, :].transpose(0, 2, 1)  # (h, nf, R)
+        out = np.concatenate([out, b2.ravel().view(np.float32)])
+        assert out.size == total, (out.size, total)
     return out
 
 
