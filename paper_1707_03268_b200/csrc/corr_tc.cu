@@ -139,6 +139,17 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc));
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
+}
+
 __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -175,8 +186,10 @@ __device__ __forceinline__ float tf32_hi(float a) {
 
 // NMAX: max filters held by the epilogue registers.  FH, FW > 0: filter
 // extent fixed at compile time (R == 8), fully unrolled MMA issue.
-template <int NMAX, int FH, int FW>
-__global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) {
+// EPI: epilogue warps (4, or 8 = two per TMEM lane quarter, each draining
+// alternate 16-filter column chunks).
+template <int NMAX, int FH, int FW, int EPI = 4>
+__global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kernel(const TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = a.R >> 2;                       // rank quads
@@ -203,11 +216,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
   {
     const float4* src = reinterpret_cast<const float4*>(a.Gtc);
     float4* dst = reinterpret_cast<float4*>(sB);
-    for (uint32_t e = threadIdx.x; e < b_bytes / 16u; e += TC_THREADS) dst[e] = __ldg(src + e);
+    for (uint32_t e = threadIdx.x; e < b_bytes / 16u; e += blockDim.x) dst[e] = __ldg(src + e);
     if constexpr (BF) {  // bf16 tap-pair block follows the tf32 block in Gtc
       const float4* src2 = src + b_bytes / 16u;
       float4* dst2 = reinterpret_cast<float4*>(sB2);
-      for (uint32_t e = threadIdx.x; e < b2_bytes / 16u; e += TC_THREADS) dst2[e] = __ldg(src2 + e);
+      for (uint32_t e = threadIdx.x; e < b2_bytes / 16u; e += blockDim.x) dst2[e] = __ldg(src2 + e);
     }
   }
   if (threadIdx.x == 0) {
@@ -217,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
     }
     for (int b = 0; b < a.nacc; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 4);
+      mbar_init(tempty + b, EPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -416,6 +429,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
   } else {
     // =================== epilogue ===================
     const int quarter = warp & 3;  // TMEM lanes 32*quarter ..
+    constexpr int SPLIT = EPI / 4;                       // warps per quarter
+    constexpr int CW = SPLIT > 1 ? 8 : 16;               // TMEM columns per chunk
+    const int half = (warp - 1 - TC_PRODUCERS) / 4;      // which column chunks
     uint32_t row_glob = 0;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_tile strip = a.strips[st];
@@ -431,16 +447,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.acc_cols);
         float* dst = a.S + job.s_off + (int64_t)y * wo + x;
-        // 16 filters at a time: hi-half columns [fc, fc+16) and lo-half [N+fc, ...)
+        // CW filters at a time: hi-half columns [fc, fc+CW) and lo-half [N+fc, ...)
 #pragma unroll
-        for (int fc = 0; fc < NMAX; fc += 16) {
-          if (fc < a.N) {
-            float vh[16], vl[16];
-            tmem_ld16(taddr + fc, vh);
-            tmem_ld16(taddr + a.N + fc, vl);
+        for (int fc = 0; fc < NMAX; fc += CW) {
+          if (fc < a.N && (fc / CW) % SPLIT == half) {
+            float vh[CW], vl[CW];
+            if constexpr (CW == 16) {
+              tmem_ld16(taddr + fc, vh);
+              tmem_ld16(taddr + a.N + fc, vl);
+            } else {
+              tmem_ld8(taddr + fc, vh);
+              tmem_ld8(taddr + a.N + fc, vl);
+            }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < CW; ++k) {
               const int f = fc + k;
               if (f < job.nf && x < wo) {
                 const float sv = vh[k] + vl[k];
@@ -459,6 +480,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) corr_tc_kernel(const TcArgs a) 
 #pragma unroll
         for (int f = 0; f < NMAX; ++f) {
           if (f >= job.nf) break;
+          if ((f / CW) % SPLIT != half) continue;
           float mx = vmax[f], mn = vmin[f];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
@@ -555,16 +577,19 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
                              : N <= 32 ? corr_tc_kernel<32, 0, 0>
                              : N <= 48 ? corr_tc_kernel<48, 0, 0>
                                        : corr_tc_kernel<64, 0, 0>;
-  if (h == 6 && w == 6 && R == 8)  // DPM part filters
-    fn = N <= 16 ? corr_tc_kernel<16, 6, 6>
-       : N <= 32 ? corr_tc_kernel<32, 6, 6>
-       : N <= 48 ? corr_tc_kernel<48, 6, 6>
-                 : corr_tc_kernel<64, 6, 6>;
+  int threads = TC_THREADS;
+  if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps
+    fn = N <= 16 ? corr_tc_kernel<16, 6, 6, 8>
+       : N <= 32 ? corr_tc_kernel<32, 6, 6, 8>
+       : N <= 48 ? corr_tc_kernel<48, 6, 6, 8>
+                 : corr_tc_kernel<64, 6, 6, 8>;
+    threads = 32 * (1 + TC_PRODUCERS + 8);
+  }
   else if (h == 6 && w == 11 && R == 8 && N <= 16)  // DPM root filters (3 mirrored pairs)
     fn = corr_tc_kernel<16, 6, 11>;
   DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = nstrips < sms ? nstrips : sms;
-  fn<<<grid, TC_THREADS, smem, as_stream(stream)>>>(a);
+  fn<<<grid, threads, smem, as_stream(stream)>>>(a);
   DPM_LAUNCHED("corr_tc_kernel");
   return DPM_OK;
 }
