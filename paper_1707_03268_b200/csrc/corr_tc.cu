@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
     // =================== epilogue ===================
     const int quarter = warp & 3;  // TMEM lanes 32*quarter ..
     constexpr int SPLIT = EPI / 4;                       // warps per quarter
-    constexpr int CW = SPLIT > 1 ? 8 : 16;               // TMEM columns per chunk
+    constexpr int CW = SPLIT == 2 ? 8 : 16;              // TMEM columns per chunk
+    constexpr int LOC = ((NMAX / CW + SPLIT - 1) / SPLIT) * CW;  // filters per warp
     const int half = (warp - 1 - TC_PRODUCERS) / 4;      // which column chunks
     uint32_t row_glob = 0;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
@@ -438,9 +439,9 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       const dpm_corr_job job = a.jobs[strip.job];
       const int ho = job.H - a.h + 1, wo = job.W - a.w + 1;
       const int x = strip.tx * TC_M + quarter * 32 + lane;
-      float vmax[NMAX], vmin[NMAX];
+      float vmax[LOC], vmin[LOC];  // this warp's chunks only (chunk c -> local c / SPLIT)
 #pragma unroll
-      for (int f = 0; f < NMAX; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
+      for (int f = 0; f < LOC; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
       for (int y = 0; y < ho; ++y, ++row_glob) {
         const int b = row_glob % a.nacc;
         mbar_wait(tfull + b, (row_glob / a.nacc) & 1);
@@ -462,12 +463,12 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int k = 0; k < CW; ++k) {
-              const int f = fc + k;
+              const int f = fc + k, li = (fc / CW / SPLIT) * CW + k;
               if (f < job.nf && x < wo) {
                 const float sv = vh[k] + vl[k];
                 dst[(int64_t)f * ho * wo] = sv;
-                vmax[f] = fmaxf(vmax[f], sv);
-                vmin[f] = fminf(vmin[f], sv);
+                vmax[li] = fmaxf(vmax[li], sv);
+                vmin[li] = fminf(vmin[li], sv);
               }
             }
           }
@@ -478,10 +479,10 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       }
       if (a.ranges != nullptr && job.range_idx >= 0) {
 #pragma unroll
-        for (int f = 0; f < NMAX; ++f) {
-          if (f >= job.nf) break;
-          if ((f / CW) % SPLIT != half) continue;
-          float mx = vmax[f], mn = vmin[f];
+        for (int li = 0; li < LOC; ++li) {
+          const int f = ((li / CW) * SPLIT + half) * CW + li % CW;
+          if (f >= job.nf) continue;
+          float mx = vmax[li], mn = vmin[li];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -578,7 +579,7 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
                              : N <= 48 ? corr_tc_kernel<48, 0, 0>
                                        : corr_tc_kernel<64, 0, 0>;
   int threads = TC_THREADS;
-  if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps
+  if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps (12 measured slower)
     fn = N <= 16 ? corr_tc_kernel<16, 6, 6, 8>
        : N <= 32 ? corr_tc_kernel<32, 6, 6, 8>
        : N <= 48 ? corr_tc_kernel<48, 6, 6, 8>
