@@ -371,7 +371,9 @@ def run_ours(args):
                          "note": "peak = per-launch roofline mix: tcgen05 3xTF32 launches vs the "
                                  "tf32 rate / 3, FFMA launches vs the FP32 FFMA rate",
                          "ffma_probe_tflops": probe_tflops,
-                         "traffic": traffic.get("corr_tc_kernel")},
+                         "traffic": (traffic["corr_tc_kernel"] + traffic["corr_kernel"]
+                                     if "corr_tc_kernel" in traffic and "corr_kernel" in traffic
+                                     else None)},
         "k1_project": {"bound": "hbm", "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm,
                        "unit": "GB/s", "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm,
                        "algorithmic_bytes_per_launch": k1_bytes,

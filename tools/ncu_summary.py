@@ -122,7 +122,11 @@ def main(launch_csv, rep, images, tag):
             dram = rec.get("dram_read", 0) + rec.get("dram_write", 0)
             name = rec["kernel"]
             # ncu reports bytes in the unit of the column (MB in --csv raw for these metrics)
-            traffic.setdefault(name.split("<")[0], dram * 1e6 / images)
+            # one entry per kernel family (template instantiations summed: a
+            # step launches each family's instantiations once)
+            fam = name.split("<")[0]
+            if "at::" not in name and "elementwise" not in name:
+                traffic[fam] = traffic.get(fam, 0.0) + dram * 1e6 / images
             fh.write(f"| `{name}` | {rec.get('duration', 0):.1f} | {dram:.1f} | "
                      f"{dram / images:.2f} | {rec.get('tensor_pipe_%', 0):.1f} | "
                      f"{rec.get('fma_pipe_%', 0):.1f} | {rec.get('fp64_pipe_%', 0):.1f} | "
