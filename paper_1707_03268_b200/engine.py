@@ -104,7 +104,7 @@ class Plan:
 
     def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
                  outputs=("totals", "positions"), max_dets=0, device=None, tensor_cores=True,
-                 tc_min_width=64, envelope=False):
+                 tc_min_width=16, envelope=False):
         import torch
 
         require_cuda()
