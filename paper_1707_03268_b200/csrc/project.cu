@@ -61,19 +61,29 @@ project_kernel(const float* __restrict__ X, float* __restrict__ P, const float* 
   const float* xr = sX + t * (L + 1);
   const int64_t plane = (int64_t)job.H * job.pitch;
   float* dst = P + job.p_off + (int64_t)y * job.pitch + x;
+  // FFMA2: the channel value broadcast as {x, x}, C read as 64-bit pairs
+  // straight into register pairs -- the same per-element fma as a scalar
+  // loop, half the FMA issue slots.
   for (int r0 = 0; r0 < R; r0 += K1_RC) {
-    float acc[K1_RC];
+    unsigned long long acc[K1_RC / 2];
 #pragma unroll
-    for (int k = 0; k < K1_RC; ++k) acc[k] = 0.f;
+    for (int k = 0; k < K1_RC / 2; ++k) acc[k] = 0ull;
     for (int l = 0; l < L; ++l) {
       const float xv = xr[l];
-      const float* cr = sC + l * Rp + r0;
+      unsigned long long xx;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(xv));
+      const unsigned long long* cr = reinterpret_cast<const unsigned long long*>(sC + l * Rp + r0);
 #pragma unroll
-      for (int k = 0; k < K1_RC; ++k) acc[k] = fmaf(xv, cr[k], acc[k]);
+      for (int k = 0; k < K1_RC / 2; ++k)
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[k]) : "l"(xx), "l"(cr[k]));
     }
 #pragma unroll
-    for (int k = 0; k < K1_RC; ++k)
-      if (r0 + k < R) dst[(int64_t)(r0 + k) * plane] = acc[k];
+    for (int k = 0; k < K1_RC / 2; ++k) {
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[k]));
+      if (r0 + 2 * k < R) dst[(int64_t)(r0 + 2 * k) * plane] = lo;
+      if (r0 + 2 * k + 1 < R) dst[(int64_t)(r0 + 2 * k + 1) * plane] = hi;
+    }
   }
 }
 
