@@ -785,3 +785,96 @@ def test_calibration_known_answers():
                        parts=((hyp.parts[0][0] + 9, hyp.parts[0][1]),) + tuple(hyp.parts[1:]))
     with pytest.raises(B.ValidationError, match="search radius|out of support"):
         B.calibrate_thresholds(dec, [(level, bad)])
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_randomized_plans_against_oracle(seed):
+    """Seeded random plans: filter shapes 1..8 x 1..12, ranks {1, 3, 8, 16}
+    (tcgen05 and FFMA classes), levels down to filter size, scale 1 or 2,
+    windowed radii {0, 1, 3, 17 (> the staged cap)} or the unbounded r*,
+    zero / negative linear deformation terms.  Maps within 1e-5 of the FP64
+    oracle; placement and totals bit-identical to the oracle run on the GPU's
+    own maps."""
+    from paper_1707_03268_b200.engine import AssemblyDef, FilterDef, PartDef, Plan
+    from paper_1707_03268_b200.geometry import gdt_root_rect
+
+    rng = np.random.default_rng(1000 + seed)
+    L = int(rng.choice([4, 7, 32]))
+    R = int(rng.choice([1, 3, 8, 16]))
+    scale = int(rng.integers(1, 3))
+    gdt = bool(rng.integers(0, 2))
+    C = rng.normal(size=(L, R)).astype(np.float32)
+    rh, rw = int(rng.integers(1, 7)), int(rng.integers(1, 13))
+    nparts = int(rng.integers(0, 4))
+    pshapes = [(int(rng.integers(1, 9)), int(rng.integers(1, 9))) for _ in range(nparts)]
+    Hr = max([rh] + [h for h, _ in pshapes]) + int(rng.integers(0, 30))
+    Wr = max([rw] + [w for _, w in pshapes]) + int(rng.integers(0, 150))
+    Hp, Wp = (Hr, Wr) if scale == 1 else (2 * Hr + int(rng.integers(0, 3)), 2 * Wr + int(rng.integers(0, 3)))
+    Hp = max(Hp, max([s[0] for s in pshapes], default=1))
+    Wp = max(Wp, max([s[1] for s in pshapes], default=1))
+    levels = [(Hr, Wr)] if scale == 1 else [(Hr, Wr), (Hp, Wp)]
+    kp = 0 if scale == 1 else 1
+    cores = [rng.normal(0, 0.3, (rh, rw, R)).astype(np.float32)] + \
+        [rng.normal(0, 0.3, (h, w, R)).astype(np.float32) for h, w in pshapes]
+    filters = [FilterDef(c) for c in cores]
+    defs, anchors = [], []
+    for h, w in pshapes:
+        q = rng.uniform(0.005, 0.1, 2) if gdt else rng.choice([0.0, 0.02, 0.1], 2)
+        defs.append((float(rng.uniform(-0.05, 0.05)), float(rng.uniform(-0.05, 0.05)),
+                     float(q[0]), float(q[1])))
+        anchors.append((int(rng.integers(0, max(1, scale * rh))), int(rng.integers(0, max(1, scale * rw)))))
+    radius = -1 if gdt else int(rng.choice([0, 1, 3, 17]))
+    rs = (Hr - rh + 1, Wr - rw + 1)
+    if gdt:
+        rect = gdt_root_rect(rs, [(Hp - h + 1, Wp - w + 1) for h, w in pshapes], anchors, scale)
+        if rect is None:
+            pytest.skip("empty GDT domain for this draw")
+    else:  # every part window within r of its support (as _hypothesis_rect, scaled)
+        ry0, ry1, rx0, rx1 = 0, rs[0] - 1, 0, rs[1] - 1
+        for (h, w), (ay, ax) in zip(pshapes, anchors):
+            sy, sx = Hp - h + 1, Wp - w + 1
+            ry0 = max(ry0, -((ay + radius) // scale))
+            ry1 = min(ry1, (sy - 1 + radius - ay) // scale)
+            rx0 = max(rx0, -((ax + radius) // scale))
+            rx1 = min(rx1, (sx - 1 + radius - ax) // scale)
+        if ry0 > ry1 or rx0 > rx1:
+            pytest.skip("empty root rectangle for this draw")
+        rect = (ry0, ry1, rx0, rx1)
+    parts = tuple(PartDef(kp, 1 + i, anchors[i], defs[i], radius, scale) for i in range(nparts))
+    asm = AssemblyDef((0, 0), rect, parts, bias=0.25)
+    plan = Plan(L, levels, C, filters, assemblies=[asm], outputs=("totals", "positions", "placed"))
+    X = [rng.uniform(0, 0.4, (h, w, L)).astype(np.float32) for h, w in levels]
+    plan.load_levels(0, X)
+    plan.run()
+    P = [O.project(x.astype(np.float64), C.astype(np.float64)) for x in X]
+    gmaps = []
+    for f, core in enumerate(cores):
+        k = 0 if f == 0 else kp
+        ref = O.correlate3_full(P[k], core.astype(np.float64))
+        gm = plan.map(0, k, f).double().cpu().numpy()
+        assert_map_close(gm, ref, f"seed {seed} filter {f}")
+        gmaps.append(gm)
+    out = {k: v.cpu().numpy() for k, v in plan.assembly_outputs(0, 0).items()}
+    ry0, ry1, rx0, rx1 = rect
+    tot = gmaps[0][ry0:ry1 + 1, rx0:rx1 + 1].copy()
+    for i in range(nparts):
+        r = O.r_star(gmaps[1 + i], defs[i]) if gdt else radius
+        placed, py, px = O.place_gathered(gmaps[1 + i], anchors[i], defs[i], r, scale, rect)
+        from paper_1707_03268_b200.engine import unpack_positions
+
+        gy, gx = unpack_positions(out["positions"][i])
+        assert np.array_equal(out["placed"][i], placed), (seed, i)
+        assert np.array_equal(gy, py) and np.array_equal(gx, px), (seed, i)
+        tot = tot + placed
+    assert np.array_equal(out["totals"], tot + 0.25), seed
+    if gdt and nparts:  # the lower-envelope kernels: same placements up to exact ties
+        env = Plan(L, levels, C, filters, assemblies=[asm],
+                   outputs=("totals", "positions", "placed"), envelope=True)
+        assert env._asm_gdt.all()
+        env.load_levels(0, X)
+        env.run()
+        eo = {k: v.cpu().numpy() for k, v in env.assembly_outputs(0, 0).items()}
+        same = eo["positions"] == out["positions"]
+        assert np.array_equal(eo["placed"][same], out["placed"][same])
+        d = np.abs(eo["placed"][~same] - out["placed"][~same])
+        assert np.all(d <= 4 * np.spacing(np.abs(out["placed"][~same]))), seed
