@@ -22,7 +22,7 @@ from .detection import (_placement_grid, best_part_placement, calibrate_threshol
 from . import formats  # noqa: F401
 from .evaluation import RocPoint, match_detections, nms, nms_records, roc_eval
 from .errors import CpdetectError, DeviceError, FormatError, NumericError, ValidationError
-from .pipeline import PyramidScorer, cores_from_stacked
+from .pipeline import PyramidScorer, cores_from_stacked, detect_batch, score_pyramid
 from .types import (CPModel, DecomposedModel, DecomposedPart, Detection, DetectStats,
                     Hypothesis, PartModel, PartSpec)
 
@@ -35,7 +35,7 @@ __all__ = [
     "best_part_placement", "cores_from_stacked", "correlate3_cp", "correlate3_full",
     "cp_multiplications", "cp_partial_stack", "cp_score_hypothesis", "deformation_penalty",
     "dense_detect", "detect",
-    "calibrate_thresholds", "nms", "nms_records", "match_detections", "roc_eval",
+    "calibrate_thresholds", "score_pyramid", "detect_batch", "nms", "nms_records", "match_detections", "roc_eval",
     "RocPoint", "full_multiplications", "score_hypothesis", "theoretical_gain",
     "valid_support", "validate",
 ]

@@ -20,7 +20,7 @@ from .engine import AssemblyDef, FilterDef, PartDef, Plan, unpack_positions
 from .errors import ValidationError
 from .geometry import gdt_root_rect, hypothesis_rect
 
-__all__ = ["PyramidScorer", "cores_from_stacked"]
+__all__ = ["PyramidScorer", "cores_from_stacked", "score_pyramid", "detect_batch"]
 
 
 def cores_from_stacked(bank, G):
@@ -228,3 +228,35 @@ class PyramidScorer:
 
     def k2_flops_per_image(self):
         return self.plan.k2_flops()
+
+
+def score_pyramid(bank, C, G, pyramid, levels, radius=-1, domain="gdt", components=None,
+                  envelope=False):
+    """One image through K1-K4 (SURVEY.md §8(b) batched API): per (root level,
+    component) the root-level total map and the part argmaxes.
+
+    ``levels`` are the image's pyramid levels ((H, W, L) arrays in the
+    geometry of ``pyramid``).  Returns ``PyramidScorer.results(0)``: dicts with
+    ``root_level``, ``component``, ``rect``, ``scores`` (float64 [hr][wr]) and
+    ``parts`` (int [n_parts][hr][wr][2], (y, x) part positions)."""
+    sc = PyramidScorer(bank, C, G, pyramid, n_images=1, radius=radius, domain=domain,
+                       components=components, envelope=envelope)
+    sc.load_image(0, levels)
+    sc.run()
+    return sc.results(0)
+
+
+def detect_batch(bank, C, G, pyramid, images, tau, max_dets=1 << 20, radius=-1,
+                 domain="gdt", components=None, chunk_images=2, envelope=False):
+    """Many images end to end: host pyramids in, detection
+    records with total >= tau out (structured array of ``_lib.DETECTION``:
+    image, level, component, ry, rx, nparts, score, packed part positions).
+    The pyramids are staged in a pinned arena and scored by
+    :meth:`PyramidScorer.score_batch` (H2D pipelined with compute)."""
+    images = list(images)
+    sc = PyramidScorer(bank, C, G, pyramid, n_images=len(images), radius=radius, domain=domain,
+                       max_dets=max_dets, components=components, envelope=envelope)
+    host = sc.host_arena(pinned=True)
+    for i, levels in enumerate(images):
+        sc.fill_host(host, i, levels)
+    return sc.score_batch(host, tau, chunk_images=chunk_images)

@@ -905,3 +905,27 @@ def test_plan_run_is_cuda_graph_capturable():
     for (ts, tp), r in zip(direct, sc.results(0)):
         assert np.array_equal(ts, r["scores"]) and np.array_equal(tp, r["parts"])
     assert int(sc.plan.det_count.item()) == ndirect > 0
+
+
+def test_batched_apis_score_pyramid_and_detect_batch():
+    """score_pyramid == PyramidScorer.results for one image; detect_batch ==
+    the detections implied by the per-image totals (same records)."""
+    wl = synth.workload(2)
+    C, G = _shared(2, 8)
+    lv0, lv1 = (synth.hog_pyramid(2, i, wl.pyramid) for i in (0, 1))
+    res = B.score_pyramid(wl.bank, C, G, wl.pyramid, lv0)
+    sc = PyramidScorer(wl.bank, C, G, wl.pyramid)
+    sc.load_image(0, lv0)
+    for a, b in zip(res, sc.run().results(0)):
+        assert np.array_equal(a["scores"], b["scores"]) and np.array_equal(a["parts"], b["parts"])
+    tau = 2.0
+    dets = B.detect_batch(wl.bank, C, G, wl.pyramid, [lv0, lv1], tau)
+    got = sorted((int(d["image"]), int(d["level"]), int(d["component"]), int(d["ry"]),
+                  int(d["rx"])) for d in dets)
+    want = []
+    for img, lv in ((0, lv0), (1, lv1)):
+        for r in B.score_pyramid(wl.bank, C, G, wl.pyramid, lv):
+            ry0, _, rx0, _ = r["rect"]
+            for iy, ix in zip(*np.nonzero(r["scores"] >= tau)):
+                want.append((img, r["root_level"], r["component"], ry0 + int(iy), rx0 + int(ix)))
+    assert got == sorted(want) and len(got) > 0
