@@ -124,8 +124,17 @@ size_t dpm_correlate_tc_smem(int h, int w, int R, int nf);
  * followed -- for the compile-time DPM shapes (R = 8, h = 6, w in {6, 11}),
  * whose kernel runs the correction MMA in bf16 over tap pairs -- by the bf16
  * block [h][ceil(w/2)][2][N][8] of the tf32-truncated values (tap 2p then
- * 2p+1; zeros past w). */
+ * 2p+1; zeros past w).  When dpm_correlate_tc_stack() returns KS > 1 the
+ * block is the stacked layout instead (KS output rows per accumulator group):
+ * with NB = h + 2(KS-1) tap-row blocks, block b holding tap row
+ * i = h-1+KS-1-b (zeros outside 0..h-1) as 16 N-rows [hi of filters 0..7 |
+ * lo of filters 0..7], the tf32 part is [w][R/4][NB*16][4] and the bf16 part
+ * [ceil(w/2)][2][NB*16][8] (hi values in rows 0..7 of each block, 0 in
+ * rows 8..15). */
 size_t dpm_correlate_tc_core_floats(int h, int w, int R, int nf);
+/* Output rows per accumulator group of the tcgen05 kernel for this shape:
+ * 6 for the compile-time DPM shapes with nf <= 8 (e.g. the DPM roots), else 1. */
+int dpm_correlate_tc_stack(int h, int w, int R, int nf);
 int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
                      const dpm_corr_tile* strips, int nstrips, int h, int w, int R, int nf,
                      uint32_t* ranges, void* stream);

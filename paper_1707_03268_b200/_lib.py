@@ -77,6 +77,7 @@ _SIGNATURES = {
     "dpm_correlate_tc_smem": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
     "dpm_correlate_tc": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "dpm_correlate_tc_core_floats": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
+    "dpm_correlate_tc_stack": (_i32, [_i32, _i32, _i32, _i32]),
     "dpm_place_prepare": (_i64, [_vp, _i32]),
     "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
     "dpm_place_ranges": (_i32, [_vp, _i32, _vp, _vp, _vp]),

@@ -188,7 +188,10 @@ __device__ __forceinline__ float tf32_hi(float a) {
 // extent fixed at compile time (R == 8), fully unrolled MMA issue.
 // EPI: epilogue warps (4, or 8 = two per TMEM lane quarter, each draining
 // alternate 16-filter column chunks).
-template <int NMAX, int FH, int FW, int EPI = 4>
+// KS > 1 (R == 8, FH/FW fixed, at most 8 filters): output rows stacked KS at
+// a time into one accumulator group [hi(y) lo(y) hi(y+1) lo(y+1) ...] (16
+// columns per row); see tc_stack() for the core layout.
+template <int NMAX, int FH, int FW, int EPI = 4, int KS = 1>
 __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kernel(const TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -196,9 +199,11 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
   const int taps = a.h * a.w;
   const int tcols = TC_M + a.w - 1;
   constexpr bool BF = FH > 0;  // bf16 correction MMA (compile-time shapes, R == 8)
-  const uint32_t b_bytes = (uint32_t)taps * nq * (2 * a.N) * 16u;
+  constexpr int NB = FH + 2 * (KS - 1);  // stacked core: tap-row blocks per tap column
   const uint32_t npairs = (uint32_t)(a.w + 1) / 2;
-  const uint32_t b2_bytes = BF ? (uint32_t)a.h * npairs * 2u * a.N * 16u : 0u;
+  const uint32_t b_bytes = KS > 1 ? (uint32_t)FW * NB * 512u : (uint32_t)taps * nq * (2 * a.N) * 16u;
+  const uint32_t b2_bytes = KS > 1 ? npairs * NB * 512u
+                          : BF     ? (uint32_t)a.h * npairs * 2u * a.N * 16u : 0u;
   const uint32_t hi_bytes = (uint32_t)nq * tcols * 16u;
   const uint32_t slot_bytes = BF ? ((hi_bytes + (tcols + 1u) * 16u + 127u) & ~127u)
                                  : 2u * hi_bytes;  // hi then lo
@@ -267,6 +272,120 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
     const uint32_t b2_pair = (2u * a.N * 16u) >> 4;
     const uint32_t idescbf = idesc_bf16(a.N);
     uint32_t q_glob = 0, row_glob = 0;
+    if constexpr (KS > 1) {
+      // Stacked rows: input row y+t meets output row y+k through tap row
+      // i = t-k, so ONE MMA per (input row, tap column) updates all KS rows of
+      // the group with the core window [B(t), B(t-1), ..., B(t-KS+1)] (zero
+      // blocks outside 0..FH-1).  Each staged row is read (KS+FH-1)/KS times
+      // per output row instead of FH times.  With few filters each MMA's cost
+      // is dominated by reading its 128-row A operand from shared memory, so
+      // fewer, wider MMAs (N = 16*KS) are the saving.
+      constexpr int NP = (FW + 1) / 2;
+      const uint32_t idesc_s = idesc_tf32(16 * KS), idesc_sb = idesc_bf16(16 * KS);
+      const uint64_t dBs = umma_desc(smem_u32(sB), NB * 256u, 128u);
+      const uint64_t dB2s = umma_desc(smem_u32(sB2), NB * 256u, 128u);
+      for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
+        const dpm_corr_job job = a.jobs[a.strips[st].job];
+        const int ho = job.H - FH + 1;
+        int qready = 0;  // rows of this strip known to be staged
+        int y = 0;
+        for (; y < ho; y += KS, ++row_glob) {
+          const int b = row_glob % a.nacc;
+          mbar_wait(tempty + b, ((row_glob / a.nacc) & 1) ^ 1);
+          const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
+          const int tmax = min(KS + FH - 1, job.H - y);
+          for (int t = 0; t < tmax; ++t) {
+            const uint32_t q = q_glob + y + t;
+            if (y + t >= qready) {
+              mbar_wait(full + q % a.ring, (q / a.ring) & 1);
+              qready = y + t + 1;
+            }
+            tc_fence_after();
+            const uint64_t da = dA0 + (q % a.ring) * slot_step;
+            const uint64_t dal = dAlo0 + (q % a.ring) * slot_step;
+            const uint32_t s0 = (uint32_t)(FH - 1 + KS - 1 - t) * 16u;  // window start (>> 4)
+            if (elect_one()) {
+#pragma unroll
+              for (int j = 0; j < FW; ++j)
+                mma_tf32(d, da + (uint32_t)j, dBs + (uint32_t)(j * NB * 32) + s0, idesc_s,
+                         (t | j) != 0);
+#pragma unroll
+              for (int jp = 0; jp < NP; ++jp)
+                mma_bf16(d, dal + (uint32_t)(2 * jp), dB2s + (uint32_t)(jp * NB * 32) + s0, idesc_sb);
+            }
+            __syncwarp();
+          }
+          if (elect_one()) {
+            tc_commit(tfull + b);
+            for (int k = 0; k < KS && y + k < job.H; ++k) tc_commit(empty + (q_glob + y + k) % a.ring);
+          }
+          __syncwarp();
+        }
+        if (elect_one())  // rows no group released (past the last group's first KS)
+          for (int rr = y; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
+        __syncwarp();
+        q_glob += job.H;
+      }
+    } else if constexpr (FH > 0) {
+      // Output rows in pairs: the taps of rows y and y+1 go to two TMEM
+      // accumulators alternately, so consecutive MMAs never chain on the same
+      // accumulator (a dependent chain issues at a fraction of the pipe rate
+      // when each MMA is short, N = 32..96).
+      for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
+        const dpm_corr_job job = a.jobs[a.strips[st].job];
+        const int ho = job.H - FH + 1;
+        for (int y = 0; y < ho; y += 2, row_glob += 2) {
+          const bool two = y + 1 < ho;
+          const int b0 = row_glob % a.nacc, b1 = (row_glob + 1) % a.nacc;
+          mbar_wait(tempty + b0, ((row_glob / a.nacc) & 1) ^ 1);
+          if (two) mbar_wait(tempty + b1, (((row_glob + 1) / a.nacc) & 1) ^ 1);
+          const int rlast = two ? FH : FH - 1;
+          for (int rr = (y == 0 ? 0 : FH - 1); rr <= rlast; ++rr) {
+            const uint32_t q = q_glob + y + rr;
+            mbar_wait(full + q % a.ring, (q / a.ring) & 1);
+          }
+          tc_fence_after();
+          const uint32_t d0 = tmem_base + (uint32_t)(b0 * a.acc_cols);
+          const uint32_t d1 = tmem_base + (uint32_t)(b1 * a.acc_cols);
+          uint64_t da_row[FH + 1], da_lo[FH + 1];
+#pragma unroll
+          for (int i = 0; i <= FH; ++i) {
+            da_row[i] = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
+            da_lo[i] = dAlo0 + ((q_glob + y + i) % a.ring) * slot_step;
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int i = 0; i < FH; ++i)
+#pragma unroll
+              for (int j = 0; j < FW; ++j) {
+                const uint64_t bb = dB0 + (uint32_t)((i * FW + j) * 2) * (uint32_t)(lboB >> 4);
+                mma_tf32(d0, da_row[i] + (uint32_t)j, bb, idesc1, (i | j) != 0);
+                if (two) mma_tf32(d1, da_row[i + 1] + (uint32_t)j, bb, idesc1, (i | j) != 0);
+              }
+#pragma unroll
+            for (int i = 0; i < FH; ++i)
+#pragma unroll
+              for (int jp = 0; jp < (FW + 1) / 2; ++jp) {
+                const uint64_t b2 = dB2 + (uint32_t)((i * ((FW + 1) / 2) + jp) * b2_pair);
+                mma_bf16(d0, da_lo[i] + (uint32_t)(2 * jp), b2, idescbf);
+                if (two) mma_bf16(d1, da_lo[i + 1] + (uint32_t)(2 * jp), b2, idescbf);
+              }
+            tc_commit(tfull + b0);
+            tc_commit(empty + (q_glob + y) % a.ring);
+            if (two) {
+              tc_commit(tfull + b1);
+              tc_commit(empty + (q_glob + y + 1) % a.ring);
+            }
+          }
+          __syncwarp();
+          if (!two) row_glob -= 1;  // odd tail: one row
+        }
+        if (elect_one())
+          for (int rr = ho; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
+        __syncwarp();
+        q_glob += job.H;
+      }
+    } else
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
       const int ho = job.H - a.h + 1;
@@ -279,35 +398,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         }
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
-        if constexpr (FH > 0) {
-          // compile-time taps: every descriptor is a row base + immediate
-          uint64_t da_row[FH], da_lo[FH];
-#pragma unroll
-          for (int i = 0; i < FH; ++i) {
-            da_row[i] = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
-            da_lo[i] = dAlo0 + ((q_glob + y + i) % a.ring) * slot_step;
-          }
-          if (elect_one()) {
-#pragma unroll
-            for (int i = 0; i < FH; ++i)
-#pragma unroll
-              for (int j = 0; j < FW; ++j) {
-                const uint64_t ahi = da_row[i] + (uint32_t)j;
-                const uint64_t bb = dB0 + (uint32_t)((i * FW + j) * 2) * (uint32_t)(lboB >> 4);
-                mma_tf32(d, ahi, bb, idesc1, (i | j) != 0);
-              }
-            // bf16 correction over tap pairs: A_lo rows at +16 B per position
-#pragma unroll
-            for (int i = 0; i < FH; ++i)
-#pragma unroll
-              for (int jp = 0; jp < (FW + 1) / 2; ++jp) {
-                const uint64_t alo = da_lo[i] + (uint32_t)(2 * jp);
-                const uint64_t b2 = dB2 + (uint32_t)((i * ((FW + 1) / 2) + jp) * b2_pair);
-                mma_bf16(d, alo, b2, idescbf);
-              }
-          }
-          __syncwarp();
-        } else {
+        {
           uint64_t db = dB0;
           for (int i = 0; i < a.h; ++i) {
             const uint64_t da_row = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
@@ -429,6 +520,60 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
   } else {
     // =================== epilogue ===================
     const int quarter = warp & 3;  // TMEM lanes 32*quarter ..
+    if constexpr (KS > 1) {
+      uint32_t row_glob = 0;
+      for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
+        const dpm_corr_tile strip = a.strips[st];
+        const dpm_corr_job job = a.jobs[strip.job];
+        const int ho = job.H - FH + 1, wo = job.W - FW + 1;
+        const int x = strip.tx * TC_M + quarter * 32 + lane;
+        float vmax[8], vmin[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
+        for (int y = 0; y < ho; y += KS, ++row_glob) {
+          const int b = row_glob % a.nacc;
+          mbar_wait(tfull + b, (row_glob / a.nacc) & 1);
+          tc_fence_after();
+          const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.acc_cols);
+#pragma unroll
+          for (int k = 0; k < KS; ++k) {
+            if (y + k >= ho) break;
+            float v[16];  // hi 0..7 | lo 8..15 of row y+k
+            tmem_ld16(taddr + 16 * k, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float* dst = a.S + job.s_off + (int64_t)(y + k) * wo + x;
+#pragma unroll
+            for (int f = 0; f < 8; ++f) {
+              if (f < job.nf && x < wo) {
+                const float sv = v[f] + v[8 + f];
+                dst[(int64_t)f * ho * wo] = sv;
+                vmax[f] = fmaxf(vmax[f], sv);
+                vmin[f] = fminf(vmin[f], sv);
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty + b);
+        }
+        if (a.ranges != nullptr && job.range_idx >= 0) {
+#pragma unroll
+          for (int f = 0; f < 8; ++f) {
+            if (f >= job.nf) continue;
+            float mx = vmax[f], mn = vmin[f];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            }
+            if (lane == 0 && mx >= mn) {
+              atomicMax(a.ranges + 2 * (job.range_idx + f), float_key(mx));
+              atomicMin(a.ranges + 2 * (job.range_idx + f) + 1, float_key(mn));
+            }
+          }
+        }
+      }
+    } else {
     constexpr int SPLIT = EPI / 4;                       // warps per quarter
     constexpr int CW = SPLIT == 2 ? 8 : 16;              // TMEM columns per chunk
     constexpr int LOC = ((NMAX / CW + SPLIT - 1) / SPLIT) * CW;  // filters per warp
@@ -495,6 +640,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         }
       }
     }
+    }
   }
 
   tc_fence_before();
@@ -507,15 +653,31 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
 
 using namespace dpm;
 
-// Input-row ring depth: at least h + 2 (the h rows of an output row plus
-// slack), then as deep as shared memory allows (up to TC_MAX_RING), so the
-// producers run further ahead of the MMA warp and hide row-load latency.
 // compile-time shapes of the launcher (DPM part / root filters at R = 8):
 // they use the bf16 correction MMA and its smem layout
 static bool tc_bf16(int h, int w, int R) { return R == 8 && h == 6 && (w == 6 || w == 11); }
 
+// Rows stacked per accumulator group (1 = one output row per group).  Stacked
+// groups (<= 8 filters, e.g. the DPM roots: 3 mirrored pairs) take the core as
+// tap-row windows: per tap column j, NB = h + 2(KS-1) blocks of 16 N-rows
+// [hi 8 filters | lo 8 filters] for tap rows i = h-1+KS-1 down to -(KS-1)
+// (zero outside 0..h-1), K-major [j][quad][NB*16][4] fp32; then the bf16
+// tap-pair blocks [pair][tap parity][NB*16][8] with rows 8..15 of each block 0.
+// KS = 6 (measured sweep, roots 6x11 at config 4: KS 1/3/4/5/6 -> 1.54/1.00/
+// 0.90/0.86/0.83 ms) is the deepest whose core + minimal ring fit 227 KB.
+static int tc_stack(int h, int w, int R, int nf) { return tc_bf16(h, w, R) && nf <= 8 ? 6 : 1; }
+
+static size_t tc_b_bytes(int h, int w, int R, int nf) {
+  const int ks = tc_stack(h, w, R, nf);
+  if (ks > 1) return ((size_t)w * (h + 2 * (ks - 1)) * 512 + 1023) & ~(size_t)1023;
+  const int N = (nf + 15) & ~15;
+  return ((size_t)h * w * (R / 4) * 2 * N * 16 + 1023) & ~(size_t)1023;
+}
+
 static size_t tc_b2_bytes(int h, int w, int R, int nf) {
   if (!tc_bf16(h, w, R)) return 0;
+  const int ks = tc_stack(h, w, R, nf);
+  if (ks > 1) return ((size_t)((w + 1) / 2) * (h + 2 * (ks - 1)) * 512 + 1023) & ~(size_t)1023;
   const int N = (nf + 15) & ~15;
   return ((size_t)h * ((w + 1) / 2) * 2 * N * 16 + 1023) & ~(size_t)1023;
 }
@@ -527,28 +689,35 @@ static size_t tc_slot(int h, int w, int R) {
   return 2ull * nq * tcols * 16;
 }
 
+// Input-row ring depth: at least the rows one accumulator group reads plus
+// slack (h + KS + 1), then as deep as shared memory allows (up to
+// TC_MAX_RING), so the producers run further ahead of the MMA warp and hide
+// row-load latency.
 static int tc_ring(int h, int w, int R, int nf) {
-  const int N = (nf + 15) & ~15;
-  const int nq = R / 4;
-  const size_t b = ((size_t)h * w * nq * 2 * N * 16 + 1023) & ~(size_t)1023;
   const size_t slot = tc_slot(h, w, R);
-  const size_t fixed = b + tc_b2_bytes(h, w, R, nf) + (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16 + 15;
-  int ring = h + 2 <= TC_MAX_RING ? h + 2 : TC_MAX_RING;
+  const size_t fixed = tc_b_bytes(h, w, R, nf) + tc_b2_bytes(h, w, R, nf) +
+                       (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16 + 15;
+  const int need = h + tc_stack(h, w, R, nf) + 1;
+  int ring = need <= TC_MAX_RING ? need : TC_MAX_RING;
   while (ring < TC_MAX_RING && fixed + (ring + 1) * slot <= 227 * 1024) ++ring;
   return ring;
 }
 
+extern "C" int dpm_correlate_tc_stack(int h, int w, int R, int nf) { return tc_stack(h, w, R, nf); }
+
 extern "C" size_t dpm_correlate_tc_smem(int h, int w, int R, int nf) {
-  const int N = (nf + 15) & ~15;
-  const int nq = R / 4;
-  const size_t b = (size_t)h * w * nq * 2 * N * 16;
   const int ring = tc_ring(h, w, R, nf);
   const size_t slot = tc_slot(h, w, R);
-  return ((b + 1023) & ~(size_t)1023) + tc_b2_bytes(h, w, R, nf) +
-         ((ring * slot + 15) & ~(size_t)15) + (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
+  return tc_b_bytes(h, w, R, nf) + tc_b2_bytes(h, w, R, nf) + ((ring * slot + 15) & ~(size_t)15) +
+         (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
 }
 
 extern "C" size_t dpm_correlate_tc_core_floats(int h, int w, int R, int nf) {
+  const int ks = tc_stack(h, w, R, nf);
+  if (ks > 1) {
+    const size_t nb = (size_t)h + 2 * (ks - 1);
+    return (size_t)w * nb * 128 + (size_t)((w + 1) / 2) * nb * 128;  // 512 B per block
+  }
   const int N = (nf + 15) & ~15;
   size_t f = (size_t)h * w * (R / 4) * 2 * N * 4;
   if (tc_bf16(h, w, R)) f += (size_t)h * ((w + 1) / 2) * 2 * N * 8 / 2;  // bf16 block
@@ -579,7 +748,13 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
                              : N <= 48 ? corr_tc_kernel<48, 0, 0>
                                        : corr_tc_kernel<64, 0, 0>;
   int threads = TC_THREADS;
-  if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps (12 measured slower)
+  const int ks = tc_stack(h, w, R, nf);
+  if (ks > 1) {  // <= 8 filters (DPM roots: 3 mirrored pairs): rows stacked 6 per group
+    a.N = 8;
+    a.acc_cols = 16 * ks;
+    a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
+    fn = w == 11 ? corr_tc_kernel<8, 6, 11, 4, 6> : corr_tc_kernel<8, 6, 6, 4, 6>;
+  } else if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps (12 measured slower)
     fn = N <= 16 ? corr_tc_kernel<16, 6, 6, 8>
        : N <= 32 ? corr_tc_kernel<32, 6, 6, 8>
        : N <= 48 ? corr_tc_kernel<48, 6, 6, 8>

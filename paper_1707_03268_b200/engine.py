@@ -610,6 +610,9 @@ def _tc_core(cores):
     N = _round_up(nf, 16)
     hi = (core.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
     lo = (core - hi).astype(np.float32)
+    ks = int(_lib.lib().dpm_correlate_tc_stack(h, w, R, nf))
+    if ks > 1:
+        return _tc_core_stacked(hi, lo, ks)
     out = np.zeros((h * w, R // 4, 2 * N, 4), dtype=np.float32)
     for src, base in ((hi, 0), (lo, N)):
         t = src.reshape(h * w, R // 4, 4, nf).transpose(0, 1, 3, 2)  # (tap, quad, nf, 4)
@@ -624,6 +627,31 @@ def _tc_core(cores):
             b2[:, j // 2, j % 2, :nf, :] = bits[:, j, :, :].transpose(0, 2, 1)  # (h, nf, R)
         out = np.concatenate([out, b2.ravel().view(np.float32)])
         assert out.size == total, (out.size, total)
+    return out
+
+
+def _tc_core_stacked(hi, lo, ks):
+    """Stacked tcgen05 core (dpm_correlate_tc_stack() = ks > 1, <= 8 filters):
+    per tap column, NB = h + 2(ks-1) tap-row blocks (block b = tap row
+    h-1+ks-1-b, zero outside the filter) of 16 N-rows [hi f0..7 | lo f0..7],
+    so the kernel's B window for input-row offset t starts at block
+    h-1+ks-1-t and covers output rows y..y+ks-1 with tap rows t..t-ks+1."""
+    h, w, R, nf = hi.shape
+    nb = h + 2 * (ks - 1)
+    tf = np.zeros((w, R // 4, nb * 16, 4), dtype=np.float32)
+    b2 = np.zeros(((w + 1) // 2, 2, nb * 16, 8), dtype=np.uint16)
+    bits = _bf16_rn(hi)  # (h, w, R, nf)
+    for b in range(nb):
+        i = h - 1 + ks - 1 - b
+        if not 0 <= i < h:
+            continue
+        for j in range(w):
+            for src, base in ((hi, 0), (lo, 8)):
+                t = src[i, j].reshape(R // 4, 4, nf).transpose(0, 2, 1)  # (quad, nf, 4)
+                tf[j, :, b * 16 + base:b * 16 + base + nf, :] = t
+            b2[j // 2, j % 2, b * 16:b * 16 + nf, :] = bits[i, j].T  # (nf, R)
+    out = np.concatenate([tf.ravel(), b2.ravel().view(np.float32)])
+    assert out.size == int(_lib.lib().dpm_correlate_tc_core_floats(h, w, R, nf))
     return out
 
 
