@@ -38,7 +38,20 @@ project_kernel(const float* __restrict__ X, float* __restrict__ P, const float* 
   }
   const float* src = X + job.x_off + cell0 * L;
   const int nflt = ncell * L;
-  if ((L & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+  if (L == 32 && ncell == K1_CELLS && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+    // full tile of HOG cells: all 8 loads per thread in flight before the
+    // shared-memory stores (one memory latency per CTA, not eight)
+    const float4* src4 = reinterpret_cast<const float4*>(src);
+    float4 q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = __ldcs(src4 + t + k * K1_CELLS);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int v = t + k * K1_CELLS;
+      float* d = sX + (v >> 3) * 33 + ((v & 7) << 2);
+      d[0] = q[k].x; d[1] = q[k].y; d[2] = q[k].z; d[3] = q[k].w;
+    }
+  } else if ((L & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
     const float4* src4 = reinterpret_cast<const float4*>(src);
     for (int v = t; v < (nflt >> 2); v += blockDim.x) {
       const float4 q = __ldg(src4 + v);
