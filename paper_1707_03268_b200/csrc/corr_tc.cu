@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         int qready = 0;  // rows of this strip known to be staged
         int y = 0;
         for (; y < ho; y += KS, ++row_glob) {
-          const int b = row_glob % a.nacc;
-          mbar_wait(tempty + b, ((row_glob / a.nacc) & 1) ^ 1);
+          const int b = row_glob & (TC_MAX_ACC - 1);
+          mbar_wait(tempty + b, ((row_glob / TC_MAX_ACC) & 1) ^ 1);
           const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
           const int tmax = min(KS + FH - 1, job.H - y);
           for (int t = 0; t < tmax; ++t) {
@@ -327,71 +327,80 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         q_glob += job.H;
       }
     } else if constexpr (FH > 0) {
-      // Output rows in pairs: the taps of rows y and y+1 go to two TMEM
-      // accumulators alternately, so consecutive MMAs never chain on the same
-      // accumulator (a dependent chain issues at a fraction of the pipe rate
-      // when each MMA is short, N = 32..96).
+      // Compile-time taps.  All bookkeeping stays on the uniform datapath: ring
+      // slots / phases and accumulator indices advance incrementally (no
+      // division), and every B descriptor is the base plus an immediate (the
+      // padded filter count N equals NMAX here).  Descriptors that had to be
+      // moved from vector registers (R2UR) per MMA throttled the issue.
+      constexpr uint32_t LB4 = (2u * NMAX * 16u) >> 4;  // B tap stride (>> 4)
+      constexpr uint32_t B2P = (2u * NMAX * 16u) >> 4;  // bf16 tap-pair block stride (>> 4)
+      const uint32_t ring = (uint32_t)a.ring;
+      uint32_t qs = 0, qph = 0;    // ring slot / phase of the strip's input row 0
+      uint32_t acc = 0, aph = 0;   // accumulator index / phase of the current output row
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
         const dpm_corr_job job = a.jobs[a.strips[st].job];
         const int ho = job.H - FH + 1;
-        for (int y = 0; y < ho; y += 2, row_glob += 2) {
-          const bool two = y + 1 < ho;
-          const int b0 = row_glob % a.nacc, b1 = (row_glob + 1) % a.nacc;
-          mbar_wait(tempty + b0, ((row_glob / a.nacc) & 1) ^ 1);
-          if (two) mbar_wait(tempty + b1, (((row_glob + 1) / a.nacc) & 1) ^ 1);
-          const int rlast = two ? FH : FH - 1;
-          for (int rr = (y == 0 ? 0 : FH - 1); rr <= rlast; ++rr) {
-            const uint32_t q = q_glob + y + rr;
-            mbar_wait(full + q % a.ring, (q / a.ring) & 1);
-          }
-          tc_fence_after();
-          const uint32_t d0 = tmem_base + (uint32_t)(b0 * a.acc_cols);
-          const uint32_t d1 = tmem_base + (uint32_t)(b1 * a.acc_cols);
-          uint64_t da_row[FH + 1], da_lo[FH + 1];
+        for (int y = 0; y < ho; ++y) {
+          uint32_t sl[FH], ph[FH];  // slots / phases of input rows y .. y+FH-1
+          sl[0] = qs;
+          ph[0] = qph;
 #pragma unroll
-          for (int i = 0; i <= FH; ++i) {
-            da_row[i] = dA0 + ((q_glob + y + i) % a.ring) * slot_step;
-            da_lo[i] = dAlo0 + ((q_glob + y + i) % a.ring) * slot_step;
+          for (int i = 1; i < FH; ++i) {
+            sl[i] = sl[i - 1] + 1;
+            ph[i] = ph[i - 1];
+            if (sl[i] == ring) { sl[i] = 0; ph[i] ^= 1; }
           }
+          mbar_wait(tempty + acc, aph ^ 1);
+#pragma unroll
+          for (int i = 0; i < FH; ++i)
+            if (y == 0 || i == FH - 1) mbar_wait(full + sl[i], ph[i]);
+          tc_fence_after();
+          const uint32_t d = tmem_base + acc * (uint32_t)a.acc_cols;
+          // opaque per row: keeps the compiler from hoisting all FH*FW B
+          // descriptors into vector registers (each then needing R2UR per MMA);
+          // base + immediate is formed at the use, on the uniform datapath
+          uint64_t bB = dB0, bB2 = dB2;
+          asm volatile("" : "+l"(bB), "+l"(bB2));
           if (elect_one()) {
 #pragma unroll
-            for (int i = 0; i < FH; ++i)
+            for (int i = 0; i < FH; ++i) {
+              const uint64_t da = dA0 + sl[i] * slot_step;
 #pragma unroll
-              for (int j = 0; j < FW; ++j) {
-                const uint64_t bb = dB0 + (uint32_t)((i * FW + j) * 2) * (uint32_t)(lboB >> 4);
-                mma_tf32(d0, da_row[i] + (uint32_t)j, bb, idesc1, (i | j) != 0);
-                if (two) mma_tf32(d1, da_row[i + 1] + (uint32_t)j, bb, idesc1, (i | j) != 0);
-              }
-#pragma unroll
-            for (int i = 0; i < FH; ++i)
-#pragma unroll
-              for (int jp = 0; jp < (FW + 1) / 2; ++jp) {
-                const uint64_t b2 = dB2 + (uint32_t)((i * ((FW + 1) / 2) + jp) * b2_pair);
-                mma_bf16(d0, da_lo[i] + (uint32_t)(2 * jp), b2, idescbf);
-                if (two) mma_bf16(d1, da_lo[i + 1] + (uint32_t)(2 * jp), b2, idescbf);
-              }
-            tc_commit(tfull + b0);
-            tc_commit(empty + (q_glob + y) % a.ring);
-            if (two) {
-              tc_commit(tfull + b1);
-              tc_commit(empty + (q_glob + y + 1) % a.ring);
+              for (int j = 0; j < FW; ++j)
+                mma_tf32(d, da + (uint32_t)j, bB + (uint32_t)((i * FW + j) * 2) * LB4, idesc1,
+                         (i | j) != 0);
             }
+#pragma unroll
+            for (int i = 0; i < FH; ++i) {
+              const uint64_t dl = dAlo0 + sl[i] * slot_step;
+#pragma unroll
+              for (int jp = 0; jp < (FW + 1) / 2; ++jp)
+                mma_bf16(d, dl + (uint32_t)(2 * jp), bB2 + (uint32_t)((i * ((FW + 1) / 2) + jp)) * B2P,
+                         idescbf);
+            }
+            tc_commit(tfull + acc);
+            tc_commit(empty + sl[0]);  // input row y no longer needed
           }
           __syncwarp();
-          if (!two) row_glob -= 1;  // odd tail: one row
+          qs = sl[1 % FH];
+          qph = ph[1 % FH];
+          if (FH == 1) { if (++qs == ring) { qs = 0; qph ^= 1; } }
+          if (++acc == TC_MAX_ACC) { acc = 0; aph ^= 1; }
         }
-        if (elect_one())
-          for (int rr = ho; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
-        __syncwarp();
-        q_glob += job.H;
+        // rows ho .. H-1 were never first rows: release them
+        for (int rr = ho; rr < job.H; ++rr) {
+          if (elect_one()) tc_commit(empty + qs);
+          __syncwarp();
+          if (++qs == ring) { qs = 0; qph ^= 1; }
+        }
       }
     } else
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
       const int ho = job.H - a.h + 1;
       for (int y = 0; y < ho; ++y, ++row_glob) {
-        const int b = row_glob % a.nacc;
-        mbar_wait(tempty + b, ((row_glob / a.nacc) & 1) ^ 1);
+        const int b = row_glob & (TC_MAX_ACC - 1);
+        mbar_wait(tempty + b, ((row_glob / TC_MAX_ACC) & 1) ^ 1);
         for (int rr = (y == 0 ? 0 : a.h - 1); rr < a.h; ++rr) {
           const uint32_t q = q_glob + y + rr;
           mbar_wait(full + q % a.ring, (q / a.ring) & 1);
@@ -531,8 +540,8 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
 #pragma unroll
         for (int f = 0; f < 8; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
         for (int y = 0; y < ho; y += KS, ++row_glob) {
-          const int b = row_glob % a.nacc;
-          mbar_wait(tfull + b, (row_glob / a.nacc) & 1);
+          const int b = row_glob & (TC_MAX_ACC - 1);
+          mbar_wait(tfull + b, (row_glob / TC_MAX_ACC) & 1);
           tc_fence_after();
           const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.acc_cols);
 #pragma unroll
@@ -587,33 +596,39 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       float vmax[LOC], vmin[LOC];  // this warp's chunks only (chunk c -> local c / SPLIT)
 #pragma unroll
       for (int f = 0; f < LOC; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
+      const int64_t plane = (int64_t)ho * wo;
+      const bool xin = x < wo;
+      // N is a compile-time constant for the fixed DPM shapes (N == NMAX)
+      const int N = FH > 0 ? NMAX : a.N;
       for (int y = 0; y < ho; ++y, ++row_glob) {
-        const int b = row_glob % a.nacc;
-        mbar_wait(tfull + b, (row_glob / a.nacc) & 1);
+        const uint32_t b = row_glob & (TC_MAX_ACC - 1);
+        mbar_wait(tfull + b, (row_glob / TC_MAX_ACC) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.acc_cols);
+        const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * (uint32_t)a.acc_cols;
         float* dst = a.S + job.s_off + (int64_t)y * wo + x;
         // CW filters at a time: hi-half columns [fc, fc+CW) and lo-half [N+fc, ...)
 #pragma unroll
         for (int fc = 0; fc < NMAX; fc += CW) {
-          if (fc < a.N && (fc / CW) % SPLIT == half) {
+          if (fc < N && (fc / CW) % SPLIT == half) {
             float vh[CW], vl[CW];
             if constexpr (CW == 16) {
               tmem_ld16(taddr + fc, vh);
-              tmem_ld16(taddr + a.N + fc, vl);
+              tmem_ld16(taddr + N + fc, vl);
             } else {
               tmem_ld8(taddr + fc, vh);
-              tmem_ld8(taddr + a.N + fc, vl);
+              tmem_ld8(taddr + N + fc, vl);
             }
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            {
 #pragma unroll
-            for (int k = 0; k < CW; ++k) {
-              const int f = fc + k, li = (fc / CW / SPLIT) * CW + k;
-              if (f < job.nf && x < wo) {
-                const float sv = vh[k] + vl[k];
-                dst[(int64_t)f * ho * wo] = sv;
-                vmax[li] = fmaxf(vmax[li], sv);
-                vmin[li] = fminf(vmin[li], sv);
+              for (int k = 0; k < CW; ++k) {
+                const int f = fc + k, li = (fc / CW / SPLIT) * CW + k;
+                if (f < job.nf && xin) {
+                  const float sv = vh[k] + vl[k];
+                  dst[(int64_t)f * plane] = sv;
+                  vmax[li] = fmaxf(vmax[li], sv);
+                  vmin[li] = fminf(vmin[li], sv);
+                }
               }
             }
           }
@@ -763,6 +778,8 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
   }
   else if (h == 6 && w == 11 && R == 8 && N <= 16)  // DPM root filters (3 mirrored pairs)
     fn = corr_tc_kernel<16, 6, 11>;
+  // the kernel indexes accumulators as row & 3 (N <= 64 keeps 4 buffers in TMEM)
+  DPM_REQUIRE(a.nacc == TC_MAX_ACC, "dpm_correlate_tc: %d accumulator buffers", a.nacc);
   DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = nstrips < sms ? nstrips : sms;
   fn<<<grid, threads, smem, as_stream(stream)>>>(a);

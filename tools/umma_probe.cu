@@ -103,6 +103,85 @@ __global__ void __launch_bounds__(128, 1) probe(int n, int iters, long long* out
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(d));
 }
 
+// The K2 part kernel's MMA sequence for one output row, replayed without
+// producers or epilogue: 6 x 6 tf32 MMAs (N = 96 = [B_hi | B_lo] of 48 filters)
+// over 6 ring slots, then 6 x 3 bf16 tap-pair MMAs (N = 48).  Same descriptors,
+// strides and smem footprint as corr_tc_kernel<48, 6, 6, 8>.
+__global__ void __launch_bounds__(128, 1) parts_row(int rows, int fill, long long* out) {
+  constexpr int N = 48, FH = 6, FW = 6, TCOLS = 128 + FW - 1, RING = 8;
+  constexpr uint32_t HI = 2 * TCOLS * 16, SLOT = (HI + (TCOLS + 1) * 16 + 127) & ~127u;
+  constexpr uint32_t BB = FH * FW * 2 * (2 * N) * 16, B2 = FH * 3 * 2 * N * 16;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  unsigned char* sB = sm;
+  unsigned char* sB2 = sm + ((BB + 1023) & ~1023u);
+  unsigned char* sA = sB2 + ((B2 + 1023) & ~1023u);
+  // operand contents: 0 = zeros, 1 = pseudo-random values of HOG / filter magnitude
+  for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ (blockIdx.x * 97u);
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    const float v = fill ? ((float)(h & 0xFFFFFF) / 16777216.0f - 0.5f) * 0.4f : 0.f;
+    reinterpret_cast<float*>(sm)[i] = v;
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(s32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tb = tslot;
+  if (threadIdx.x < 32) {
+    const uint32_t lboA = TCOLS * 16, lboB = 2 * N * 16;
+    const uint64_t dA0 = desc(s32(sA), lboA, 128, 0), dB0 = desc(s32(sB), lboB, 128, 0);
+    const uint64_t dAlo0 = desc(s32(sA) + HI, 16, 128, 0), dB2 = desc(s32(sB2), N * 16, 128, 0);
+    const uint32_t i1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(2 * N >> 3) << 17) | (8u << 24);
+    const uint32_t ib = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+    long long t0 = clock64();
+    for (int y = 0; y < rows; ++y) {
+      const uint32_t d = tb + (uint32_t)((y & 3) * 128);
+      uint64_t da[FH], dl[FH];
+#pragma unroll
+      for (int i = 0; i < FH; ++i) {
+        da[i] = dA0 + ((y + i) % RING) * (SLOT >> 4);
+        dl[i] = dAlo0 + ((y + i) % RING) * (SLOT >> 4);
+      }
+      if (elect_one()) {
+#pragma unroll
+        for (int i = 0; i < FH; ++i)
+#pragma unroll
+          for (int j = 0; j < FW; ++j)
+            mma<false>(d, da[i] + (uint32_t)j, dB0 + (uint32_t)((i * FW + j) * 2) * (lboB >> 4), i1,
+                       (i | j) != 0);
+#pragma unroll
+        for (int i = 0; i < FH; ++i)
+#pragma unroll
+          for (int jp = 0; jp < 3; ++jp)
+            mma<true>(d, dl[i] + (uint32_t)(2 * jp), dB2 + (uint32_t)((i * 3 + jp) * (2 * N * 16 >> 4)), ib, 1u);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       s32(&bar)) : "memory");
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, P;\n\t}" : "=r"(done) : "r"(s32(&bar)) : "memory");
+      out[blockIdx.x] = clock64() - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb));
+}
+
 typedef void (*Probe)(int, int, long long*);
 
 int main() {
@@ -139,6 +218,22 @@ int main() {
         printf("%8.1f", (double)mx / iters);
       }
       printf("\n");
+    }
+  }
+  {
+    const int rows = 4096;
+    for (int fill = 0; fill < 2; ++fill) {
+    cudaFuncSetAttribute(parts_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    parts_row<<<sms, 128, 200 * 1024>>>(rows, fill, out);
+    parts_row<<<sms, 128, 200 * 1024>>>(rows, fill, out);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("parts_row error %s\n", cudaGetErrorString(e)); return 1; }
+    long long h[256];
+    cudaMemcpy(h, out, sms * sizeof(long long), cudaMemcpyDeviceToHost);
+    long long mx = 0;
+    for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("K2 part-kernel MMA sequence, %s operands: %.0f cycles per output row "
+           "(36 tf32 N=96 + 18 bf16 N=48)\n", fill ? "random" : "zero", (double)mx / rows);
     }
   }
   return 0;
