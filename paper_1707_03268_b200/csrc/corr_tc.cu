@@ -315,15 +315,11 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
             }
             __syncwarp();
           }
-          if (elect_one()) {
-            tc_commit(tfull + b);
-            for (int k = 0; k < KS && y + k < job.H; ++k) tc_commit(empty + (q_glob + y + k) % a.ring);
-          }
+          // one commit per group (each commit costs the tensor pipe a bubble);
+          // the epilogue frees the group's dead input rows once it sees tfull
+          if (elect_one()) tc_commit(tfull + b);
           __syncwarp();
         }
-        if (elect_one())  // rows no group released (past the last group's first KS)
-          for (int rr = y; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
-        __syncwarp();
         q_glob += job.H;
       }
     } else if constexpr (FH > 0) {
@@ -378,8 +374,9 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
                 mma_bf16(d, dl + (uint32_t)(2 * jp), bB2 + (uint32_t)((i * ((FW + 1) / 2) + jp)) * B2P,
                          idescbf);
             }
+            // one commit per row (each costs the tensor pipe a bubble): the
+            // epilogue frees input row y's slot once it sees this row's tfull
             tc_commit(tfull + acc);
-            tc_commit(empty + sl[0]);  // input row y no longer needed
           }
           __syncwarp();
           qs = sl[1 % FH];
@@ -387,12 +384,8 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
           if (FH == 1) { if (++qs == ring) { qs = 0; qph ^= 1; } }
           if (++acc == TC_MAX_ACC) { acc = 0; aph ^= 1; }
         }
-        // rows ho .. H-1 were never first rows: release them
-        for (int rr = ho; rr < job.H; ++rr) {
-          if (elect_one()) tc_commit(empty + qs);
-          __syncwarp();
+        for (int rr = ho; rr < job.H; ++rr)  // rows never first of an output row
           if (++qs == ring) { qs = 0; qph ^= 1; }
-        }
       }
     } else
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
@@ -529,6 +522,16 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
   } else {
     // =================== epilogue ===================
     const int quarter = warp & 3;  // TMEM lanes 32*quarter ..
+    // input-row slots are freed here, after the MMAs that last read them
+    // completed (tfull), by one thread of the first epilogue warp
+    const bool releaser = warp == 1 + TC_PRODUCERS && lane == 0;
+    uint32_t eslot = 0;  // ring slot of the current strip's next unreleased row
+    auto release = [&](int nrows) {
+      for (int k = 0; k < nrows; ++k) {
+        if (releaser) mbar_arrive(empty + eslot);
+        if (++eslot == (uint32_t)a.ring) eslot = 0;
+      }
+    };
     if constexpr (KS > 1) {
       uint32_t row_glob = 0;
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
@@ -539,10 +542,12 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         float vmax[8], vmin[8];
 #pragma unroll
         for (int f = 0; f < 8; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
-        for (int y = 0; y < ho; y += KS, ++row_glob) {
+        int y = 0;
+        for (; y < ho; y += KS, ++row_glob) {
           const int b = row_glob & (TC_MAX_ACC - 1);
           mbar_wait(tfull + b, (row_glob / TC_MAX_ACC) & 1);
           tc_fence_after();
+          release(min(KS, job.H - y));  // rows y .. y+KS-1: no later group reads them
           const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * a.acc_cols);
 #pragma unroll
           for (int k = 0; k < KS; ++k) {
@@ -565,6 +570,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty + b);
         }
+        if (y < job.H) release(job.H - y);  // rows past the last group's first KS
         if (a.ranges != nullptr && job.range_idx >= 0) {
 #pragma unroll
           for (int f = 0; f < 8; ++f) {
@@ -604,6 +610,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         const uint32_t b = row_glob & (TC_MAX_ACC - 1);
         mbar_wait(tfull + b, (row_glob / TC_MAX_ACC) & 1);
         tc_fence_after();
+        if constexpr (FH > 0) release(1);  // input row y: no later output row reads it
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * (uint32_t)a.acc_cols;
         float* dst = a.S + job.s_off + (int64_t)y * wo + x;
         // CW filters at a time: hi-half columns [fc, fc+CW) and lo-half [N+fc, ...)
@@ -637,6 +644,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + b);
       }
+      if constexpr (FH > 0) release(job.H - ho);  // rows never first of an output row
       if (a.ranges != nullptr && job.range_idx >= 0) {
 #pragma unroll
         for (int li = 0; li < LOC; ++li) {

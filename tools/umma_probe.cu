@@ -107,12 +107,14 @@ __global__ void __launch_bounds__(128, 1) probe(int n, int iters, long long* out
 // producers or epilogue: 6 x 6 tf32 MMAs (N = 96 = [B_hi | B_lo] of 48 filters)
 // over 6 ring slots, then 6 x 3 bf16 tap-pair MMAs (N = 48).  Same descriptors,
 // strides and smem footprint as corr_tc_kernel<48, 6, 6, 8>.
-__global__ void __launch_bounds__(128, 1) parts_row(int rows, int fill, long long* out) {
+// extra: 0 none, 1 per-row fence::after_thread_sync, 2 per-row commits (2),
+// 3 per-row wait on an already-completed mbarrier + fence, 4 all of them
+__global__ void __launch_bounds__(128, 1) parts_row(int rows, int fill, int extra, long long* out) {
   constexpr int N = 48, FH = 6, FW = 6, TCOLS = 128 + FW - 1, RING = 8;
   constexpr uint32_t HI = 2 * TCOLS * 16, SLOT = (HI + (TCOLS + 1) * 16 + 127) & ~127u;
   constexpr uint32_t BB = FH * FW * 2 * (2 * N) * 16, B2 = FH * 3 * 2 * N * 16;
   extern __shared__ __align__(1024) unsigned char sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2[4];
   __shared__ uint32_t tslot;
   unsigned char* sB = sm;
   unsigned char* sB2 = sm + ((BB + 1023) & ~1023u);
@@ -130,12 +132,14 @@ __global__ void __launch_bounds__(128, 1) parts_row(int rows, int fill, long lon
   }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar)));
+    for (int k = 0; k < 4; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar2[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tslot;
+  uint32_t dummy_phase = 0;
   if (threadIdx.x < 32) {
     const uint32_t lboA = TCOLS * 16, lboB = 2 * N * 16;
     const uint64_t dA0 = desc(s32(sA), lboA, 128, 0), dB0 = desc(s32(sB), lboB, 128, 0);
@@ -145,6 +149,15 @@ __global__ void __launch_bounds__(128, 1) parts_row(int rows, int fill, long lon
     long long t0 = clock64();
     for (int y = 0; y < rows; ++y) {
       const uint32_t d = tb + (uint32_t)((y & 3) * 128);
+      if (extra == 3 || extra == 4) {  // wait for the commit of 4 rows ago (completes long before)
+        if (y >= 4) {
+          uint32_t done = 0;
+          while (!done)
+            asm volatile("{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+                         "selp.u32 %0, 1, 0, P;\n\t}" : "=r"(done) : "r"(s32(&bar2[y & 3])), "r"(((y >> 2) - 1) & 1) : "memory");
+        }
+      }
+      if (extra == 1 || extra >= 3) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint64_t da[FH], dl[FH];
 #pragma unroll
       for (int i = 0; i < FH; ++i) {
@@ -163,6 +176,13 @@ __global__ void __launch_bounds__(128, 1) parts_row(int rows, int fill, long lon
 #pragma unroll
           for (int jp = 0; jp < 3; ++jp)
             mma<true>(d, dl[i] + (uint32_t)(2 * jp), dB2 + (uint32_t)((i * 3 + jp) * (2 * N * 16 >> 4)), ib, 1u);
+        if (extra == 2 || extra >= 3) {
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           s32(&bar2[y & 3])) : "memory");
+          if (extra == 2 || extra == 4)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             s32(&bar)) : "memory");
+        }
       }
       __syncwarp();
     }
@@ -222,18 +242,21 @@ int main() {
   }
   {
     const int rows = 4096;
-    for (int fill = 0; fill < 2; ++fill) {
+    for (int extra = 0; extra < 5; ++extra) {
+    const int fill = 1;
     cudaFuncSetAttribute(parts_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    parts_row<<<sms, 128, 200 * 1024>>>(rows, fill, out);
-    parts_row<<<sms, 128, 200 * 1024>>>(rows, fill, out);
+    parts_row<<<sms, 128, 200 * 1024>>>(rows, fill, extra, out);
+    parts_row<<<sms, 128, 200 * 1024>>>(rows, fill, extra, out);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("parts_row error %s\n", cudaGetErrorString(e)); return 1; }
     long long h[256];
     cudaMemcpy(h, out, sms * sizeof(long long), cudaMemcpyDeviceToHost);
     long long mx = 0;
     for (int i = 0; i < sms; ++i) mx = h[i] > mx ? h[i] : mx;
-    printf("K2 part-kernel MMA sequence, %s operands: %.0f cycles per output row "
-           "(36 tf32 N=96 + 18 bf16 N=48)\n", fill ? "random" : "zero", (double)mx / rows);
+    const char* ex[] = {"none", "fence::after_thread_sync", "2 commits", "wait(done)+fence+commit",
+                        "wait+fence+2 commits"};
+    printf("K2 part-kernel MMA sequence, per-row extra = %-26s: %.0f cycles per output row\n",
+           ex[extra], (double)mx / rows);
     }
   }
   return 0;
