@@ -264,7 +264,7 @@ class Plan:
 
         self._tc_classes = []
         for fl, strips in sorted(tc_classes.items()):
-            strips.sort(key=lambda t: -t[3])  # tall strips first (static round robin)
+            strips = _snake_order(strips, key=lambda t: t[3], ctas=_sm_count())
             fd = self.filters[fl[0]]
             arr = np.array([(j, 0, sx, 0) for j, _, sx, _ in strips], dtype=_lib.CORR_TILE)
             self._tc_classes.append((fd.h, fd.w, fd.R, len(fl), self.tc_core_off[fl], arr))
@@ -591,6 +591,35 @@ class Plan:
 
     def k1_bytes(self):
         return sum(4 * (self.L + self.Rtot) * H * W for H, W in self.levels)
+
+
+def _sm_count():
+    """SMs of the current CUDA device (the persistent tcgen05 grid), 148 on
+    B200; the B200 value when no device is visible (host-only planning)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    except Exception:  # planning without a usable device
+        pass
+    return 148
+
+
+def _snake_order(items, key, ctas=148):
+    """Order work items for a persistent kernel whose CTA b takes items b,
+    b + G, b + 2G, ... (G = grid size): tallest first, dealt in boustrophedon
+    rounds (CTA 0..G-1, then G-1..0, ...), so every CTA gets a near-equal
+    total instead of CTA 0 taking the largest item of every round.  G is the
+    SM count (the grid of the tcgen05 kernel); with fewer items than SMs the
+    order is irrelevant."""
+    srt = sorted(items, key=lambda t: -key(t))
+    out = list(srt)
+    for r in range(0, len(srt), ctas):
+        rnd = srt[r:r + ctas]
+        if (r // ctas) % 2 == 1 and len(rnd) == ctas:
+            rnd = rnd[::-1]
+        out[r:r + len(rnd)] = rnd
+    return out
 
 
 def _bf16_rn(x):
