@@ -243,7 +243,13 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   const int ntx = (wr + PT_W - 1) / PT_W;
   const int tile = blockIdx.x - aj.block0;
   const int ty0 = (tile / ntx) * PT_H, tx0 = (tile % ntx) * PT_W;  // offsets inside the rect
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // thread index read once through a volatile asm: the compiler may not
+  // re-derive it (S2R + shifts) at every use, which it did under the
+  // 64-register cap (7% of the kernel's instructions, with S2R latency)
+  int tid_;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_));
+  const int tid = tid_;
+  const int lane = tid & 31, warp = tid >> 5;
   constexpr int RPT = PT_H / PT_WARPS;  // roots per thread (4)
   // Narrow tiles pack: lpr = lanes per band row / per root row (power of two
   // >= the tile's valid columns), so a warp screens 32 / lpr rows at once and
@@ -252,7 +258,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   const int lpr_log = wt > 16 ? 5 : wt > 8 ? 4 : wt > 4 ? 3 : wt > 2 ? 2 : wt > 1 ? 1 : 0;
   const int lpr = 1 << lpr_log;
   auto root_of = [&](int k, int& iyr, int& ixr) -> bool {  // k-th root of this thread
-    const int e = threadIdx.x + PT_THREADS * k;
+    const int e = tid + PT_THREADS * k;
     iyr = e >> lpr_log;
     ixr = e & (lpr - 1);
     return iyr < h_tile && ixr < wt;
@@ -320,8 +326,8 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
-    if (threadIdx.x >= PT_THREADS - 2 * (2 * RCAP + 1)) {  // last warps: penalty tables
-      const int t = threadIdx.x - (PT_THREADS - 2 * (2 * RCAP + 1));
+    if (tid >= PT_THREADS - 2 * (2 * RCAP + 1)) {  // last warps: penalty tables
+      const int t = tid - (PT_THREADS - 2 * (2 * RCAP + 1));
       const int d = (t % (2 * RCAP + 1)) - RCAP;
       if (t < 2 * RCAP + 1) {
         const float v = (float)(-pen(pj.cdx, pj.cdxx, d));
@@ -402,7 +408,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     // band rows outside the map have no candidate (reference: (-inf, -r))
     const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
     const int n_out = r_lo + (nrows - r_hi);
-    for (int i = threadIdx.x; i < n_out * PT_W; i += PT_THREADS) {
+    for (int i = tid; i < n_out * PT_W; i += PT_THREADS) {
       const int k = i / PT_W, l = i - k * PT_W;
       const int r = k < r_lo ? k : r_hi + (k - r_lo);
       sh.x32[r * PT_W + l] = OUT_SENTINEL;
