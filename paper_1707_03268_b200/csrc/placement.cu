@@ -246,10 +246,11 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   // thread index read once through a volatile asm: the compiler may not
   // re-derive it (S2R + shifts) at every use, which it did under the
   // 64-register cap (7% of the kernel's instructions, with S2R latency)
-  int tid_;
+  int tid_, lane_, warp_;
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_));
-  const int tid = tid_;
-  const int lane = tid & 31, warp = tid >> 5;
+  asm volatile("and.b32 %0, %1, 31;" : "=r"(lane_) : "r"(tid_));
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp_) : "r"(tid_));
+  const int tid = tid_, lane = lane_, warp = warp_;
   constexpr int RPT = PT_H / PT_WARPS;  // roots per thread (4)
   // Narrow tiles pack: lpr = lanes per band row / per root row (power of two
   // >= the tile's valid columns), so a warp screens 32 / lpr rows at once and
