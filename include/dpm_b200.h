@@ -24,7 +24,11 @@
  *    check_feature_map order, validation.py:65-86).
  *  - Projected level P: float32 planar [R][H][pitch], pitch >= W, pitch % 4 == 0.
  *  - Core G of a filter group: float32 [h][w][R][nf_pad] (filter fastest).
- *  - Response maps S: float32 [nf][H-h+1][W-w+1].
+ *  - Response maps S: float32 [nf][Ho][pitch] with Ho = H-h+1, Wo = W-w+1 and
+ *    pitch = (Wo + 3) & ~3 (rows padded to 16 bytes; the padding is never
+ *    read as data).  Map offsets (s_off) are multiples of 4 floats.  Every
+ *    kernel that reads or writes S uses this pitch; descriptor fields named
+ *    Wp / Wo hold the valid width.  (ABI version 2.)
  */
 #ifndef DPM_B200_H
 #define DPM_B200_H
@@ -36,7 +40,7 @@
 extern "C" {
 #endif
 
-#define DPM_ABI_VERSION 1
+#define DPM_ABI_VERSION 2
 #define DPM_MAX_PARTS 16
 
 typedef enum {
@@ -82,7 +86,7 @@ int dpm_project(const float* X, float* P, const float* C, int L, int R,
  * correlate3_full (correlation.py:92-112; C = identity, G = the filter). */
 typedef struct {
   int64_t p_off;     /* float offset of the (image, level) P block           */
-  int64_t s_off;     /* float offset of the output maps [nf][Ho][Wo]         */
+  int64_t s_off;     /* float offset of the output maps [nf][Ho][pitch(Wo)]  */
   int64_t g_off;     /* float offset of the group's core [h][w][R][nf_pad]   */
   int32_t H, W, pitch, chan_off;
   int32_t h, w, R, nf;
@@ -157,7 +161,7 @@ int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
  * c_dxx, c_dyy > 0).  Every placed map needs a range slot (filled by
  * dpm_correlate): it bounds the FP32 screening error and gives r*. */
 typedef struct {
-  int64_t s_off;     /* float offset of the part response map [Hp][Wp]       */
+  int64_t s_off;     /* float offset of the part response map [Hp][pitch(Wp)] */
   int64_t x_off;     /* GDT path: offset of the x-pass scratch (sv/dx)      */
   int32_t Hp, Wp;
   int32_t ay, ax;

@@ -111,7 +111,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.dpm_abi_version() != 1:
+        if handle.dpm_abi_version() != 2:
             raise DeviceError("libdpm_b200.so ABI version mismatch")
         _lib = handle
     return _lib

@@ -43,6 +43,11 @@ const char* last_error();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Row pitch (floats) of a response map S of width w: rows are padded to 16
+// bytes, so band / row copies can move whole 16-byte chunks and a map can be
+// described to the TMA unit (strides must be multiples of 16 B).
+__host__ __device__ constexpr int s_pitch(int w) { return (w + 3) & ~3; }
+
 // Order-preserving float <-> uint32 key (max over keys == max over floats).
 __device__ __forceinline__ uint32_t float_key(float f) {
   uint32_t u = __float_as_uint(f);

@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
         const dpm_corr_tile strip = a.strips[st];
         const dpm_corr_job job = a.jobs[strip.job];
-        const int ho = job.H - FH + 1, wo = job.W - FW + 1;
+        const int ho = job.H - FH + 1, wo = job.W - FW + 1, wp = s_pitch(wo);
         const int x = strip.tx * TC_M + quarter * 32 + lane;
         float vmax[8], vmin[8];
 #pragma unroll
@@ -555,12 +555,12 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
             float v[16];  // hi 0..7 | lo 8..15 of row y+k
             tmem_ld16(taddr + 16 * k, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float* dst = a.S + job.s_off + (int64_t)(y + k) * wo + x;
+            float* dst = a.S + job.s_off + (int64_t)(y + k) * wp + x;
 #pragma unroll
             for (int f = 0; f < 8; ++f) {
               if (f < job.nf && x < wo) {
                 const float sv = v[f] + v[8 + f];
-                dst[(int64_t)f * ho * wo] = sv;
+                dst[(int64_t)f * ho * wp] = sv;
                 vmax[f] = fmaxf(vmax[f], sv);
                 vmin[f] = fminf(vmin[f], sv);
               }
@@ -602,7 +602,8 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       float vmax[LOC], vmin[LOC];  // this warp's chunks only (chunk c -> local c / SPLIT)
 #pragma unroll
       for (int f = 0; f < LOC; ++f) { vmax[f] = -INFINITY; vmin[f] = INFINITY; }
-      const int64_t plane = (int64_t)ho * wo;
+      const int wp = s_pitch(wo);
+      const int64_t plane = (int64_t)ho * wp;
       const bool xin = x < wo;
       // N is a compile-time constant for the fixed DPM shapes (N == NMAX)
       const int N = FH > 0 ? NMAX : a.N;
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         tc_fence_after();
         if constexpr (FH > 0) release(1);  // input row y: no later output row reads it
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * (uint32_t)a.acc_cols;
-        float* dst = a.S + job.s_off + (int64_t)y * wo + x;
+        float* dst = a.S + job.s_off + (int64_t)y * wp + x;
         // CW filters at a time: hi-half columns [fc, fc+CW) and lo-half [N+fc, ...)
 #pragma unroll
         for (int fc = 0; fc < NMAX; fc += CW) {

@@ -180,12 +180,13 @@ __device__ __forceinline__ void tile_epilogue(unsigned long long (&acc)[K2_MP][N
     const int fg = wf * NF + f;
     float vmax = -INFINITY, vmin = INFINITY;
     if (fg < job.nf) {
-      float* dst = a.S + job.s_off + (int64_t)fg * ho * wo;
+      const int wp = s_pitch(wo);
+      float* dst = a.S + job.s_off + (int64_t)fg * ho * wp;
 #pragma unroll
       for (int p = 0; p < MP; ++p) {
         const int y = yb + p;
         if (x < wo && y < ho) {
-          dst[(int64_t)y * wo + x] = out[p][f];
+          dst[(int64_t)y * wp + x] = out[p][f];
           vmax = fmaxf(vmax, out[p][f]);
           vmin = fminf(vmin, out[p][f]);
         }
@@ -360,7 +361,7 @@ corr_generic_kernel(const CorrArgs a) {
             acc = fmaf(__ldg(pb + r * plane + (int64_t)i * job.pitch + j),
                        __ldg(a.G + job.g_off + (((int64_t)i * job.w + j) * job.R + r) * job.nf_pad + f),
                        acc);
-      a.S[job.s_off + ((int64_t)f * ho + y) * wo + x] = acc;
+      a.S[job.s_off + ((int64_t)f * ho + y) * s_pitch(wo) + x] = acc;
       if (a.ranges != nullptr && job.range_idx >= 0) {
         atomicMax(a.ranges + 2 * (job.range_idx + f), float_key(acc));
         atomicMin(a.ranges + 2 * (job.range_idx + f) + 1, float_key(acc));

@@ -173,7 +173,7 @@ gdt_x_kernel(const float* __restrict__ S, float* __restrict__ SV, int16_t* __res
   const dpm_place_job pj = jobs[jid];
   const int y0 = (int)(wb - pj.block0) * 32;
   if (y0 >= pj.Hp) return;
-  const int Hp = pj.Hp, Wp = pj.Wp, wr = pj.wr, sc = pj.scale;
+  const int Hp = pj.Hp, Wp = pj.Wp, wr = pj.wr, sc = pj.scale, sp = s_pitch(pj.Wp);
   const float vmax = key_float(ranges[2 * pj.range_idx]);
   const float vmin = key_float(ranges[2 * pj.range_idx + 1]);
   const int rs = gdt_rstar(pj.cdxx, pj.cdx, pj.cdyy, pj.cdy, vmax, vmin);
@@ -203,10 +203,10 @@ gdt_x_kernel(const float* __restrict__ S, float* __restrict__ SV, int16_t* __res
       double best = -INFINITY;
       int bq = 0;
       for (int q = 0; q < Wp; ++q) {
-        const double v = __dadd_rn((double)__ldg(sm + (int64_t)y * Wp + q), -gpen(b, a, q - p));
+        const double v = __dadd_rn((double)__ldg(sm + (int64_t)y * sp + q), -gpen(b, a, q - p));
         if (v > best) { best = v; bq = q; }
       }
-      sh.osv[cq & 31][lane] = __ldg(sm + (int64_t)y * Wp + bq);
+      sh.osv[cq & 31][lane] = __ldg(sm + (int64_t)y * sp + bq);
       sh.odx[cq & 31][lane] = (int16_t)(bq - p);
       if ((cq & 31) == 31 || cq == wr - 1) flush(cq);
     }
@@ -229,7 +229,7 @@ gdt_x_kernel(const float* __restrict__ S, float* __restrict__ SV, int16_t* __res
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     const int yy = y0 + r, xx = lane;
-    nxt[r] = (yy < Hp && xx < Wp) ? __ldg(sm + (int64_t)yy * Wp + xx) : 0.f;
+    nxt[r] = (yy < Hp && xx < Wp) ? __ldg(sm + (int64_t)yy * sp + xx) : 0.f;
   }
   for (int kb = 0; kb < nblk; ++kb) {
     const int xb = kb * 32;
@@ -241,7 +241,7 @@ gdt_x_kernel(const float* __restrict__ S, float* __restrict__ SV, int16_t* __res
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int yy = y0 + r, xx = xb + 32 + lane;
-        nxt[r] = (yy < Hp && xx < Wp) ? __ldg(sm + (int64_t)yy * Wp + xx) : 0.f;
+        nxt[r] = (yy < Hp && xx < Wp) ? __ldg(sm + (int64_t)yy * sp + xx) : 0.f;
       }
     }
     const int ncol = min(32, Wp - xb);

@@ -208,7 +208,7 @@ __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job
     int xd = -rx_;
     const int lo = max(-rx_, -cx), hi = min(rx_, pj.Wp - 1 - cx);
     for (int dx = lo; dx <= hi; ++dx) {
-      const double c = __dadd_rn((double)__ldg(sm + (int64_t)y * pj.Wp + cx + dx),
+      const double c = __dadd_rn((double)__ldg(sm + (int64_t)y * s_pitch(pj.Wp) + cx + dx),
                                  -pen(pj.cdx, pj.cdxx, dx));
       if (c > xb) { xb = c; xd = dx; }
     }
@@ -295,11 +295,11 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     // only band rows inside the map are staged (the x pass never reads the others)
     const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
     const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(sh.s);
-    const int Wp = pj.Wp;
-    const float* sbase = sm + (int64_t)yb0 * Wp + xb0;
+    const int Wp = pj.Wp, sp = s_pitch(pj.Wp);
+    const float* sbase = sm + (int64_t)yb0 * sp + xb0;
     if (xb0 >= 0 && xb0 + ncols <= Wp) {  // every band column inside the map (uniform)
       for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
-        const float* srow = sbase + (int64_t)r * Wp;
+        const float* srow = sbase + (int64_t)r * sp;
         const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -311,7 +311,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       }
     } else {
       for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
-        const float* srow = sbase + (int64_t)r * Wp;
+        const float* srow = sbase + (int64_t)r * sp;
         const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {

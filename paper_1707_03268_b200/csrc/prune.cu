@@ -32,7 +32,7 @@ prune_ranks_kernel(const float* __restrict__ S, const int64_t* __restrict__ map_
   int fail = 0;
   if (j.radius < 0) {  // root: the prefix value at the root itself
     for (int r = 0; r < j.R && !fail; ++r) {
-      const float v = __ldg(S + map_offs[j.offs0 + r] + (int64_t)ry * j.Wp + rx);
+      const float v = __ldg(S + map_offs[j.offs0 + r] + (int64_t)ry * s_pitch(j.Wp) + rx);
       if ((double)v < thr[j.thr0 + r]) fail = r + 1;
     }
   } else {
@@ -43,7 +43,7 @@ prune_ranks_kernel(const float* __restrict__ S, const int64_t* __restrict__ map_
       const float* m = S + map_offs[j.offs0 + r];
       float wmax = -INFINITY;
       for (int y = y0; y <= y1; ++y)
-        for (int x = x0; x <= x1; ++x) wmax = fmaxf(wmax, __ldg(m + (int64_t)y * j.Wp + x));
+        for (int x = x0; x <= x1; ++x) wmax = fmaxf(wmax, __ldg(m + (int64_t)y * s_pitch(j.Wp) + x));
       if ((double)wmax < thr[j.thr0 + r]) fail = r + 1;
     }
   }

@@ -225,13 +225,14 @@ class Plan:
                 H, W = self.levels[k]
                 fd = self.filters[fl[0]]
                 ho, wo = H - fd.h + 1, W - fd.w + 1
-                s_off = sa.take(len(fl) * ho * wo, align=4)
+                wp = _spitch(wo)  # rows padded to 16 B (include/dpm_b200.h, "S maps")
+                s_off = sa.take(len(fl) * ho * wp, align=4)
                 rng = -1
                 if any((k, f) in placed_maps for f in fl):
                     rng = nslots
                     nslots += len(fl)
                 for i, f in enumerate(fl):
-                    self.map_off[(img, k, f)] = s_off + i * ho * wo
+                    self.map_off[(img, k, f)] = s_off + i * ho * wp
                     self.map_shape[(k, f)] = (ho, wo)
                     if rng >= 0:
                         self.range_slot[(img, k, f)] = rng + i
@@ -299,7 +300,7 @@ class Plan:
                 root_off, root_pitch = -1, 0
                 if a.root is not None:
                     root_off = self.map_off[(img, a.root[0], a.root[1])]
-                    root_pitch = self.map_shape[tuple(a.root)][1]
+                    root_pitch = _spitch(self.map_shape[tuple(a.root)][1])
                     rh, rw = self.map_shape[tuple(a.root)]
                     if not (0 <= ry0 and ry1 < rh and 0 <= rx0 and rx1 < rw):
                         raise ValidationError(f"assembly {ai}: rect {a.rect} outside the root "
@@ -522,7 +523,8 @@ class Plan:
     def map(self, image, level, filt):
         ho, wo = self.map_shape[(level, filt)]
         off = self.map_off[(image, level, filt)]
-        return self.S[off:off + ho * wo].view(ho, wo)
+        wp = _spitch(wo)
+        return self.S[off:off + ho * wp].view(ho, wp)[:, :wo]
 
     def assembly_outputs(self, image, a):
         t_off, p_off, pl_off, hr, wr = self.asm_index[(image, a)]
@@ -603,6 +605,11 @@ def _sm_count():
     except Exception:  # planning without a usable device
         pass
     return 148
+
+
+def _spitch(w):
+    """Row pitch (floats) of a response map of width w (s_pitch in csrc)."""
+    return (w + 3) & ~3
 
 
 def _snake_order(items, key, ctas=148):
