@@ -170,6 +170,8 @@ typedef struct {
   int32_t rx0, wr;   /* root columns (centres scale*rx + ax) = the assembly's */
   int32_t range_idx; /* range slot of the map                                */
   int32_t block0;    /* reserved                                             */
+  int32_t smap;      /* dpm_assemble: TMA tensor map (dpm_smap_encode) of the */
+  int32_t smap_z;    /*   map's group, and the map's index in that group     */
   double cdx, cdy, cdxx, cdyy;
 } dpm_place_job;
 
@@ -218,10 +220,30 @@ typedef struct {
 int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uint32_t* ranges,
                      dpm_place_range* prep, void* stream);
 
+/* TMA descriptors of S map groups.  One descriptor per group [nf][Ho][pitch]
+ * (a 3-D tensor of floats, x = column < Wo, y = row < Ho, z = map < nf) at
+ * S + s_off; dpm_assemble copies each part's band of the map into shared
+ * memory with it (boxes of DPM_SMAP_BOX_W x DPM_SMAP_BOX_H, cells outside the
+ * map read as NaN).  Host function (no GPU work): writes n descriptors of
+ * DPM_SMAP_BYTES (64-byte aligned) to maps_host, which the caller copies to
+ * device memory.  The descriptors embed the address of S. */
+#define DPM_SMAP_BYTES 128
+#define DPM_SMAP_BOX_W 100
+#define DPM_SMAP_BOX_H 32
+typedef struct {
+  int64_t s_off;     /* float offset of the group (multiple of 4)            */
+  int32_t Ho, Wo, nf;
+  int32_t pad;
+} dpm_smap_desc;
+int dpm_smap_encode(const float* S, const dpm_smap_desc* descs_host, int n, void* maps_host);
+
 /* Placement of every part (x pass + y pass) fused with the assembly; one
  * CTA per 32 x 64 tile of roots.  `prep` is dpm_place_ranges' output for the
- * same placement table.  Detections require the positions output. */
-int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
+ * same placement table; `smaps` the device copy of dpm_smap_encode's
+ * descriptors for S (each placement job names its map by smap / smap_z).
+ * Detections require the positions output. */
+int dpm_assemble(const float* S, const void* smaps, const dpm_place_job* pjobs,
+                 const dpm_asm_job* ajobs,
                  int najobs, int64_t nblocks, const dpm_place_range* prep, double* total,
                  uint32_t* pos, double* placed, double tau, dpm_detection* dets, int max_dets,
                  int* det_count, void* stream);

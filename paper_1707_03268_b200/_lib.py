@@ -12,7 +12,7 @@ import numpy as np
 
 from .errors import DeviceError, NumericError, ValidationError
 
-__all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "ASM_JOB",
+__all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "ASM_JOB", "SMAP_DESC",
            "DETECTION", "PLACE_RANGE", "PRUNE_JOB", "MIX_JOB", "LIB_PATH", "MAX_PARTS", "table_ptr"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdpm_b200.so")
@@ -32,6 +32,7 @@ CORR_TILE = np.dtype([("job", "<i4"), ("ty", "<i4"), ("tx", "<i4"), ("pad", "<i4
 PLACE_JOB = np.dtype([("s_off", "<i8"), ("x_off", "<i8"), ("Hp", "<i4"), ("Wp", "<i4"),
                       ("ay", "<i4"), ("ax", "<i4"), ("scale", "<i4"), ("radius", "<i4"),
                       ("rx0", "<i4"), ("wr", "<i4"), ("range_idx", "<i4"), ("block0", "<i4"),
+                      ("smap", "<i4"), ("smap_z", "<i4"),
                       ("cdx", "<f8"), ("cdy", "<f8"), ("cdxx", "<f8"), ("cdyy", "<f8")],
                      align=True)
 ASM_JOB = np.dtype([("root_off", "<i8"), ("total_off", "<i8"), ("pos_off", "<i8"),
@@ -54,7 +55,12 @@ MIX_JOB = np.dtype([("out_off", "<i8"), ("ry0", "<i4"), ("ry1", "<i4"), ("rx0", 
                     ("rx1", "<i4"), ("member0", "<i4"), ("nmembers", "<i4"), ("block0", "<i4"),
                     ("pad", "<i4")], align=True)
 
-_SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 88, "ASM_JOB": 88,
+SMAP_DESC = np.dtype([("s_off", "<i8"), ("Ho", "<i4"), ("Wo", "<i4"), ("nf", "<i4"),
+                      ("pad", "<i4")], align=True)
+SMAP_BYTES = 128
+
+_SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 96, "ASM_JOB": 88,
+          "SMAP_DESC": 24,
           "DETECTION": 96, "PLACE_RANGE": 16, "PRUNE_JOB": 64,
           "MIX_JOB": 40}
 for _n, _s in _SIZES.items():
@@ -81,8 +87,9 @@ _SIGNATURES = {
     "dpm_place_prepare": (_i64, [_vp, _i32]),
     "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
     "dpm_place_ranges": (_i32, [_vp, _i32, _vp, _vp, _vp]),
-    "dpm_assemble": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32, _vp,
-                            _vp]),
+    "dpm_assemble": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32,
+                            _vp, _vp]),
+    "dpm_smap_encode": (_i32, [_vp, _vp, _i32, _vp]),
     "dpm_gdt_x_prepare": (_i64, [_vp, _i32]),
     "dpm_gdt_x": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
     "dpm_gdt_y_prepare": (_i64, [_vp, _i32, _vp, _i32]),

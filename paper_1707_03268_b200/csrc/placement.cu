@@ -40,6 +40,9 @@
 // with the same arithmetic.
 #include <math.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace dpm {
@@ -49,9 +52,14 @@ constexpr int PT_W = 32;                                  // root columns per ti
 constexpr int PT_H = 64;                                  // root rows per tile
 constexpr int PT_THREADS = 512;
 constexpr int PT_WARPS = PT_THREADS / 32;
-constexpr int BAND_MAX = 2 * (PT_H - 1) + 1 + 2 * RCAP;   // 159 (scale <= 2)
+constexpr int BAND_ROWS = 2 * (PT_H - 1) + 1 + 2 * RCAP;  // 159 band rows (scale <= 2)
+constexpr int TMA_BH = DPM_SMAP_BOX_H;                      // band rows per TMA box
+constexpr int BAND_MAX = (BAND_ROWS + TMA_BH - 1) / TMA_BH * TMA_BH;  // 160: whole boxes
 // even, so band rows start 8-byte aligned (packed pairs in the x pass)
-constexpr int COLS_PITCH = 2 * (PT_W - 1) + 1 + 2 * RCAP + 3;  // 98
+// band row pitch in shared memory = the TMA box width (the box lands dense)
+constexpr int COLS_PITCH = DPM_SMAP_BOX_W;  // 100 >= 2 * (PT_W - 1) + 1 + 2 * RCAP = 95
+static_assert(COLS_PITCH >= 2 * (PT_W - 1) + 1 + 2 * RCAP && COLS_PITCH % 4 == 0, "band width");
+constexpr uint32_t TMA_BOX_BYTES = DPM_SMAP_BOX_W * DPM_SMAP_BOX_H * 4;
 
 __device__ __forceinline__ double pen(double c1, double c2, int d) {
   const double dd = (double)d;
@@ -115,6 +123,16 @@ __device__ __forceinline__ float enc_idx(float v, uint32_t mask) {
   return __uint_as_float(r);
 }
 
+// min that propagates NaN (FMNMX.NAN): cells outside the map arrive as NaN
+// (TMA out-of-bounds fill); in the top-2 merge below a NaN candidate must
+// drop out of both m1 and m2 -- with the NaN-ignoring fminf it would make m2
+// equal to the winner and force a needless exact rescan.
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 // Window of 2R+1 candidates src[d*STRIDE] + np[d], d = -R..R (pointers at
 // d = 0); m1 = top encoded value (code d + R in its low bits), m2 = best of
 // the others.
@@ -125,8 +143,8 @@ __device__ __forceinline__ void screen_pairs(const float* __restrict__ src,
   if constexpr (D < R) {
     const float a = enc_idx<D + R>(src[D * STRIDE] + np[D], mask);
     const float b = enc_idx<D + 1 + R>(src[(D + 1) * STRIDE] + np[D + 1], mask);
-    const float hi = fmaxf(a, b), lo = fminf(a, b);
-    m2 = fmaxf(m2, fmaxf(lo, fminf(m1, hi)));
+    const float hi = fmaxf(a, b), lo = fmin_nan(a, b);
+    m2 = fmaxf(m2, fmaxf(lo, fmin_nan(m1, hi)));
     m1 = fmaxf(m1, hi);
     screen_pairs<R, STRIDE, D + 2>(src, np, mask, m1, m2);
   }
@@ -148,31 +166,41 @@ __device__ __forceinline__ void screen_pairs_packed(const float* __restrict__ sr
     asm("mov.b64 {%0, %1}, %2;" : "=f"(va), "=f"(vb) : "l"(v2));
     const float a = enc_idx<D + R>(va, mask);
     const float b = enc_idx<D + 1 + R>(vb, mask);
-    const float hi = fmaxf(a, b), lo = fminf(a, b);
-    m2 = fmaxf(m2, fmaxf(lo, fminf(m1, hi)));
+    const float hi = fmaxf(a, b), lo = fmin_nan(a, b);
+    m2 = fmaxf(m2, fmaxf(lo, fmin_nan(m1, hi)));
     m1 = fmaxf(m1, hi);
     screen_pairs_packed<R, D + 2>(src, np, mask, m1, m2);
   }
 }
 
-// np_odd: the same table shifted by one element, so that for odd R the pair
-// starts are 8-byte aligned too (packed path only)
+// Packed x pass (scale 2): candidates d = -R..R at src[d] (pointer at d = 0).
+// The band may be staged with an odd float shift (`odd`), which decides the
+// 8-byte pair alignment: pairs start at d = odd - R and carry codes
+// 0..2R-1 (d = code - R + odd); the remaining single candidate (d = R, or
+// d = -R when odd) carries code 2R.  One code path for both parities keeps
+// the hot code small (a per-parity instantiation doubled it and the kernel
+// stalled on instruction fetch).  np_odd: the penalty table shifted by one
+// element, for the pair alignment of the table side.
 template <int R, int STRIDE, bool PACKED>
 __device__ __forceinline__ void screen_window(const float* __restrict__ src,
                                               const float* __restrict__ np,
                                               const float* __restrict__ np_odd, uint32_t mask,
-                                              float& m1, float& m2) {
+                                              int odd, float& m1, float& m2) {
   m1 = -INFINITY;
   m2 = -INFINITY;
   if constexpr (PACKED) {
-    const float* npp = (R & 1) ? np_odd : np;
-    screen_pairs_packed<R, -R>(src, npp, mask, m1, m2);
+    const float* npp = (((R + odd) & 1) ? np_odd : np) + (odd - R);
+    screen_pairs_packed<R, -R>(src + (odd - R) + R, npp + R, mask, m1, m2);
+    const int sd = odd ? -R : R;
+    const float c = enc_idx<2 * R>(src[sd] + np[sd], mask);
+    m2 = fmaxf(m2, fmin_nan(m1, c));
+    m1 = fmaxf(m1, c);
   } else {
     screen_pairs<R, STRIDE, -R>(src, np, mask, m1, m2);
+    const float c = enc_idx<2 * R>(src[R * STRIDE] + np[R], mask);
+    m2 = fmaxf(m2, fmin_nan(m1, c));
+    m1 = fmaxf(m1, c);
   }
-  const float c = enc_idx<2 * R>(src[R * STRIDE] + np[R], mask);
-  m2 = fmaxf(m2, fminf(m1, c));
-  m1 = fmaxf(m1, c);
 }
 
 // runtime radius -> unrolled instantiation (radius <= RCAP on the staged path)
@@ -180,10 +208,10 @@ template <int STRIDE, bool PACKED>
 __device__ __forceinline__ void screen_dispatch(int r, const float* __restrict__ src,
                                                 const float* __restrict__ np,
                                                 const float* __restrict__ np_odd, uint32_t mask,
-                                                float& m1, float& m2) {
+                                                int odd, float& m1, float& m2) {
   switch (r) {
 #define DPM_SCREEN_CASE(R) \
-  case R: screen_window<R, STRIDE, PACKED>(src, np, np_odd, mask, m1, m2); break;
+  case R: screen_window<R, STRIDE, PACKED>(src, np, np_odd, mask, odd, m1, m2); break;
     DPM_SCREEN_CASE(0) DPM_SCREEN_CASE(1) DPM_SCREEN_CASE(2) DPM_SCREEN_CASE(3)
     DPM_SCREEN_CASE(4) DPM_SCREEN_CASE(5) DPM_SCREEN_CASE(6) DPM_SCREEN_CASE(7)
     DPM_SCREEN_CASE(8) DPM_SCREEN_CASE(9) DPM_SCREEN_CASE(10) DPM_SCREEN_CASE(11)
@@ -217,8 +245,8 @@ __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job
   }
 }
 
-struct __align__(16) PlaceSmem {
-  float s[BAND_MAX * COLS_PITCH];  // staged S band (OUT_SENTINEL outside the map)
+struct __align__(128) PlaceSmem {
+  float s[BAND_MAX * COLS_PITCH];  // S band, TMA-staged (NaN outside the map)
   float x32[BAND_MAX * PT_W];      // x-pass winners' FP32 screen values
   float xsv[BAND_MAX * PT_W];      // x-pass winners' S values (exact y values)
   int8_t xdx[BAND_MAX * PT_W];     // x-pass winning dx
@@ -227,15 +255,44 @@ struct __align__(16) PlaceSmem {
   float npy[2][2 * RCAP + 4];
   alignas(16) JobRange jr[2];      // r*, E2 of the current / next part (16-B cp.async)
   alignas(16) dpm_place_job pj[2]; // placement job of the current / next part
+  alignas(8) uint64_t band_bar;    // TMA completion of the current band (one phase per band)
 };
+static_assert(TMA_BOX_BYTES % 128 == 0, "TMA boxes land 128-byte aligned");
+
+__device__ __forceinline__ uint32_t pl_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// Band copy: one TMA tensor load of a DPM_SMAP_BOX_W x DPM_SMAP_BOX_H box of
+// map z starting at (x, y) (signed; cells outside the map arrive as NaN).
+__device__ __forceinline__ void tma_band_box(uint32_t dst, const void* map, int x, int y, int z,
+                                             uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void pl_mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (int spin = 0; spin < 2000 && !done; ++spin)  // each try suspends up to 10 ms
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(10000000u)
+        : "memory");
+  if (!done) asm volatile("trap;");  // a band that never lands is a bug, not a hang
+}
 
 __global__ void __launch_bounds__(PT_THREADS, 2)
-place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restrict__ pjobs,
+place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restrict__ smaps,
+                      const dpm_place_job* __restrict__ pjobs,
                       const dpm_asm_job* __restrict__ ajobs, int najobs,
                       const dpm_place_range* __restrict__ prep, double* __restrict__ total,
                       uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
                       dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   PlaceSmem& sh = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int jid = find_job(ajobs, najobs, blockIdx.x);
   const dpm_asm_job aj = ajobs[jid];
@@ -286,47 +343,30 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   auto staged_ok = [&](const dpm_place_job& pj, const JobRange& jr) {
     return jr.rx <= RCAP && jr.ry <= RCAP && pj.scale <= 2;
   };
+  // Band of a part: one thread issues the TMA boxes covering band rows
+  // 0..nrows-1 and columns xb0..xb0+COLS_PITCH-1 (outside the map: NaN, which
+  // the screens treat as no candidate); the band barrier completes when all
+  // bytes landed.  The buffer's previous band was last read before the
+  // __syncthreads preceding this call.
+  const uint32_t band_bar = pl_smem(&sh.band_bar);
   auto stage_issue = [&](const dpm_place_job& pj, const JobRange& jr, int buf) {
-    const float* sm = S + pj.s_off;
     const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
     const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
-    const int ncols = pj.scale * (lpr - 1) + 1 + 2 * jr.rx;
-    // only band rows inside the map are staged (the x pass never reads the others)
-    const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
-    const uint32_t s_base = (uint32_t)__cvta_generic_to_shared(sh.s);
-    const int Wp = pj.Wp, sp = s_pitch(pj.Wp);
-    const float* sbase = sm + (int64_t)yb0 * sp + xb0;
-    if (xb0 >= 0 && xb0 + ncols <= Wp) {  // every band column inside the map (uniform)
-      for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
-        const float* srow = sbase + (int64_t)r * sp;
-        const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int c = lane + 32 * q;
-          if (c < ncols)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(drow + 4u * c),
-                         "l"(srow + c));
-        }
-      }
-    } else {
-      for (int r = r_lo + warp; r < r_hi; r += PT_WARPS) {
-        const float* srow = sbase + (int64_t)r * sp;
-        const uint32_t drow = s_base + 4u * (uint32_t)(r * COLS_PITCH);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int c = lane + 32 * q, x = xb0 + c;
-          if (c >= ncols) continue;
-          if (x >= 0 && x < Wp) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(drow + 4u * c),
-                         "l"(srow + c));
-          } else {
-            sh.s[r * COLS_PITCH + c] = OUT_SENTINEL;
-          }
-        }
-      }
+    if (tid == 0) {
+      const int nbox = (nrows + TMA_BH - 1) / TMA_BH;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(band_bar),
+                   "r"((uint32_t)nbox * TMA_BOX_BYTES)
+                   : "memory");
+      const void* map = smaps + (int64_t)pj.smap * DPM_SMAP_BYTES;
+      const uint32_t dst = pl_smem(sh.s);
+      // the box's first column must be 16-byte aligned in the map: start at
+      // xb0 & ~3; band column c then lands at shared column c + (xb0 & 3)
+      for (int k = 0; k < nbox; ++k)
+        tma_band_box(dst + (uint32_t)k * TMA_BOX_BYTES, map, xb0 & ~3, yb0 + k * TMA_BH, pj.smap_z,
+                     band_bar);
     }
-    asm volatile("cp.async.commit_group;\n" ::);
     if (tid >= PT_THREADS - 2 * (2 * RCAP + 1)) {  // last warps: penalty tables
       const int t = tid - (PT_THREADS - 2 * (2 * RCAP + 1));
       const int d = (t % (2 * RCAP + 1)) - RCAP;
@@ -362,6 +402,11 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     const JobRange jn = sh.jr[buf];
     if (staged_ok(pn, jn)) stage_issue(pn, jn, buf);
   };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(band_bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t bands = 0;  // bands staged so far: band k completes barrier phase k
   if (aj.nparts > 0) {
     fetch_job(0, 0);
     asm volatile("cp.async.wait_group 0;\n" ::);
@@ -370,10 +415,12 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
   }
   for (int p = 0; p < aj.nparts; ++p) {
     const int buf = p & 1;
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();  // band p and its penalty tables resident; part p-1 finished
+    // the job record of part p landed before the previous barrier
     const dpm_place_job pj = sh.pj[buf];
     const JobRange jr = sh.jr[buf];
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    if (staged_ok(pj, jr)) pl_mbar_wait(band_bar, bands++ & 1);  // band p landed
+    __syncthreads();  // penalty tables of part p visible; part p-1 finished
     const float* sm = S + pj.s_off;
     const bool have_next = p + 1 < aj.nparts;
     if (have_next) fetch_job(p + 1, buf ^ 1);
@@ -402,6 +449,8 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     }
     const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
+    const int xsh = (pj.scale * rx_lo + pj.ax - jr.rx) & 3;  // band column 0's shared column
+    const int xodd = pj.scale == 2 ? (xsh & 1) : 0;           // packed-pair parity (screen_window)
 
     // x pass: band row r (warp-strided), centre column = lane
     const float* npx = sh.npx[buf] + RCAP;
@@ -421,15 +470,16 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
     for (int rb = r_lo + warp * rpw; rb < r_hi; rb += PT_WARPS * rpw) {  // in-map rows only
       const int r = rb + xsub;
       if (r >= r_hi) continue;
-      const float* srow = sh.s + r * COLS_PITCH + pj.scale * xc + jr.rx;  // dx = 0
+      const float* srow = sh.s + r * COLS_PITCH + xsh + pj.scale * xc + jr.rx;  // dx = 0
       float m1, m2;
-      if (pj.scale == 2)  // 2*lane + even row base: pair starts are 8-byte aligned
-        screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
+      if (pj.scale == 2)  // even row base + 2*lane: pair alignment follows the shift parity
+        screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, xodd, m1, m2);
       else
-        screen_dispatch<1, false>(jr.rx, srow, npx, npx_odd, code_mask, m1, m2);
+        screen_dispatch<1, false>(jr.rx, srow, npx, npx_odd, code_mask, 0, m1, m2);
       // the y-pass screen only needs the winner's value to the screening
       // accuracy; exact values are recomputed from xsv for y winners and ties
-      int xi = (__float_as_int(m1) & 63) - jr.rx;
+      const int code = __float_as_int(m1) & 63;
+      int xi = code == 2 * jr.rx ? (xodd ? -jr.rx : jr.rx) : code - jr.rx + xodd;
       if (m1 < NONE_BELOW) {  // no candidate inside the map: reference gives (-inf, -r)
         xi = -jr.rx;
         m1 = OUT_SENTINEL;
@@ -465,7 +515,7 @@ place_assemble_kernel(const float* __restrict__ S, const dpm_place_job* __restri
       const int r0 = cy - yb0;  // band row of dy = 0
       const float* xcol = sh.x32 + r0 * PT_W + ixr;
       float m1, m2;
-      screen_dispatch<PT_W, false>(jr.ry, xcol, npy, npy, code_mask, m1, m2);
+      screen_dispatch<PT_W, false>(jr.ry, xcol, npy, npy, code_mask, 0, m1, m2);
       auto exact = [&](int dy) -> double {
         const int row = (r0 + dy) * PT_W + ixr;
         const int dx = sh.xdx[row];
@@ -607,11 +657,14 @@ extern "C" int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uin
   return DPM_OK;
 }
 
-extern "C" int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dpm_asm_job* ajobs,
-                            int najobs, int64_t nblocks, const dpm_place_range* prep, double* total,
-                            uint32_t* pos, double* placed, double tau, dpm_detection* dets,
-                            int max_dets, int* det_count, void* stream) {
-  DPM_REQUIRE(S && pjobs && ajobs && prep, "dpm_assemble: null pointer");
+extern "C" int dpm_assemble(const float* S, const void* smaps, const dpm_place_job* pjobs,
+                            const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
+                            const dpm_place_range* prep, double* total, uint32_t* pos,
+                            double* placed, double tau, dpm_detection* dets, int max_dets,
+                            int* det_count, void* stream) {
+  DPM_REQUIRE(S && smaps && pjobs && ajobs && prep, "dpm_assemble: null pointer");
+  DPM_REQUIRE((reinterpret_cast<uintptr_t>(smaps) & 63) == 0,
+              "dpm_assemble: tensor maps must be 64-byte aligned");
   DPM_REQUIRE(!dets || (det_count && pos), "dpm_assemble: detections need a counter and positions");
   DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_assemble: nblocks");
   if (najobs == 0 || nblocks == 0) return DPM_OK;
@@ -619,7 +672,47 @@ extern "C" int dpm_assemble(const float* S, const dpm_place_job* pjobs, const dp
   DPM_CUDA(cudaFuncSetAttribute(place_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   place_assemble_kernel<<<(unsigned)nblocks, PT_THREADS, smem, as_stream(stream)>>>(
-      S, pjobs, ajobs, najobs, prep, total, pos, placed, tau, dets, max_dets, det_count);
+      S, static_cast<const unsigned char*>(smaps), pjobs, ajobs, najobs, prep, total, pos, placed,
+      tau, dets, max_dets, det_count);
   DPM_LAUNCHED("place_assemble_kernel");
+  return DPM_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link); host only, no context work.
+extern "C" int dpm_smap_encode(const float* S, const dpm_smap_desc* descs, int n, void* maps_host) {
+  DPM_REQUIRE(S && (n == 0 || (descs && maps_host)), "dpm_smap_encode: null pointer");
+  DPM_REQUIRE((reinterpret_cast<uintptr_t>(S) & 15) == 0, "dpm_smap_encode: S must be 16-byte aligned");
+  DPM_REQUIRE((reinterpret_cast<uintptr_t>(maps_host) & 63) == 0,
+              "dpm_smap_encode: maps_host must be 64-byte aligned");
+  static_assert(sizeof(CUtensorMap) == DPM_SMAP_BYTES, "CUtensorMap size");
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (encode == nullptr) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    DPM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    DPM_REQUIRE(q == cudaDriverEntryPointSuccess && fn != nullptr,
+                "dpm_smap_encode: cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  for (int i = 0; i < n; ++i) {
+    const dpm_smap_desc& d = descs[i];
+    DPM_REQUIRE(d.Ho >= 1 && d.Wo >= 1 && d.nf >= 1 && d.s_off >= 0 && d.s_off % 4 == 0,
+                "dpm_smap_encode: descriptor %d has Ho=%d Wo=%d nf=%d s_off=%lld", i, d.Ho, d.Wo,
+                d.nf, (long long)d.s_off);
+    const int pitch = s_pitch(d.Wo);
+    const cuuint64_t dims[3] = {(cuuint64_t)d.Wo, (cuuint64_t)d.Ho, (cuuint64_t)d.nf};
+    const cuuint64_t strides[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)pitch * 4 * d.Ho};
+    const cuuint32_t box[3] = {DPM_SMAP_BOX_W, DPM_SMAP_BOX_H, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(reinterpret_cast<CUtensorMap*>(maps_host) + i,
+                              CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                              const_cast<float*>(S + d.s_off), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
+    DPM_REQUIRE(r == CUDA_SUCCESS, "dpm_smap_encode: descriptor %d rejected (CUresult %d)", i,
+                (int)r);
+  }
   return DPM_OK;
 }

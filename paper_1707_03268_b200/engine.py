@@ -220,6 +220,8 @@ class Plan:
         jobs, classes = [], {}
         job_image = []
         nslots = 0
+        self.map_smap = {}  # (image, level, filt) -> (TMA descriptor, index in its group)
+        smap_descs = []
         for img in range(nimg):
             for k, fl in self.groups:
                 H, W = self.levels[k]
@@ -227,6 +229,9 @@ class Plan:
                 ho, wo = H - fd.h + 1, W - fd.w + 1
                 wp = _spitch(wo)  # rows padded to 16 B (include/dpm_b200.h, "S maps")
                 s_off = sa.take(len(fl) * ho * wp, align=4)
+                for i, f in enumerate(fl):
+                    self.map_smap[(img, k, f)] = (len(smap_descs), i)
+                smap_descs.append((s_off, ho, wo, len(fl), 0))
                 rng = -1
                 if any((k, f) in placed_maps for f in fl):
                     rng = nslots
@@ -254,6 +259,7 @@ class Plan:
                     for tx in range((wo + tw - 1) // tw):
                         cls["tiles"].append((jid, ty, tx, 0))
         self.s_size = max(sa.size, 4)
+        self._smap_descs = np.array(smap_descs, dtype=_lib.SMAP_DESC)
         self.n_ranges = nslots
         self._corr_jobs = np.array(jobs, dtype=_lib.CORR_JOB) if jobs else np.zeros(0, _lib.CORR_JOB)
         self._corr_job_image = np.array(job_image, dtype=np.int64)
@@ -296,6 +302,7 @@ class Plan:
                     place.append((self.map_off[(img, p.level, p.filt)], x_off,
                                   hp, wp, p.anchor[0], p.anchor[1], p.scale, p.radius, rx0, wr,
                                   self.range_slot[(img, p.level, p.filt)], 0,
+                                  *self.map_smap[(img, p.level, p.filt)],
                                   *[float(v) for v in p.deformation]))
                 root_off, root_pitch = -1, 0
                 if a.root is not None:
@@ -374,6 +381,13 @@ class Plan:
         self.X = t.empty(self.n_images * self.x_image_stride, dtype=t.float32, device=dev)
         self.P = t.empty(self.n_images * self.p_image_stride, dtype=t.float32, device=dev)
         self.S = t.empty(self.s_size, dtype=t.float32, device=dev)
+        # TMA descriptors of the S map groups (K3 band staging); they embed S's address
+        maps = np.zeros(max(len(self._smap_descs), 1) * _lib.SMAP_BYTES + 64, dtype=np.uint8)
+        a64 = (-maps.ctypes.data) % 64
+        maps_h = maps[a64:a64 + len(self._smap_descs) * _lib.SMAP_BYTES]
+        _lib.check(_lib.lib().dpm_smap_encode(self.S.data_ptr(), _lib.table_ptr(self._smap_descs),
+                                       len(self._smap_descs), maps_h.ctypes.data), "smap encode")
+        self.smaps = t.from_numpy(maps_h.copy()).to(dev)
         self.ranges = t.empty(max(2 * self.n_ranges, 2), dtype=t.int32, device=dev)
         self.totals = t.empty(max(self.total_size, 1), dtype=t.float64, device=dev)
         self.positions = t.empty(max(self.pos_size, 1), dtype=t.int32, device=dev)
@@ -509,7 +523,8 @@ class Plan:
             mark("k3k4_place_assemble")
             aj_d, naj, nblk = tb["asm"]
             _lib.check(lib.dpm_assemble(
-                ptr(self.S), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk, ptr(self.prep),
+                ptr(self.S), ptr(self.smaps), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk,
+                ptr(self.prep),
                 ptr(self.totals) if self.total_size else None,
                 ptr(self.positions) if self.pos_size else None,
                 ptr(self.placed) if self.placed_size else None,

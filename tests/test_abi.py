@@ -32,7 +32,7 @@ def test_struct_sizes_match_header_comments():
     # sizes asserted at import against the C layout (int64 first, natural alignment)
     assert _lib.PROJ_JOB.itemsize == 32
     assert _lib.CORR_JOB.itemsize == 72
-    assert _lib.PLACE_JOB.itemsize == 88
+    assert _lib.PLACE_JOB.itemsize == 96
     assert _lib.ASM_JOB.itemsize == 88
     assert _lib.DETECTION.itemsize == 96
 
@@ -43,7 +43,8 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
     fields = {
         "dpm_proj_job": ("x_off", "p_off", "H", "W", "pitch", "block0"),
         "dpm_corr_job": ("p_off", "s_off", "g_off", "H", "nf_pad", "range_idx"),
-        "dpm_place_job": ("s_off", "x_off", "Hp", "rx0", "block0", "cdx", "cdyy"),
+        "dpm_place_job": ("s_off", "x_off", "Hp", "rx0", "block0", "smap", "smap_z", "cdx", "cdyy"),
+        "dpm_smap_desc": ("s_off", "Ho", "Wo", "nf", "pad"),
         "dpm_asm_job": ("root_off", "placed_off", "root_pitch", "block0", "bias"),
         "dpm_detection": ("image", "score", "parts"),
         "dpm_place_range": ("rx", "ry", "E2", "pad"),
@@ -65,7 +66,7 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
     dts = {"dpm_proj_job": _lib.PROJ_JOB, "dpm_corr_job": _lib.CORR_JOB,
            "dpm_place_job": _lib.PLACE_JOB, "dpm_asm_job": _lib.ASM_JOB,
            "dpm_detection": _lib.DETECTION, "dpm_place_range": _lib.PLACE_RANGE,
-           "dpm_prune_job": _lib.PRUNE_JOB}
+           "dpm_prune_job": _lib.PRUNE_JOB, "dpm_smap_desc": _lib.SMAP_DESC}
     for st, fs in fields.items():
         assert int(out[st]) == dts[st].itemsize, st
         for f in fs:
