@@ -16,7 +16,9 @@
 //
 // One kernel: each CTA owns a 32 x 64 tile of roots of one (image,
 // component, root level).  Per part it stages the S band its windows touch
-// in shared memory, runs the x pass for every band row at the 32 centre
+// in shared memory (TMA tensor boxes, one thread, mbarrier completion; the
+// next part's band lands during this part's y pass), runs the x pass for
+// every band row at the 32 centre
 // columns (64-row tiles keep the band overlap between vertically adjacent
 // tiles at 2r / 128 rows), then the y pass for its roots; exact FP64 values
 // are recomputed from the staged band.  Root + parts + bias are summed in
@@ -31,8 +33,10 @@
 // least twice the FP32 error plus the encoding error of any candidate,
 // m2 < m1 - E2 proves the decoded winner is the unique exact winner;
 // otherwise (ties, near ties) the candidates within E2 of m1 are rescanned
-// in FP64 in the reference's order.  Cells outside the map are staged as a
-// finite sentinel (-1e37) so encodings stay finite.
+// in FP64 in the reference's order.  Cells outside the map arrive as NaN
+// (TMA out-of-bounds fill): fmaxf ignores them and the NaN-propagating min of
+// the merge keeps them out of m2, so a window without any in-map cell ends
+// with m1 = -inf, the reference's "no candidate".
 //
 // radius < 0 selects the unbounded generalised distance transform, realised
 // as the window of radius r* computed from the map's
@@ -111,7 +115,7 @@ __device__ __forceinline__ uint32_t pack_pos(int y, int x) {
   return ((uint32_t)(uint16_t)(int16_t)y << 16) | (uint32_t)(uint16_t)(int16_t)x;
 }
 
-constexpr float OUT_SENTINEL = -1.0e37f;  // staged cells outside the map
+constexpr float OUT_SENTINEL = -1.0e37f;  // x-pass result of a band row without candidates
 constexpr float NONE_BELOW = -1.0e36f;    // m1 below this: no candidate inside the map
 
 // (bits(v) & mask) | code in ONE lop3 (LUT 0xEA = (a & b) | c): the mask
