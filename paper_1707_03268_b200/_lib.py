@@ -17,6 +17,7 @@ __all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "AS
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdpm_b200.so")
 MAX_PARTS = 16
+ABI_VERSION = 2  # DPM_ABI_VERSION of include/dpm_b200.h
 
 DPM_OK, DPM_ERR_ARG, DPM_ERR_UNSUPPORTED, DPM_ERR_CUDA, DPM_ERR_NUMERIC = 0, -1, -2, -3, -4
 
@@ -118,7 +119,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.dpm_abi_version() != 2:
+        if handle.dpm_abi_version() != ABI_VERSION:
             raise DeviceError("libdpm_b200.so ABI version mismatch")
         _lib = handle
     return _lib
