@@ -284,6 +284,10 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       const uint32_t idesc_s = idesc_tf32(16 * KS), idesc_sb = idesc_bf16(16 * KS);
       const uint64_t dBs = umma_desc(smem_u32(sB), NB * 256u, 128u);
       const uint64_t dB2s = umma_desc(smem_u32(sB2), NB * 256u, 128u);
+      // ring slot / phase of each group's first input row advance
+      // incrementally (no division on the issue path; see the FH > 0 branch)
+      const uint32_t ring = (uint32_t)a.ring;
+      uint32_t gs = 0, gph = 0;
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
         const dpm_corr_job job = a.jobs[a.strips[st].job];
         const int ho = job.H - FH + 1;
@@ -295,14 +299,15 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
           const uint32_t d = tmem_base + (uint32_t)(b * a.acc_cols);
           const int tmax = min(KS + FH - 1, job.H - y);
           for (int t = 0; t < tmax; ++t) {
-            const uint32_t q = q_glob + y + t;
+            uint32_t sl = gs + (uint32_t)t, ph = gph;
+            if (sl >= ring) { sl -= ring; ph ^= 1; }
             if (y + t >= qready) {
-              mbar_wait(full + q % a.ring, (q / a.ring) & 1);
+              mbar_wait(full + sl, ph);
               qready = y + t + 1;
             }
             tc_fence_after();
-            const uint64_t da = dA0 + (q % a.ring) * slot_step;
-            const uint64_t dal = dAlo0 + (q % a.ring) * slot_step;
+            const uint64_t da = dA0 + sl * slot_step;
+            const uint64_t dal = dAlo0 + sl * slot_step;
             const uint32_t s0 = (uint32_t)(FH - 1 + KS - 1 - t) * 16u;  // window start (>> 4)
             if (elect_one()) {
 #pragma unroll
@@ -319,6 +324,17 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
           // the epilogue frees the group's dead input rows once it sees tfull
           if (elect_one()) tc_commit(tfull + b);
           __syncwarp();
+          gs += KS;  // next group's first row (KS < ring)
+          if (gs >= ring) { gs -= ring; gph ^= 1; }
+        }
+        // rows y .. H-1 of the strip were never first rows of a group
+        for (int rr = y; rr < job.H; ++rr)
+          if (++gs == ring) { gs = 0; gph ^= 1; }
+        if (y > job.H) {  // the last group stepped past the strip end
+          for (int rr = job.H; rr < y; ++rr) {
+            if (gs == 0) { gs = ring; gph ^= 1; }
+            --gs;
+          }
         }
         q_glob += job.H;
       }
