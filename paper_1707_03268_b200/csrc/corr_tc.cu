@@ -194,7 +194,9 @@ __device__ __forceinline__ float tf32_hi(float a) {
 template <int NMAX, int FH, int FW, int EPI = 4, int KS = 1>
 __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kernel(const TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: provably warp-uniform, so the role
+  // branches below do not make the MMA warp's bookkeeping divergent
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int nq = a.R >> 2;                       // rank quads
   const int taps = a.h * a.w;
   const int tcols = TC_M + a.w - 1;
