@@ -121,6 +121,32 @@ def test_placement_grid_bit_exact_on_fp32_maps_and_golden():
         assert err == 0, k
 
 
+def test_placement_band_edges_bit_exact():
+    """TMA band staging at the map edges: maps narrower and wider than the
+    100-column box, windows reaching past every edge (negative and odd band
+    origins: every 16-byte shift parity of the box start), radii up to the
+    staged cap (16) and one beyond it (unstaged path).  Cells outside the map
+    arrive as NaN; results (values, -inf for empty windows, positions) must
+    equal the oracle's exactly."""
+    rng = np.random.default_rng(1707)
+    shapes = [(4, 3), (40, 17), (9, 37), (33, 99), (21, 101), (70, 133)]
+    for case in range(60):
+        H, W = shapes[case % len(shapes)]
+        smap = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+        r = int(rng.choice([0, 1, 2, 7, 15, 16, 17]))
+        # |anchor| <= r: windows reach up to 2r past the edges (the reference's
+        # padding, detection.py:320-373)
+        anc = (int(rng.integers(-r, r + 1)), int(rng.integers(-r, r + 1)))
+        de = (float(rng.uniform(-0.05, 0.05)), float(rng.uniform(-0.05, 0.05)),
+              float(rng.uniform(0.005, 0.05)), float(rng.uniform(0.005, 0.05)))
+        rect = (0, H - 1, 0, W - 1)
+        part = B.PartSpec(np.zeros((1, 1, 1)), anc, de, r)
+        placed, py, px = B._placement_grid(smap, part, rect)
+        o_placed, o_py, o_px = O.placement_grid(f32(smap), anc, de, r, rect)
+        assert np.array_equal(placed, o_placed), (case, H, W, r, anc)
+        assert np.array_equal(py, o_py) and np.array_equal(px, o_px), (case, H, W, r, anc)
+
+
 def test_best_part_placement_known_answers():
     part = B.PartSpec(np.zeros((2, 2, 3)), (0, 0), (0.0, 0.0, 0.0, 0.0), 1)
     assert B.best_part_placement(part, np.zeros((5, 5)), (2, 2)) == ((1, 1), 0.0)
