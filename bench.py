@@ -104,59 +104,100 @@ def cpu_run(tasks, workers):
 # ---------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during a timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING a timed
+    region.  NVML polled from a thread every 5 ms (no process start-up, so a
+    short region still gets samples; the device is found by the CUDA
+    device's UUID, right under CUDA_VISIBLE_DEVICES remapping); nvidia-smi
+    -lms 100 as the fallback when NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, device_index):
-        self.dev = str(device_index)
-        self.rows = []
+        self.index = int(device_index)
+        self.rows = []  # (sm_mhz, max_mhz, reason names)
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+        self.thread = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        uuid = getattr(torch.cuda.get_device_properties(self.index), "uuid", None)
+        if uuid is not None:
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(uuid))
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
         try:
+            nv, h = self._nvml_handle()
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_reasons = (getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None)
+                           or nv.nvmlDeviceGetCurrentClocksThrottleReasons)
+            self.nvml = (nv, h)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        bits = get_reasons(h)
+                        self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                          float(smax),
+                                          {n for n, m in self.REASONS if bits & m}))
+                    except Exception:
+                        pass
+                    self.stop.wait(0.005)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:  # fallback: nvidia-smi
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", self.dev, f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(target=self._read_smi, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
+            r = [v.strip() for v in line.split(",")]
+            try:
+                names = {n for (n, _), v in zip(self.REASONS, r[5:9]) if v.lower().startswith("active")}
+                self.rows.append((float(r[1]), float(r[2]), names))
+            except (ValueError, IndexError):
+                continue
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.thread is not None:
             self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], [], set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in self.rows:
-            try:
-                sm.append(float(r[1]))
-                smax.append(float(r[2]))
-            except (ValueError, IndexError):
-                continue
-            for n, v in zip(names, r[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"],
+                    "source": "nvml" if self.nvml else "nvidia-smi"}
+        reasons = set().union(*(r[2] for r in self.rows))
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------- helpers
