@@ -2,6 +2,8 @@
 
     python tools/ncu_lines.py <report.ncu-rep> <kernel regex> <object.o> <mangled kernel> [top]
 
+NCU_LINES_SORT=stall ranks the lines by stall samples instead of instructions.
+
 Joins the SASS page of the report (executed instructions and stall samples
 per instruction) with `nvdisasm --print-line-info` of the kernel in the
 object file (same build), by offset from the function start.
@@ -56,7 +58,9 @@ def main():
     ti, ts = sum(ins.values()), sum(st.values())
     print(f"instructions {ti}, stall samples {ts}")
     srcs = {}
-    for k, n in ins.most_common(top):
+    order = st if os.environ.get("NCU_LINES_SORT") == "stall" else ins
+    for k, _ in order.most_common(top):
+        n = ins[k]
         f, _, ln = k.partition(":")
         if f not in srcs:
             path = os.path.join(os.path.dirname(obj), "..", "..", "paper_1707_03268_b200", "csrc", f)
