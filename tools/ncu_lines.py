@@ -2,7 +2,7 @@
 
     python tools/ncu_lines.py <report.ncu-rep> <kernel regex> <object.o> <mangled kernel> [top]
 
-NCU_LINES_SORT=stall ranks the lines by stall samples instead of instructions.
+NCU_LINES_SKIP=k takes the (k+1)-th matching launch.  NCU_LINES_SORT=stall ranks the lines by stall samples instead of instructions.
 
 Joins the SASS page of the report (executed instructions and stall samples
 per instruction) with `nvdisasm --print-line-info` of the kernel in the
@@ -22,7 +22,8 @@ def main():
     rep, kre, obj, fn = sys.argv[1:5]
     top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
-                          f"regex:{kre}", "--launch-count", "1"], capture_output=True, text=True).stdout
+                          f"regex:{kre}", "--launch-skip", os.environ.get("NCU_LINES_SKIP", "0"),
+                          "--launch-count", "1"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
     seen, data = set(), []
