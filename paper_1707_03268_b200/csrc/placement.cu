@@ -249,6 +249,41 @@ __device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job
   }
 }
 
+// Exact rescans of a near-tie window in the reference's order (ascending
+// offset, strict '>'), over the candidates whose FP32 screen value reaches
+// lo.  Rare; kept out of line so the screening loops do not reserve their
+// FP64 registers.
+__device__ __noinline__ int x_rescan(const float* srow, const float* npx, float lo, int rx,
+                                     const dpm_place_job* pj) {
+  const double cdx = pj->cdx, cdxx = pj->cdxx;
+  double xv = -INFINITY;
+  int xi = -rx;
+  for (int dx = -rx; dx <= rx; ++dx) {
+    if (srow[dx] + npx[dx] >= lo) {
+      const double e = __dadd_rn((double)srow[dx], -pen(cdx, cdxx, dx));
+      if (e > xv) { xv = e; xi = dx; }
+    }
+  }
+  return xi;
+}
+
+// y: xcol / xsv / xdx point at the dy = 0 row of the root's column (stride PT_W)
+__device__ __noinline__ int y_rescan(const float* xcol, const float* xsv, const int8_t* xdx,
+                                     const float* npy, float lo, int ry, const dpm_place_job* pj,
+                                     double& best) {
+  const double cdx = pj->cdx, cdxx = pj->cdxx, cdy = pj->cdy, cdyy = pj->cdyy;
+  best = -INFINITY;
+  int bi = -ry;
+  for (int dy = -ry; dy <= ry; ++dy) {
+    if (xcol[dy * PT_W] + npy[dy] >= lo) {
+      const double xv = __dadd_rn((double)xsv[dy * PT_W], -pen(cdx, cdxx, xdx[dy * PT_W]));
+      const double e = __dadd_rn(xv, -pen(cdy, cdyy, dy));
+      if (e > best) { best = e; bi = dy; }
+    }
+  }
+  return bi;
+}
+
 struct __align__(128) PlaceSmem {
   float s[BAND_MAX * COLS_PITCH];  // S band, TMA-staged (NaN outside the map)
   float x32[BAND_MAX * PT_W];      // x-pass winners' FP32 screen values
@@ -488,15 +523,7 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
         xi = -jr.rx;
         m1 = OUT_SENTINEL;
       } else if (m2 >= m1 - jr.E2) {  // tie or near tie: exact rescan, reference order
-        const float lo = m1 - jr.E2;
-        double xv = -INFINITY;
-        xi = -jr.rx;
-        for (int dx = -jr.rx; dx <= jr.rx; ++dx) {
-          if (srow[dx] + npx[dx] >= lo) {
-            const double e = __dadd_rn((double)srow[dx], -pen(pj.cdx, pj.cdxx, dx));
-            if (e > xv) { xv = e; xi = dx; }
-          }
-        }
+        xi = x_rescan(srow, npx, m1 - jr.E2, jr.rx, &sh.pj[buf]);
       }
       sh.x32[r * PT_W + xc] = m1;
       sh.xsv[r * PT_W + xc] = srow[xi];
@@ -532,15 +559,8 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
         best = -INFINITY;
         bi = -jr.ry;
       } else if (m2 >= m1 - jr.E2) {
-        const float lo = m1 - jr.E2;
-        best = -INFINITY;
-        bi = -jr.ry;
-        for (int dy = -jr.ry; dy <= jr.ry; ++dy) {
-          if (xcol[dy * PT_W] + npy[dy] >= lo) {
-            const double e = exact(dy);
-            if (e > best) { best = e; bi = dy; }
-          }
-        }
+        bi = y_rescan(xcol, sh.xsv + r0 * PT_W + ixr, sh.xdx + r0 * PT_W + ixr, npy, m1 - jr.E2,
+                      jr.ry, &sh.pj[buf], best);
       } else {
         best = exact(bi);
       }
