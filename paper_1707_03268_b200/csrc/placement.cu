@@ -455,8 +455,8 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
   for (int p = 0; p < aj.nparts; ++p) {
     const int buf = p & 1;
     // the job record of part p landed before the previous barrier
-    const dpm_place_job pj = sh.pj[buf];
-    const JobRange jr = sh.jr[buf];
+    const dpm_place_job& pj = sh.pj[buf];
+    const JobRange& jr = sh.jr[buf];
     asm volatile("cp.async.wait_group 0;\n" ::);
     if (staged_ok(pj, jr)) pl_mbar_wait(band_bar, bands++ & 1);  // band p landed
     __syncthreads();  // penalty tables of part p visible; part p-1 finished
