@@ -294,6 +294,7 @@ struct __align__(128) PlaceSmem {
   float npy[2][2 * RCAP + 4];
   alignas(16) JobRange jr[2];      // r*, E2 of the current / next part (16-B cp.async)
   alignas(16) dpm_place_job pj[2]; // placement job of the current / next part
+  dpm_asm_job aj;                  // this CTA's assembly job
   alignas(8) uint64_t band_bar;    // TMA completion of the current band (one phase per band)
 };
 static_assert(TMA_BOX_BYTES % 128 == 0, "TMA boxes land 128-byte aligned");
@@ -334,7 +335,9 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   PlaceSmem& sh = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int jid = find_job(ajobs, najobs, blockIdx.x);
-  const dpm_asm_job aj = ajobs[jid];
+  if (threadIdx.x == 0) sh.aj = ajobs[jid];
+  __syncthreads();
+  const dpm_asm_job& aj = sh.aj;
   const int hr = aj.ry1 - aj.ry0 + 1, wr = aj.rx1 - aj.rx0 + 1;
   const int ntx = (wr + PT_W - 1) / PT_W;
   const int tile = blockIdx.x - aj.block0;
