@@ -455,18 +455,22 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
     __syncthreads();
     issue_part(0);
   }
+  // this job's position / placed outputs (nullptr: not requested)
+  uint32_t* const posb = aj.pos_off >= 0 ? pos + aj.pos_off : nullptr;
+  double* const placedb = aj.placed_off >= 0 ? placed + aj.placed_off : nullptr;
   for (int p = 0; p < aj.nparts; ++p) {
     const int buf = p & 1;
     // the job record of part p landed before the previous barrier
     const dpm_place_job& pj = sh.pj[buf];
     const JobRange& jr = sh.jr[buf];
     asm volatile("cp.async.wait_group 0;\n" ::);
-    if (staged_ok(pj, jr)) pl_mbar_wait(band_bar, bands++ & 1);  // band p landed
+    const bool staged = staged_ok(pj, jr);
+    if (staged) pl_mbar_wait(band_bar, bands++ & 1);  // band p landed
     __syncthreads();  // penalty tables of part p visible; part p-1 finished
     const float* sm = S + pj.s_off;
     const bool have_next = p + 1 < aj.nparts;
     if (have_next) fetch_job(p + 1, buf ^ 1);
-    if (!staged_ok(pj, jr)) {
+    if (!staged) {
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         int iyr, ixr;
@@ -478,9 +482,9 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
         int bdy, bdx;
         place_unstaged(sm, pj, cy, cx, jr.rx, jr.ry, best, bdy, bdx);
         tot[k] = __dadd_rn(tot[k], best);
-        const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
-        if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bdy, cx + bdx);
-        if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
+        const int o = (p * hr + iy) * wr + ix;  // < nparts * hr * wr: 32-bit
+        if (posb) posb[o] = pack_pos(cy + bdy, cx + bdx);
+        if (placedb) placedb[o] = best;
       }
       if (have_next) {
         asm volatile("cp.async.wait_group 0;\n" ::);
@@ -509,10 +513,11 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
     }
     const int xsub = lane >> lpr_log, xc = lane & (lpr - 1);
     const int rpw = PT_W >> lpr_log;  // band rows per warp step
+    const float* srow0 = sh.s + xsh + pj.scale * xc + jr.rx;  // band row 0, dx = 0
     for (int rb = r_lo + warp * rpw; rb < r_hi; rb += PT_WARPS * rpw) {  // in-map rows only
       const int r = rb + xsub;
       if (r >= r_hi) continue;
-      const float* srow = sh.s + r * COLS_PITCH + xsh + pj.scale * xc + jr.rx;  // dx = 0
+      const float* srow = srow0 + r * COLS_PITCH;
       float m1, m2;
       if (pj.scale == 2)  // even row base + 2*lane: pair alignment follows the shift parity
         screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, xodd, m1, m2);
@@ -569,9 +574,9 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
       }
       const int bdx = sh.xdx[(r0 + bi) * PT_W + ixr];
       tot[k] = __dadd_rn(tot[k], best);
-      const int64_t o = ((int64_t)p * hr + iy) * wr + ix;
-      if (aj.pos_off >= 0) pos[aj.pos_off + o] = pack_pos(cy + bi, cx + bdx);
-      if (aj.placed_off >= 0) placed[aj.placed_off + o] = best;
+      const int o = (p * hr + iy) * wr + ix;
+      if (posb) posb[o] = pack_pos(cy + bi, cx + bdx);
+      if (placedb) placedb[o] = best;
     }
   }
 
@@ -664,6 +669,11 @@ extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_
     }
     jobs[i].block0 = (int32_t)b;
     const int64_t hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
+    if ((int64_t)(j.nparts > 0 ? j.nparts : 1) * hr * wr > INT32_MAX) {  // 32-bit output offsets
+      set_error("dpm_assemble_prepare: job %d: %d parts x %lld x %lld roots exceed 2^31 outputs", i,
+                j.nparts, (long long)hr, (long long)wr);
+      return DPM_ERR_ARG;
+    }
     b += ((hr + PT_H - 1) / PT_H) * ((wr + PT_W - 1) / PT_W);
   }
   if (b > INT32_MAX) {
