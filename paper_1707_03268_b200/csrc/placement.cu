@@ -299,6 +299,37 @@ struct __align__(128) PlaceSmem {
 };
 static_assert(TMA_BOX_BYTES % 128 == 0, "TMA boxes land 128-byte aligned");
 
+// x pass over one warp's band rows rb0, rb0 + step, ... (< r_hi) for a
+// compile-time radius: the radius switch sits outside the row loop, so the
+// loop carries no per-row dispatch and the winner decode folds R.
+template <int R, bool PACKED>
+__device__ __forceinline__ void x_rows(PlaceSmem& sh, int buf, const float* srow0, int rb0,
+                                       int r_hi, int step, int xsub, int xc, uint32_t mask,
+                                       int xodd, float E2) {
+  const float* npx = sh.npx[buf] + RCAP;
+  const float* npx_odd = sh.npx_odd[buf] + RCAP + 1;
+  for (int rb = rb0; rb < r_hi; rb += step) {
+    const int r = rb + xsub;
+    if (r >= r_hi) continue;
+    const float* srow = srow0 + r * COLS_PITCH;
+    float m1, m2;
+    screen_window<R, 1, PACKED>(srow, npx, npx_odd, mask, xodd, m1, m2);
+    // the y-pass screen only needs the winner's value to the screening
+    // accuracy; exact values are recomputed from xsv for y winners and ties
+    const int code = __float_as_int(m1) & 63;
+    int xi = code == 2 * R ? (xodd ? -R : R) : code - R + xodd;
+    if (m1 < NONE_BELOW) {  // no candidate inside the map: reference gives (-inf, -r)
+      xi = -R;
+      m1 = OUT_SENTINEL;
+    } else if (m2 >= m1 - E2) {  // tie or near tie: exact rescan, reference order
+      xi = x_rescan(srow, npx, m1 - E2, R, &sh.pj[buf]);
+    }
+    sh.x32[r * PT_W + xc] = m1;
+    sh.xsv[r * PT_W + xc] = srow[xi];
+    sh.xdx[r * PT_W + xc] = (int8_t)xi;
+  }
+}
+
 __device__ __forceinline__ uint32_t pl_smem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -499,8 +530,6 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
     const int xodd = pj.scale == 2 ? (xsh & 1) : 0;           // packed-pair parity (screen_window)
 
     // x pass: band row r (warp-strided), centre column = lane
-    const float* npx = sh.npx[buf] + RCAP;
-    const float* npx_odd = sh.npx_odd[buf] + RCAP + 1;
     // band rows outside the map have no candidate (reference: (-inf, -r))
     const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
     const int n_out = r_lo + (nrows - r_hi);
@@ -514,28 +543,28 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
     const int xsub = lane >> lpr_log, xc = lane & (lpr - 1);
     const int rpw = PT_W >> lpr_log;  // band rows per warp step
     const float* srow0 = sh.s + xsh + pj.scale * xc + jr.rx;  // band row 0, dx = 0
-    for (int rb = r_lo + warp * rpw; rb < r_hi; rb += PT_WARPS * rpw) {  // in-map rows only
-      const int r = rb + xsub;
-      if (r >= r_hi) continue;
-      const float* srow = srow0 + r * COLS_PITCH;
-      float m1, m2;
-      if (pj.scale == 2)  // even row base + 2*lane: pair alignment follows the shift parity
-        screen_dispatch<1, true>(jr.rx, srow, npx, npx_odd, code_mask, xodd, m1, m2);
-      else
-        screen_dispatch<1, false>(jr.rx, srow, npx, npx_odd, code_mask, 0, m1, m2);
-      // the y-pass screen only needs the winner's value to the screening
-      // accuracy; exact values are recomputed from xsv for y winners and ties
-      const int code = __float_as_int(m1) & 63;
-      int xi = code == 2 * jr.rx ? (xodd ? -jr.rx : jr.rx) : code - jr.rx + xodd;
-      if (m1 < NONE_BELOW) {  // no candidate inside the map: reference gives (-inf, -r)
-        xi = -jr.rx;
-        m1 = OUT_SENTINEL;
-      } else if (m2 >= m1 - jr.E2) {  // tie or near tie: exact rescan, reference order
-        xi = x_rescan(srow, npx, m1 - jr.E2, jr.rx, &sh.pj[buf]);
+    {  // in-map rows only, warp-strided
+      const int rb0 = r_lo + warp * rpw, step = PT_WARPS * rpw;
+      const float E2 = jr.E2;
+      if (pj.scale == 2) {  // even row base + 2*lane: pair alignment follows the shift parity
+        switch (jr.rx) {
+#define DPM_X_CASE(R) \
+  case R: x_rows<R, true>(sh, buf, srow0, rb0, r_hi, step, xsub, xc, code_mask, xodd, E2); break;
+          DPM_X_CASE(0) DPM_X_CASE(1) DPM_X_CASE(2) DPM_X_CASE(3) DPM_X_CASE(4) DPM_X_CASE(5)
+          DPM_X_CASE(6) DPM_X_CASE(7) DPM_X_CASE(8) DPM_X_CASE(9) DPM_X_CASE(10) DPM_X_CASE(11)
+          DPM_X_CASE(12) DPM_X_CASE(13) DPM_X_CASE(14) DPM_X_CASE(15) DPM_X_CASE(16)
+#undef DPM_X_CASE
+        }
+      } else {
+        switch (jr.rx) {
+#define DPM_X_CASE(R) \
+  case R: x_rows<R, false>(sh, buf, srow0, rb0, r_hi, step, xsub, xc, code_mask, 0, E2); break;
+          DPM_X_CASE(0) DPM_X_CASE(1) DPM_X_CASE(2) DPM_X_CASE(3) DPM_X_CASE(4) DPM_X_CASE(5)
+          DPM_X_CASE(6) DPM_X_CASE(7) DPM_X_CASE(8) DPM_X_CASE(9) DPM_X_CASE(10) DPM_X_CASE(11)
+          DPM_X_CASE(12) DPM_X_CASE(13) DPM_X_CASE(14) DPM_X_CASE(15) DPM_X_CASE(16)
+#undef DPM_X_CASE
+        }
       }
-      sh.x32[r * PT_W + xc] = m1;
-      sh.xsv[r * PT_W + xc] = srow[xi];
-      sh.xdx[r * PT_W + xc] = (int8_t)xi;
     }
     asm volatile("cp.async.wait_group 0;\n" ::);  // job p+1 (warp 0's copies)
     __syncthreads();  // x pass done: the band buffer is free for part p+1
