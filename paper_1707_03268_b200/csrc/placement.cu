@@ -44,6 +44,8 @@
 // with the same arithmetic.
 #include <math.h>
 
+#include <type_traits>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -572,40 +574,52 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
 
     // y pass for this thread's roots; exact values from the x winners
     const float* npy = sh.npy[buf] + RCAP;
+    // the radius switch sits outside the per-root loop (R compile-time inside)
+    auto y_roots = [&](auto rc) {
+      constexpr int R = decltype(rc)::value;
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      int iyr, ixr;
-      if (!root_of(k, iyr, ixr)) continue;
-      const int iy = ty0 + iyr, ix = tx0 + ixr;
-      const int ry = aj.ry0 + iy;
-      const int cy = pj.scale * ry + pj.ay;
-      const int cx = pj.scale * (aj.rx0 + ix) + pj.ax;
-      const int r0 = cy - yb0;  // band row of dy = 0
-      const float* xcol = sh.x32 + r0 * PT_W + ixr;
-      float m1, m2;
-      screen_dispatch<PT_W, false>(jr.ry, xcol, npy, npy, code_mask, 0, m1, m2);
-      auto exact = [&](int dy) -> double {
-        const int row = (r0 + dy) * PT_W + ixr;
-        const int dx = sh.xdx[row];
-        const double xv = __dadd_rn((double)sh.xsv[row], -pen(pj.cdx, pj.cdxx, dx));
-        return __dadd_rn(xv, -pen(pj.cdy, pj.cdyy, dy));
-      };
-      double best;
-      int bi = (__float_as_int(m1) & 63) - jr.ry;
-      if (m1 < NONE_BELOW) {
-        best = -INFINITY;
-        bi = -jr.ry;
-      } else if (m2 >= m1 - jr.E2) {
-        bi = y_rescan(xcol, sh.xsv + r0 * PT_W + ixr, sh.xdx + r0 * PT_W + ixr, npy, m1 - jr.E2,
-                      jr.ry, &sh.pj[buf], best);
-      } else {
-        best = exact(bi);
+      for (int k = 0; k < RPT; ++k) {
+        int iyr, ixr;
+        if (!root_of(k, iyr, ixr)) continue;
+        const int iy = ty0 + iyr, ix = tx0 + ixr;
+        const int ry = aj.ry0 + iy;
+        const int cy = pj.scale * ry + pj.ay;
+        const int cx = pj.scale * (aj.rx0 + ix) + pj.ax;
+        const int r0 = cy - yb0;  // band row of dy = 0
+        const float* xcol = sh.x32 + r0 * PT_W + ixr;
+        float m1, m2;
+        screen_window<R, PT_W, false>(xcol, npy, npy, code_mask, 0, m1, m2);
+        auto exact = [&](int dy) -> double {
+          const int row = (r0 + dy) * PT_W + ixr;
+          const int dx = sh.xdx[row];
+          const double xv = __dadd_rn((double)sh.xsv[row], -pen(pj.cdx, pj.cdxx, dx));
+          return __dadd_rn(xv, -pen(pj.cdy, pj.cdyy, dy));
+        };
+        double best;
+        int bi = (__float_as_int(m1) & 63) - R;
+        if (m1 < NONE_BELOW) {
+          best = -INFINITY;
+          bi = -R;
+        } else if (m2 >= m1 - jr.E2) {
+          bi = y_rescan(xcol, sh.xsv + r0 * PT_W + ixr, sh.xdx + r0 * PT_W + ixr, npy, m1 - jr.E2,
+                        R, &sh.pj[buf], best);
+        } else {
+          best = exact(bi);
+        }
+        const int bdx = sh.xdx[(r0 + bi) * PT_W + ixr];
+        tot[k] = __dadd_rn(tot[k], best);
+        const int o = (p * hr + iy) * wr + ix;
+        if (posb) posb[o] = pack_pos(cy + bi, cx + bdx);
+        if (placedb) placedb[o] = best;
       }
-      const int bdx = sh.xdx[(r0 + bi) * PT_W + ixr];
-      tot[k] = __dadd_rn(tot[k], best);
-      const int o = (p * hr + iy) * wr + ix;
-      if (posb) posb[o] = pack_pos(cy + bi, cx + bdx);
-      if (placedb) placedb[o] = best;
+    };
+    switch (jr.ry) {
+#define DPM_Y_CASE(R) \
+  case R: y_roots(std::integral_constant<int, R>{}); break;
+      DPM_Y_CASE(0) DPM_Y_CASE(1) DPM_Y_CASE(2) DPM_Y_CASE(3) DPM_Y_CASE(4) DPM_Y_CASE(5)
+      DPM_Y_CASE(6) DPM_Y_CASE(7) DPM_Y_CASE(8) DPM_Y_CASE(9) DPM_Y_CASE(10) DPM_Y_CASE(11)
+      DPM_Y_CASE(12) DPM_Y_CASE(13) DPM_Y_CASE(14) DPM_Y_CASE(15) DPM_Y_CASE(16)
+#undef DPM_Y_CASE
     }
   }
 
