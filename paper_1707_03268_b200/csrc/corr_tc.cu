@@ -87,6 +87,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (!done) asm volatile("trap;");
 }
 
+#ifdef DPM_TC_PROBE
+// MMA-warp wait cycles (debug builds only, tools/tc_probe.py): accumulator
+// free, input rows staged, output rows, total loop cycles
+__device__ unsigned long long dpm_tc_probe[4];
+#endif
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -349,6 +355,10 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       constexpr uint32_t LB4 = (2u * NMAX * 16u) >> 4;  // B tap stride (>> 4)
       constexpr uint32_t B2P = (2u * NMAX * 16u) >> 4;  // bf16 tap-pair block stride (>> 4)
       const uint32_t ring = (uint32_t)a.ring;
+#ifdef DPM_TC_PROBE
+      long long pr_empty = 0, pr_full = 0, pr_rows = 0;
+      const long long pr_t0 = clock64();
+#endif
       uint32_t qs = 0, qph = 0;    // ring slot / phase of the strip's input row 0
       uint32_t acc = 0, aph = 0;   // accumulator index / phase of the current output row
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
@@ -364,10 +374,21 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
             ph[i] = ph[i - 1];
             if (sl[i] == ring) { sl[i] = 0; ph[i] ^= 1; }
           }
+#ifdef DPM_TC_PROBE
+          const long long t0 = clock64();
+#endif
           mbar_wait(tempty + acc, aph ^ 1);
+#ifdef DPM_TC_PROBE
+          const long long t1 = clock64();
+          pr_empty += t1 - t0;
+#endif
 #pragma unroll
           for (int i = 0; i < FH; ++i)
             if (y == 0 || i == FH - 1) mbar_wait(full + sl[i], ph[i]);
+#ifdef DPM_TC_PROBE
+          pr_full += clock64() - t1;
+          pr_rows += 1;
+#endif
           tc_fence_after();
           const uint32_t d = tmem_base + acc * (uint32_t)a.acc_cols;
           // opaque per row: keeps the compiler from hoisting all FH*FW B
@@ -405,6 +426,14 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         for (int rr = ho; rr < job.H; ++rr)  // rows never first of an output row
           if (++qs == ring) { qs = 0; qph ^= 1; }
       }
+#ifdef DPM_TC_PROBE
+      if (lane == 0) {
+        atomicAdd(&dpm_tc_probe[0], (unsigned long long)pr_empty);
+        atomicAdd(&dpm_tc_probe[1], (unsigned long long)pr_full);
+        atomicAdd(&dpm_tc_probe[2], (unsigned long long)pr_rows);
+        atomicAdd(&dpm_tc_probe[3], (unsigned long long)(clock64() - pr_t0));
+      }
+#endif
     } else
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
@@ -813,3 +842,13 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
   DPM_LAUNCHED("corr_tc_kernel");
   return DPM_OK;
 }
+
+#ifdef DPM_TC_PROBE
+extern "C" int dpm_tc_probe_read(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, dpm_tc_probe, sizeof(unsigned long long) * 4);
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(dpm_tc_probe, z, sizeof(z));
+  return 0;
+}
+#endif
