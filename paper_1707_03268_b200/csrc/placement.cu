@@ -367,7 +367,7 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
                       dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   PlaceSmem& sh = *reinterpret_cast<PlaceSmem*>(smem_raw);
-  const int jid = find_job(ajobs, najobs, blockIdx.x);
+  const int jid = find_job_warp(ajobs, najobs, blockIdx.x);
   if (threadIdx.x == 0) sh.aj = ajobs[jid];
   __syncthreads();
   const dpm_asm_job& aj = sh.aj;

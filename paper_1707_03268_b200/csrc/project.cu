@@ -25,7 +25,7 @@ project_kernel(const float* __restrict__ X, float* __restrict__ P, const float* 
   float* sC = smem;                 // [L][Rp]
   float* sX = smem + L * Rp;        // [K1_CELLS][L+1]
 
-  const int jid = find_job(jobs, njobs, blockIdx.x);
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
   const dpm_proj_job job = jobs[jid];
   const int64_t ncells_level = (int64_t)job.H * job.W;
   const int64_t cell0 = (int64_t)(blockIdx.x - job.block0) * K1_CELLS;

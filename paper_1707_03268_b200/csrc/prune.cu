@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(256)
 prune_ranks_kernel(const float* __restrict__ S, const int64_t* __restrict__ map_offs,
                    const double* __restrict__ thr, const dpm_prune_job* __restrict__ jobs,
                    int njobs, uint8_t* __restrict__ out) {
-  const int jid = find_job(jobs, njobs, blockIdx.x);
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
   const dpm_prune_job j = jobs[jid];
   const int hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
   const int64_t e = (int64_t)(blockIdx.x - j.block0) * 256 + threadIdx.x;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256)
 mixture_max_kernel(const double* __restrict__ total, const dpm_asm_job* __restrict__ ajobs,
                    const int32_t* __restrict__ members, const dpm_mix_job* __restrict__ jobs,
                    int njobs, double* __restrict__ best, int32_t* __restrict__ comp) {
-  const int jid = find_job(jobs, njobs, blockIdx.x);
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
   const dpm_mix_job j = jobs[jid];
   const int hu = j.ry1 - j.ry0 + 1, wu = j.rx1 - j.rx0 + 1;
   const int64_t e = (int64_t)(blockIdx.x - j.block0) * 256 + threadIdx.x;
