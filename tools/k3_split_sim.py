@@ -2,8 +2,8 @@
 
     python tools/k3_split_sim.py [part level]   (default 0: 180 x 320, config 4 image 0)
 
-For the part maps of one config-4 component (float64 oracle maps of the real
-filters and factors) and the kernel's radius r* + 1, counts the fraction of
+For the part maps of one config-4 component (float64 maps of the real
+filters and factors, computed here with numpy) and the kernel's radius r* + 1, counts the fraction of
 warps (32 centres two columns apart in the x pass; 32 root columns of one
 root row in the y pass) for which the inner window |d| <= r1 does NOT prove
 that every outer candidate loses: max over the band row (x) or column (y)
@@ -18,8 +18,23 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
-from oracle import dpm_oracle as O  # noqa: E402  (analysis tool, not product code)
 from paper_1707_03268_b200 import synth  # noqa: E402
+
+
+def correlate(P, core):
+    """Valid correlation of a projected level (H, W, R) with a core (h, w, R), float64."""
+    h, w, _ = core.shape
+    H, W, _ = P.shape
+    out = np.zeros((H - h + 1, W - w + 1))
+    for i in range(h):
+        for j in range(w):
+            out += P[i:i + H - h + 1, j:j + W - w + 1] @ core[i, j]
+    return out
+
+
+def r_star(S, a):
+    """SURVEY.md App. A.2 radius for a pure quadratic penalty a*d^2 on both axes."""
+    return int(np.floor(np.sqrt(4 * a * float(S.max() - S.min())) / (2 * a)))
 
 
 def main():
@@ -35,12 +50,13 @@ def main():
         return G[offs[f]:offs[f] + h * w].reshape(h, w, -1)
 
     H, W = wl.pyramid.levels[lev]
-    P = O.project(synth.hog_level(4, 0, lev, H, W), fx["C"])
+    X = synth.hog_level(4, 0, lev, H, W).astype(np.float64)
+    P = X @ fx["C"].astype(np.float64)
     a = 0.01
     xs, ys = {}, {}
     for f in bank.components[0].parts[:3]:
-        S = O.correlate3_full(P, core(f))
-        R = O.r_star(S, (0, 0, a, a)) + 1
+        S = correlate(P, core(f).astype(np.float64))
+        R = r_star(S, a) + 1
         Hs, Ws = S.shape
         pad = np.full((Hs, Ws + 2 * R), -np.inf)
         pad[:, R:R + Ws] = S
