@@ -205,7 +205,9 @@ typedef struct {
 } dpm_detection;
 
 /* Validates both tables (host memory), fills block0 of the assembly jobs and
- * returns the CTA count to pass to dpm_assemble. */
+ * returns the CTA count to pass to dpm_assemble.  One job's outputs
+ * (nparts x hr x wr) must stay below 2^31 elements (32-bit offsets inside a
+ * job); larger rectangles are split by the caller. */
 int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs, const dpm_place_job* pjobs_host,
                              int npjobs);
 
