@@ -94,6 +94,13 @@ def test_prepare_validates_and_numbers_blocks():
         _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1))
     aj["rx1"] = 4
     assert lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1) == 1
+    # one job's outputs must fit 32-bit offsets (nparts x hr x wr < 2^31)
+    big_pj = np.repeat(pj, 8)
+    big_pj["wr"] = 50000
+    big = aj.copy()
+    big["ry1"], big["rx1"], big["nparts"] = 6000 - 1, 50000 - 1, 8
+    with pytest.raises(Exception, match="exceed 2\\^31"):
+        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(big), 1, _lib.table_ptr(big_pj), 8))
 
 
 def test_tile_shapes():
