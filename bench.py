@@ -1,28 +1,37 @@
 """Benchmark of the DPM score path (BASELINE.json metric) on B200.
 
-Workload (config 4): 64 seeded 1280x720 images (HOG pyramids, 49 levels,
-441,041 cells x 32 ch each), the 54-filter model (3 mirrored pairs of a
-6x11 root + 8 parts 6x6 one octave finer) on a shared rank-8 basis from the
-reference's cp_als, unbounded GDT placement, root + parts assembly and tau
-compaction.  A step scores the whole 64-image batch (sharded 64/N over N
-GPUs, one process per GPU; the only collective is the final detection
+Default workload (config 4): 64 seeded 1280x720 images (HOG pyramids, 49
+levels, 441,041 cells x 32 ch each), the 54-filter model (3 mirrored pairs
+of a 6x11 root + 8 parts 6x6 one octave finer) on a shared rank-8 basis from
+the reference's cp_als, unbounded GDT placement, root + parts assembly and
+tau compaction.  A step scores the whole 64-image batch, sharded 64/N over N
+GPUs (one process per GPU; the only collective is the final detection
 gather).  Metric: cell x filter evaluations per second (20,013,786 per
-image); images/s alongside.
+image); images/s alongside.  ``--config`` / ``--rank`` / ``--basis`` select
+the other BASELINE.json configs (2: 640x480, R in {4, 8, 16, 32}; 3: the
+1080-filter bank at R = 16; 5: 1920x1080 with roots up to 15x15, R in
+{8, 32} or the dense 32-channel filters), each through the same full path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W]          # this repo
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C --rank R]
   python bench.py --impl reference [--steps K] [--warmup W]    # CPU reference arm
 
-Timing: CUDA events on the launching stream, barrier + synchronize on both
-sides, max over ranks.  The device-resident inputs (3.6 GB at N=1) exceed
-the 126 MB L2, so no explicit flush is needed between steps.
+``--gpus N`` without torchrun re-launches itself under
+``torch.distributed.run`` with N ranks (127.0.0.1); under torchrun the
+ranks come from the environment.  Timing: CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks.  Inputs larger
+than the 126 MB L2 need no flush; smaller ones (configs 1-3, 5) get a 512 MB
+write between timed steps, outside the timed windows.
 """
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -31,41 +40,41 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-CFG = 4
-N_IMAGES = 64
-RANK = 8
 METRIC = "DPM cell*filter evals/s (decomposed conv + GDT + assembly)"
 UNIT = "evals/s"
+DEFAULT_IMAGES = {1: 1, 2: 1, 3: 1, 4: 64, 5: 1}
+L2_BYTES = 126 << 20
+
+
+# ---------------------------------------------------------------- workload
+
+def _factors(wl, cfg, rank, basis):
+    """(C, stacked G) of the bench model: the committed cp_als factors of the
+    shared basis, or the dense filters over the identity basis."""
+    if basis == "dense":
+        C = np.eye(32, dtype=np.float32)
+        G = np.concatenate([np.asarray(f, np.float32).reshape(-1, 32) for f in wl.bank.filters])
+        return C, G
+    fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg{cfg}_R{rank}.npz"))
+    return fx["C"], fx["G"]
+
+
+def _describe(cfg, wl, rank, basis, images):
+    hw = wl.image_hw
+    nf = len(wl.bank.filters)
+    basis_s = "dense 32-channel filters (identity basis)" if basis == "dense" else f"shared rank-{rank} basis"
+    return (f"config {cfg}: {images} x {hw[1]}x{hw[0]} HOG pyramid(s) ({len(wl.pyramid.levels)} levels, "
+            f"{wl.pyramid.n_cells} cells x 32 ch each), {nf} filters in {len(wl.bank.components)} "
+            f"components, {basis_s}, unbounded GDT (r*) + assembly + tau compaction")
 
 
 # ---------------------------------------------------------------- CPU leg
 
-def _cpu_task(task):
-    """One (image, root level, component) of config 4 through the oracle:
-    project, correlate root + parts (reference correlate3_full on the
-    projected level), place parts with r* and gather, assemble."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    from oracle import dpm_oracle as O
-    from paper_1707_03268_b200 import synth
-
-    img, i, ci = task
-    wl = _cpu_task.wl
-    C, cores = _cpu_task.C, _cpu_task.cores
-    pyr, bank = wl.pyramid, wl.bank
-    kr, kp = pyr.root_levels[i], pyr.part_levels[i]
-    lv = [np.zeros((1, 1, 32), np.float32)] * len(pyr.levels)
-    lv = list(lv)
-    lv[kr] = synth.hog_level(CFG, img, kr, *pyr.levels[kr])
-    lv[kp] = synth.hog_level(CFG, img, kp, *pyr.levels[kp])
-    t0 = time.perf_counter()
-    res, maps = O.score_pyramid(lv, bank, C, cores, root_levels=[kr], part_levels=[kp],
-                                components=[bank.components[ci]])
-    dt = time.perf_counter() - t0
-    evals = sum(m.size for m in maps.values())
-    return evals, dt
+class _CpuState:
+    pass
 
 
-def _cpu_init():
+def _cpu_init(cfg, rank, basis):
     os.environ["OMP_NUM_THREADS"] = "1"
     try:
         from threadpoolctl import threadpool_limits
@@ -76,29 +85,69 @@ def _cpu_init():
     from paper_1707_03268_b200 import synth
     from paper_1707_03268_b200.pipeline import cores_from_stacked
 
-    wl = synth.workload(CFG)
-    fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg{CFG}_R{RANK}.npz"))
-    _cpu_task.wl = wl
-    _cpu_task.C = fx["C"]
-    _cpu_task.cores = cores_from_stacked(wl.bank, fx["G"])
+    wl = synth.workload(cfg)
+    C, G = _factors(wl, cfg, rank, basis)
+    _CpuState.wl, _CpuState.C = wl, C
+    _CpuState.cores = cores_from_stacked(wl.bank, G)
+    _CpuState.maps = {}
 
 
-def _cpu_sample_tasks(image, n_root, stride=1):
-    # biggest levels first so the pool's tail is short
-    return [(image, i, c) for i in range(0, n_root, stride) for c in range(6)]
+def _cpu_task(task):
+    """One (image, root level, component) through the oracle: project,
+    correlate root + parts (reference correlate3_full on the projected
+    level), place parts with r* and gather, assemble.  The image's levels
+    were synthesised before the timed region into a memory-mapped file."""
+    from oracle import dpm_oracle as O
+
+    path, offs, i, ci = task
+    wl = _CpuState.wl
+    pyr, bank = wl.pyramid, wl.bank
+    if path not in _CpuState.maps:
+        _CpuState.maps[path] = np.load(path, mmap_mode="r")
+    arena = _CpuState.maps[path]
+    kr, kp = pyr.root_levels[i], pyr.part_levels[i]
+    lv = [np.zeros((1, 1, 32), np.float32)] * len(pyr.levels)
+    for k in {kr, kp}:
+        H, W = pyr.levels[k]
+        lv[k] = np.asarray(arena[offs[k]:offs[k] + H * W * 32]).reshape(H, W, 32)
+    t0 = time.perf_counter()
+    res, maps = O.score_pyramid(lv, bank, _CpuState.C, _CpuState.cores, root_levels=[kr],
+                                part_levels=[kp], components=[bank.components[ci]])
+    dt = time.perf_counter() - t0
+    return sum(m.size for m in maps.values()) if res else 0, dt
 
 
-def cpu_run(tasks, workers):
-    """Wall time of ``tasks`` on a spawn pool of ``workers`` processes."""
+def _cpu_write_image(cfg, wl, image, tmpdir):
+    """Synthesise one image's pyramid (outside any timed region) into a .npy
+    the pool workers memory-map; returns (path, level offsets)."""
+    from paper_1707_03268_b200 import synth
+
+    levels = synth.hog_pyramid(cfg, image, wl.pyramid)
+    offs, o = [], 0
+    for lv in levels:
+        offs.append(o)
+        o += lv.size
+    path = os.path.join(tmpdir, f"img{image}.npy")
+    np.save(path, np.concatenate([lv.ravel() for lv in levels]))
+    return path, tuple(offs)
+
+
+def _cpu_tasks(wl, path, offs, max_tasks=None):
+    pyr = wl.pyramid
+    tasks = [(path, offs, i, c) for i in range(len(pyr.root_levels))
+             for c in range(len(wl.bank.components))]
+    if max_tasks is not None and len(tasks) > max_tasks:
+        # a seeded, level-stratified sample (the metric is a per-eval rate)
+        rng = np.random.default_rng(0)
+        tasks = [tasks[j] for j in sorted(rng.choice(len(tasks), max_tasks, replace=False))]
+    return tasks
+
+
+def _cpu_pool(args, workers):
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
-    with ctx.Pool(workers, initializer=_cpu_init) as pool:
-        pool.map(_cpu_task, tasks[:workers], chunksize=1)  # warm the workers
-        t0 = time.perf_counter()
-        out = pool.map(_cpu_task, tasks, chunksize=1)
-        wall = time.perf_counter() - t0
-    return sum(e for e, _ in out), wall
+    return ctx.Pool(workers, initializer=_cpu_init, initargs=(args.config, args.rank, args.basis))
 
 
 # ---------------------------------------------------------------- clocks
@@ -116,8 +165,9 @@ class ClockSampler:
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
                ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
-    def __init__(self, device_index):
+    def __init__(self, device_index, enabled=True):
         self.index = int(device_index)
+        self.enabled = enabled
         self.rows = []  # (sm_mhz, max_mhz, reason names)
         self.proc = None
         self.nvml = None
@@ -135,6 +185,8 @@ class ClockSampler:
         return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             nv, h = self._nvml_handle()
             smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
@@ -200,14 +252,157 @@ class ClockSampler:
                 "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
-# ---------------------------------------------------------------- helpers
+# ---------------------------------------------------------------- ranks
 
-def _dist():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
+
+def self_launch(n):
+    """Re-run this script under torch.distributed.run with ``n`` ranks on
+    this node (rendezvous on 127.0.0.1); returns its exit code."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines name nranks
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+class CpuEvent:
+    """torch.cuda.Event stand-in for the CPU harness test (--stub)."""
+
+    def __init__(self, **_):
+        self.t = None
+
+    def record(self, stream=None):
+        self.t = time.perf_counter()
+
+    def elapsed_time(self, other):
+        return 1e3 * (other.t - self.t)
+
+
+class Ranks:
+    """One process per GPU: rank / world from the torchrun environment, the
+    process group (NCCL on the GPU, gloo for the CPU harness test), barrier,
+    max over ranks and the detection gather."""
+
+    def __init__(self, stub=False):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.stub = torch, dist, stub
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # under torchrun the process group is used even at world size 1, so the
+        # one-GPU launch exercises the same barrier / max / gather path as N > 1
+        self.on = self.world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+        if stub:
+            self.device = torch.device("cpu")
+            if self.on:
+                dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(self.local)
+            self.device = torch.device("cuda", self.local)
+            if self.on:
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                dist.init_process_group("nccl", device_id=self.device)
+
+    def event(self):
+        return CpuEvent() if self.stub else self.torch.cuda.Event(enable_timing=True)
+
+    def sync(self):
+        if not self.stub:
+            self.torch.cuda.synchronize()
+
+    def barrier(self):
+        if self.on:
+            self.dist.barrier()
+        self.sync()
+
+    def max(self, x):
+        if not self.on:
+            return x
+        t = self.torch.tensor([x], device=self.device, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def broadcast(self, x):
+        if not self.on:
+            return x
+        t = self.torch.tensor([x], device=self.device, dtype=self.torch.float64)
+        self.dist.broadcast(t, 0)
+        return float(t.item())
+
+    def gather(self, dets):
+        if not self.on:
+            return dets
+        from paper_1707_03268_b200.dist import gather_detections
+
+        return gather_detections(dets, device=self.device)
+
+    def close(self):
+        if self.on:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- stub scorer
+
+def stub_detections(image):
+    """Deterministic detection records of one image (CPU harness test)."""
+    from paper_1707_03268_b200._lib import DETECTION
+
+    n = 1 + image % 3
+    d = np.zeros(n, dtype=DETECTION)
+    d["image"] = image
+    d["level"] = np.arange(n)
+    d["score"] = image + 0.25 * np.arange(n)
+    return d
+
+
+class StubScorer:
+    """Stands in for PyramidScorer in ``--stub`` runs: the harness (ranks,
+    sharding, timing, gather, JSON line) without a GPU."""
+
+    class _Plan:
+        def __init__(self, torch):
+            self.X = torch.zeros(16)
+
+        def run(self, tau=None, mark=None, **_):
+            mark = mark or (lambda n: None)
+            mark("stub_step")
+            time.sleep(0.002)
+            mark(None)
+
+        def launches_per_run(self):
+            return 0
+
+    def __init__(self, torch, images):
+        self.images = list(images)
+        self.plan = self._Plan(torch)
+        self.n_images = len(self.images)
+        self.torch = torch
+
+    def host_arena(self, pinned=False):
+        return self.torch.zeros(16)
+
+    def score_batch(self, host, tau, chunk_images=2):
+        from paper_1707_03268_b200._lib import DETECTION
+
+        recs = [stub_detections(i) for i in self.images]
+        return np.concatenate(recs) if recs else np.zeros(0, dtype=DETECTION)
+
+    def evals_per_image(self):
+        return 1000
+
+    def h2d_bytes(self):
+        return 0
+
+
+# ---------------------------------------------------------------- our arm
 
 def _peaks():
     try:
@@ -219,7 +414,8 @@ def _peaks():
 
 def _traffic(images):
     """DRAM bytes per launch (scaled to `images`) from the committed ncu --set full
-    summary (profiles/kernel_traffic.json, written by tools/ncu_summary.py)."""
+    summary (profiles/kernel_traffic.json, written by tools/ncu_summary.py);
+    only for the config it was captured on (config 4)."""
     try:
         with open(os.path.join(REPO, "profiles", "kernel_traffic.json")) as fh:
             per_image = json.load(fh)["per_image"]
@@ -228,117 +424,22 @@ def _traffic(images):
     return {k: v * images for k, v in per_image.items()}
 
 
-# ---------------------------------------------------------------- our arm
-
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    from paper_1707_03268_b200 import synth
-    from paper_1707_03268_b200.dist import gather_detections, shard
-    from paper_1707_03268_b200.pipeline import PyramidScorer
-
-    world, rank, local = _dist()
-    torch.cuda.set_device(local)
-    # under torchrun the process group is used even at world size 1, so the
-    # one-GPU launch exercises the same barrier / max / gather path as N > 1
-    dist_on = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
-    if dist_on:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    wl = synth.workload(CFG)
-    fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg{CFG}_R{RANK}.npz"))
-    mine = list(shard(args.images, world, rank))
-    n = len(mine)
-    sc = PyramidScorer(wl.bank, fx["C"], fx["G"], wl.pyramid, n_images=n,
-                       outputs=("totals", "positions"), max_dets=args.max_dets,
-                       envelope=args.k3 == "envelope")
-    plan = sc.plan
-    host = sc.host_arena(pinned=True)
-    for j, img in enumerate(mine):
-        sc.fill_host(host, j, synth.hog_pyramid(CFG, img, wl.pyramid))
-    plan.X.copy_(host)
-    stream = torch.cuda.current_stream()
-
-    # tau: keep ~0.1% of roots (calibrated once on this rank's first image)
+def _calibrate_tau(plan):
+    """tau keeping ~0.1% of roots (from this rank's first image)."""
     plan.run()
-    torch.cuda.synchronize()
+    plan.torch.cuda.synchronize()
     tot = np.concatenate([plan.assembly_outputs(0, a)["totals"].cpu().numpy().ravel()
                           for a in range(len(plan.assemblies))])
-    tau = float(np.quantile(tot, 0.999)) if args.tau is None else args.tau
-    if dist_on:
-        t = torch.tensor([tau], device="cuda", dtype=torch.float64)
-        dist.broadcast(t, 0)
-        tau = float(t.item())
+    return float(np.quantile(tot, 0.999)) if tot.size else 0.0
 
-    def barrier():
-        if dist_on:
-            dist.barrier()
-        torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        if not dist_on:
-            return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    for _ in range(args.warmup):
-        plan.run(tau=tau)
-    barrier()
-
-    # ---- device-resident timing (value); per-kernel shares via events recorded
-    # on the launching stream between launches
-    marks = []
-
-    def mark(name):
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(stream)
-        marks[-1].append((name, ev))
-
-    with ClockSampler(local) as clocks:
-        barrier()
-        for _ in range(args.steps):
-            marks.append([])
-            plan.run(tau=tau, mark=mark)
-        barrier()
-    step_ms = [m[0][1].elapsed_time(m[-1][1]) for m in marks]
-    kernel_ms = {}
-    for m in marks:
-        for (name, ev), (_, ev2) in zip(m[:-1], m[1:]):
-            kernel_ms[name] = kernel_ms.get(name, 0.0) + ev.elapsed_time(ev2) / args.steps
-    total_ms = max_over_ranks(sum(step_ms))
-    ms_per_step = total_ms / args.steps
-
-    evals_img = sc.evals_per_image()
-    evals_step = evals_img * args.images
-    value = evals_step * args.steps / (total_ms / 1e3)
-    images_s = args.images * args.steps / (total_ms / 1e3)
-
-    # ---- end to end through the public API: pinned H2D + run + D2H detections
-    for _ in range(max(1, args.warmup // 2)):
-        sc.score_batch(host, tau, chunk_images=args.chunk)
-    barrier()
-    e2e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    ndets = []
-    with ClockSampler(local) as clocks_e2e:
-        barrier()
-        e2e_ev[0].record(stream)
-        for _ in range(args.steps):
-            d = sc.score_batch(host, tau, chunk_images=args.chunk)
-            if dist_on:
-                d = gather_detections(d, device="cuda")
-            ndets.append(len(d))
-        e2e_ev[1].record(stream)
-        barrier()
-    e2e_ms = max_over_ranks(e2e_ev[0].elapsed_time(e2e_ev[1]))
-    e2e_value = evals_step * args.steps / (e2e_ms / 1e3)
-    from paper_1707_03268_b200._lib import DETECTION
-    d2h = 4 + int(statistics.mean(ndets)) * DETECTION.itemsize
-
-    # ---- FFMA peak probe (context for the FFMA launches' denominator)
-    from paper_1707_03268_b200 import _lib
+def _ffma_probe(stream):
+    """Measured FP32 FFMA rate (context for the FFMA launches' denominator)."""
     import ctypes
+
+    import torch
+
+    from paper_1707_03268_b200 import _lib
 
     sink = torch.zeros(148 * 16, device="cuda")
     flops = ctypes.c_double(0)
@@ -350,19 +451,26 @@ def run_ours(args):
         lib.dpm_ffma_probe(sink.data_ptr(), 2048, ctypes.byref(flops), stream.cuda_stream)
     pe[1].record(stream)
     torch.cuda.synchronize()
-    probe_tflops = 5 * flops.value / (pe[0].elapsed_time(pe[1]) / 1e3) / 1e12
+    return 5 * flops.value / (pe[0].elapsed_time(pe[1]) / 1e3) / 1e12
 
+
+def _rooflines(plan, n, kernel_ms, stream, traffic_ok):
+    """Per-stage rooflines (SURVEY.md §8(d) algorithmic work per launch over
+    the launch's CUDA-event time) and the dominant one."""
+    probe_tflops = _ffma_probe(stream)
     peaks = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
     bf16 = float(peaks.get("bf16_tflops", 1590.0))
-    tc_peak = bf16 / 2.0 / 3.0  # tf32 = half the bf16 rate; 3xTF32 = 3 MMA passes per MAC
+    # the tcgen05 K2 issues two tf32 MMA passes (N doubled: [B_hi | B_lo])
+    # plus a bf16 correction pass (A_lo * B_hi) at twice the tf32 rate: 2.5
+    # tf32-equivalent passes per MAC
+    tc_peak = bf16 / 2.0 / 2.5
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = _traffic(n)
+    traffic = _traffic(n) if traffic_ok else {}
 
-    launch_flops = plan.launch_flops()
     k2 = []
-    for name, fl in launch_flops.items():
+    for name, fl in plan.launch_flops().items():
         ms = kernel_ms.get(name)
         if not ms:
             continue
@@ -370,7 +478,8 @@ def run_ours(args):
         k2.append({"kernel": name, "ms": ms, "algorithmic_flops": fl,
                    "achieved_tflops": fl / (ms / 1e3) / 1e12, "peak_tflops": pk,
                    "frac": fl / (ms / 1e3) / 1e12 / pk,
-                   "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 3 (3xTF32 passes)"
+                   "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (tf32) / 2.5 "
+                                   "(2 tf32 passes + 1 bf16 correction pass per MAC)"
                                    if "tcgen05" in name else
                                    f"148 SMs x 128 FFMA x 2 x {sm_max:.0f} MHz (sm_max_mhz)")})
     k2_ms = sum(d["ms"] for d in k2)
@@ -378,16 +487,19 @@ def run_ours(args):
     k2_roof_ms = sum(d["algorithmic_flops"] / (d["peak_tflops"] * 1e12) * 1e3 for d in k2)
 
     # K3/K4 algorithmic bytes: 12 B per part-map cell (read S,
-    # write D and the packed argmax) + 4*(2 + 2*n_parts) B per root eval
-    part_cells, root_evals = 0, 0
+    # write D and the packed argmax) + 4*(2 + 2*n_parts) B per root eval.  The
+    # fused kernel's own bytes (it never writes D): 4 B per part-map cell read
+    # + 8 B total + 4 B per part position per root.
+    part_cells, root_evals, root_parts = 0, 0, 0
     for a in plan.assemblies:
         hr, wr = a.rect[1] - a.rect[0] + 1, a.rect[3] - a.rect[2] + 1
         root_evals += hr * wr
+        root_parts += hr * wr * len(a.parts)
         for p in a.parts:
-            part_cells += plan.map_shape[(p.level, p.filt)][0] * plan.map_shape[(p.level, p.filt)][1]
+            ho, wo = plan.map_shape[(p.level, p.filt)]
+            part_cells += ho * wo
     k34_bytes = n * (12 * part_cells + 4 * (2 + 2 * 8) * root_evals)
-    # K3/K4 = the lower-envelope GDT pair (x pass, y pass + assembly) and/or
-    # the windowed kernel, whichever the plan launched
+    k34_fused_bytes = n * (4 * part_cells + 8 * root_evals + 4 * root_parts)
     k34_parts = {k: v for k, v in kernel_ms.items() if k.startswith("k3")}
     k34_ms = sum(k34_parts.values())
     k34_traffic = [traffic.get(k) for k in ("gdt_x_kernel", "gdt_y_kernel")
@@ -397,26 +509,28 @@ def run_ours(args):
     k34_traffic = (sum(k34_traffic) if k34_traffic and None not in k34_traffic else None)
     k1_bytes = n * plan.k1_bytes()
     k1_ms = kernel_ms.get("k1_project", 0.0)
+    gbs = lambda b, ms: b / (ms / 1e3) / 1e9 if ms else 0.0  # noqa: E731
     rooflines = {
-        "k3k4_place_assemble": {"bound": "hbm", "achieved": k34_bytes / (k34_ms / 1e3) / 1e9,
-                                "peak": hbm, "unit": "GB/s",
-                                "frac": k34_bytes / (k34_ms / 1e3) / 1e9 / hbm,
+        "k3k4_place_assemble": {"bound": "hbm", "achieved": gbs(k34_bytes, k34_ms),
+                                "peak": hbm, "unit": "GB/s", "frac": gbs(k34_bytes, k34_ms) / hbm,
                                 "algorithmic_bytes_per_launch": k34_bytes,
-                                "launch_ms": k34_parts,
-                                "traffic": k34_traffic},
-        "k2_correlate": {"bound": "tensor", "achieved": k2_flops / (k2_ms / 1e3) / 1e12,
-                         "ffma_roofline_frac": k2_flops / (k2_ms / 1e3) / 1e12 / ffma_peak,
-                         "peak": k2_flops / (k2_roof_ms / 1e3) / 1e12, "unit": "TFLOP/s",
-                         "frac": k2_roof_ms / k2_ms,
+                                "fused_kernel_bytes_per_launch": k34_fused_bytes,
+                                "fused_frac": gbs(k34_fused_bytes, k34_ms) / hbm,
+                                "launch_ms": k34_parts, "traffic": k34_traffic},
+        "k2_correlate": {"bound": "tensor", "achieved": k2_flops / (k2_ms / 1e3) / 1e12 if k2_ms else 0.0,
+                         "ffma_roofline_frac": (k2_flops / (k2_ms / 1e3) / 1e12 / ffma_peak
+                                                if k2_ms else 0.0),
+                         "peak": k2_flops / (k2_roof_ms / 1e3) / 1e12 if k2_roof_ms else 0.0,
+                         "unit": "TFLOP/s", "frac": k2_roof_ms / k2_ms if k2_ms else 0.0,
                          "algorithmic_flops_per_launch": k2_flops, "launches": k2,
-                         "note": "peak = per-launch roofline mix: tcgen05 3xTF32 launches vs the "
-                                 "tf32 rate / 3, FFMA launches vs the FP32 FFMA rate",
+                         "note": "peak = per-launch roofline mix: tcgen05 launches vs the "
+                                 "tf32 rate / 2.5, FFMA launches vs the FP32 FFMA rate",
                          "ffma_probe_tflops": probe_tflops,
                          "traffic": (traffic["corr_tc_kernel"] + traffic["corr_kernel"]
                                      if "corr_tc_kernel" in traffic and "corr_kernel" in traffic
                                      else None)},
-        "k1_project": {"bound": "hbm", "achieved": k1_bytes / (k1_ms / 1e3) / 1e9, "peak": hbm,
-                       "unit": "GB/s", "frac": k1_bytes / (k1_ms / 1e3) / 1e9 / hbm,
+        "k1_project": {"bound": "hbm", "achieved": gbs(k1_bytes, k1_ms), "peak": hbm,
+                       "unit": "GB/s", "frac": gbs(k1_bytes, k1_ms) / hbm,
                        "algorithmic_bytes_per_launch": k1_bytes,
                        "traffic": traffic.get("project_kernel")},
     }
@@ -425,88 +539,220 @@ def run_ours(args):
     roofline = dict(rooflines[dominant], kernel=dominant,
                     peak_source="MEASURED_PEAKS.json" if rooflines[dominant]["bound"] == "hbm"
                     else "derived from MEASURED_PEAKS.json / FFMA rate (see launches)")
+    return roofline, rooflines
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        tasks = [t for img in range(3)
-                 for t in _cpu_sample_tasks(image=img, n_root=len(wl.pyramid.root_levels))]
+
+def _cpu_baseline(args, wl):
+    """The oracle port on the host cores, on a bounded sample of the same
+    workload (rank 0, N = 1 only)."""
+    n_img = 3 if args.config == 4 else 1
+    with tempfile.TemporaryDirectory(prefix="dpm_cpu_") as tmp:
+        tasks = []
+        for img in range(n_img):
+            path, offs = _cpu_write_image(args.config, wl, img, tmp)
+            tasks += _cpu_tasks(wl, path, offs, max_tasks=None if args.config in (1, 2, 4) else 96)
         workers = min(os.cpu_count() or 1, len(tasks))
-        evals, wall = cpu_run(tasks, workers)
-        cpu = {"value": evals / wall, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": f"three full images of config {CFG} ({len(tasks)} (root level, component) "
-                         f"tasks, {evals} evals) on a {workers}-process pool running the numpy "
-                         f"oracle (reference algorithm restated); {wall:.1f} s wall"}
+        with _cpu_pool(args, workers) as pool:
+            pool.map(_cpu_task, tasks[:workers], chunksize=1)  # warm the workers
+            t0 = time.perf_counter()
+            out = pool.map(_cpu_task, tasks, chunksize=1)
+            wall = time.perf_counter() - t0
+    evals = sum(e for e, _ in out)
+    return {"value": evals / wall, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"{n_img} image(s) of config {args.config} ({len(tasks)} (root level, component) "
+                      f"tasks, {evals} evals; levels synthesised before the timed region) on a "
+                      f"{workers}-process pool running the numpy oracle (reference algorithm "
+                      f"restated); {wall:.1f} s wall"}
 
-    if rank == 0:
+
+def run_ours(args):
+    import torch
+
+    from paper_1707_03268_b200 import synth
+    from paper_1707_03268_b200.dist import shard
+
+    rk = Ranks(stub=args.stub)
+    if rk.world != args.gpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={rk.world}")
+    mine = list(shard(args.images, rk.world, rk.rank))
+    n = len(mine)
+    wl = None
+    if args.stub:
+        sc = StubScorer(torch, mine)
+        stream = None
+    else:
+        from paper_1707_03268_b200.pipeline import PyramidScorer
+
+        wl = synth.workload(args.config)
+        C, G = _factors(wl, args.config, args.rank, args.basis)
+        sc = PyramidScorer(wl.bank, C, G, wl.pyramid, n_images=n,
+                           outputs=("totals", "positions"), max_dets=args.max_dets,
+                           envelope=args.k3 == "envelope")
+        host = sc.host_arena(pinned=True)
+        for j, img in enumerate(mine):
+            sc.fill_host(host, j, synth.hog_pyramid(args.config, img, wl.pyramid))
+        sc.plan.X.copy_(host)
+        stream = torch.cuda.current_stream()
+    if args.stub:
+        host = sc.host_arena()
+    plan = sc.plan
+
+    tau = (0.0 if args.stub else _calibrate_tau(plan)) if args.tau is None else args.tau
+    tau = rk.broadcast(tau)
+    x_bytes = 0 if args.stub else plan.X.numel() * 4
+    flush = None
+    if not args.stub and x_bytes < 4 * L2_BYTES:
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=rk.device)
+
+    for _ in range(args.warmup):
+        plan.run(tau=tau)
+    rk.barrier()
+
+    # ---- device-resident timing (value); per-kernel shares via events recorded
+    # on the launching stream between launches
+    marks = []
+
+    def mark(name):
+        ev = rk.event()
+        ev.record(stream)
+        marks[-1].append((name, ev))
+
+    with ClockSampler(rk.local, enabled=not args.stub) as clocks:
+        rk.barrier()
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)  # between timed windows: L2 holds no input
+            marks.append([])
+            plan.run(tau=tau, mark=mark)
+        rk.barrier()
+    step_ms = [m[0][1].elapsed_time(m[-1][1]) for m in marks]
+    kernel_ms = {}
+    for m in marks:
+        for (name, ev), (_, ev2) in zip(m[:-1], m[1:]):
+            kernel_ms[name] = kernel_ms.get(name, 0.0) + ev.elapsed_time(ev2) / args.steps
+    total_ms = rk.max(sum(step_ms))
+    ms_per_step = total_ms / args.steps
+
+    evals_img = sc.evals_per_image()
+    evals_step = evals_img * args.images
+    value = evals_step * args.steps / (total_ms / 1e3)
+    images_s = args.images * args.steps / (total_ms / 1e3)
+
+    # ---- end to end through the public API: pinned H2D + run + D2H detections,
+    # gathered over the ranks (the path's only collective)
+    for _ in range(max(1, args.warmup // 2)):
+        sc.score_batch(host, tau, chunk_images=args.chunk)
+    rk.barrier()
+    e2e_ev = [rk.event() for _ in range(2)]
+    ndets, nmine, gathered = [], [], None
+    with ClockSampler(rk.local, enabled=not args.stub) as clocks_e2e:
+        rk.barrier()
+        e2e_ev[0].record(stream)
+        for _ in range(args.steps):
+            d = sc.score_batch(host, tau, chunk_images=args.chunk)
+            nmine.append(len(d))
+            gathered = rk.gather(d)
+            ndets.append(len(gathered))
+        e2e_ev[1].record(stream)
+        rk.barrier()
+    e2e_ms = rk.max(e2e_ev[0].elapsed_time(e2e_ev[1]))
+    e2e_value = evals_step * args.steps / (e2e_ms / 1e3)
+    from paper_1707_03268_b200._lib import DETECTION
+    d2h = 4 + int(statistics.mean(nmine)) * DETECTION.itemsize
+    g_sorted = np.sort(gathered, order=["image", "level", "component", "ry", "rx"])
+    gather_info = {"detections": int(len(gathered)),
+                   "images": int(len(np.unique(gathered["image"]))),
+                   "sha16": hashlib.sha256(g_sorted.tobytes()).hexdigest()[:16]}
+
+    roofline = rooflines = None
+    if not args.stub:
+        roofline, rooflines = _rooflines(plan, n, kernel_ms, stream,
+                                         traffic_ok=args.config == 4 and args.basis == "shared")
+    cpu = None
+    if rk.rank == 0 and rk.world == 1 and not args.no_cpu and not args.stub:
+        cpu = _cpu_baseline(args, wl)
+
+    if rk.rank == 0:
+        basis = "dense" if args.basis == "dense" else f"R{args.rank}"
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "fp32 (K1; K2 tcgen05 3xTF32 + FFMA) + f64 (K3/K4 placement)",
+            "dtype": ("fp32 (K1; K2 tcgen05 2xTF32 + bf16 correction, FFMA) + f64 (K3/K4 placement)"),
             "data": "synthetic",
-            "config": {"workload": f"config {CFG}: {args.images} x 1280x720 HOG pyramids "
-                                   "(49 levels, 441,041 cells x 32 ch), 54 filters (3 mirrored "
-                                   "pairs: root 6x11 + 8 parts 6x6 at 2x), shared rank-8 basis, "
-                                   "unbounded GDT (r*) + assembly + tau compaction",
-                       "images": args.images, "evals_per_image": evals_img,
-                       "parallelism": f"image shards x{world}",
-                       "k3": ("windowed r* kernel" if args.k3 == "window"
-                              else "Felzenszwalb lower-envelope kernels"),
-                       "l2": "inputs 3.6 GB per step > 126 MB L2 (no flush needed)"},
+            "config": ({"workload": "stub scorer (CPU harness test)", "images": args.images}
+                       if args.stub else
+                       {"workload": _describe(args.config, wl, args.rank, args.basis, args.images),
+                        "config": args.config, "basis": basis, "images": args.images,
+                        "evals_per_image": evals_img,
+                        "parallelism": f"image shards x{rk.world} ({n} on rank 0)",
+                        "k3": ("windowed r* kernel" if args.k3 == "window"
+                               else "Felzenszwalb lower-envelope kernels"),
+                        "l2": (f"inputs {x_bytes / 1e9:.2f} GB per rank > 126 MB L2 (no flush)"
+                               if flush is None else
+                               f"inputs {x_bytes / 1e6:.1f} MB: 512 MB L2 flush write between "
+                               "timed steps (outside the timed windows)")}),
             "images_per_s": images_s,
             "kernel_ms": kernel_ms,
             "roofline": roofline,
             "rooflines": rooflines,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sc.h2d_bytes(),
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": 0 if args.stub else sc.h2d_bytes(),
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
-                    "detections_per_step": statistics.mean(ndets), "tau": tau},
+                    "detections_per_step": statistics.mean(ndets), "tau": tau,
+                    "gathered": gather_info},
             "gpu_launches": plan.launches_per_run() * args.steps,
             "clocks": clocks.summary(),
             "clocks_e2e": clocks_e2e.summary(),
             "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)
-    if dist_on:
-        dist.destroy_process_group()
+    rk.close()
 
 
 # ---------------------------------------------------------------- reference arm
 
 def run_reference(args):
-    world, rank, _ = _dist()
+    """The reference algorithm (numpy oracle port; the reference is pure
+    Python and cannot travel to the GPU box) on all host cores, one image
+    (config 4) or the whole single-image workload per step: the metric is a
+    per-eval rate, and a full 64-image batch would take ~35 s per step on 16
+    cores.  Levels are synthesised before each timed pool.map."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_1707_03268_b200 import synth
 
-    wl = synth.workload(CFG)
+    wl = synth.workload(args.config)
     workers = os.cpu_count() or 1
-    n_root = len(wl.pyramid.root_levels)
-    import multiprocessing as mp
-
-    ctx = mp.get_context("spawn")
     times, evals = [], 0
-    with ctx.Pool(workers, initializer=_cpu_init) as pool:
+    with tempfile.TemporaryDirectory(prefix="dpm_ref_") as tmp, _cpu_pool(args, workers) as pool:
         for k in range(args.warmup + args.steps):
-            tasks = _cpu_sample_tasks(image=k % N_IMAGES, n_root=n_root)
+            path, offs = _cpu_write_image(args.config, wl, k % args.images, tmp)
+            tasks = _cpu_tasks(wl, path, offs, max_tasks=None if args.config in (1, 2, 4) else 96)
             t0 = time.perf_counter()
             out = pool.map(_cpu_task, tasks, chunksize=1)
             dt = time.perf_counter() - t0
+            os.remove(path)
             if k >= args.warmup:
                 times.append(dt)
-                evals = sum(e for e, _ in out)
+                evals += sum(e for e, _ in out)
     total = sum(times)
-    value = evals * len(times) / total
-    sample = (f"per step: one full image of config {CFG} ({len(tasks)} (root level, component) "
-              f"tasks, {evals} evals; each task also synthesises its two HOG levels) on a "
-              f"{workers}-process pool of the numpy oracle port (the reference is pure "
+    value = evals / total
+    sample = (f"per step: one image of config {args.config} ({len(tasks)} (root level, component) "
+              f"tasks, {evals // len(times)} evals; levels synthesised before the timed pool.map) "
+              f"on a {workers}-process pool of the numpy oracle port (the reference is pure "
               "Python/numpy and cannot travel to the GPU box)")
+    basis = "dense" if args.basis == "dense" else f"R{args.rank}"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"config {CFG} sample (CPU)", "images": 1,
-                   "evals_per_step": evals},
+        "config": {"workload": _describe(args.config, wl, args.rank, args.basis, 1) + " (CPU sample)",
+                   "config": args.config, "basis": basis, "images": 1,
+                   "evals_per_step": evals // len(times)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -519,7 +765,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--images", type=int, default=N_IMAGES)
+    ap.add_argument("--config", type=int, choices=(1, 2, 3, 4, 5), default=4)
+    ap.add_argument("--rank", type=int, default=None,
+                    help="CP rank of the shared basis (default: the config's first)")
+    ap.add_argument("--basis", choices=("shared", "dense"), default="shared",
+                    help="dense = the undecomposed 32-channel filters (identity basis)")
+    ap.add_argument("--images", type=int, default=None)
     ap.add_argument("--tau", type=float, default=None)
     ap.add_argument("--max-dets", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -528,9 +779,22 @@ def main():
     ap.add_argument("--k3", choices=("window", "envelope"), default="window",
                     help="K3 placement kernel: windowed r* (default, faster at the benchmark's "
                          "r*) or the Felzenszwalb lower envelope")
+    ap.add_argument("--stub", action="store_true",
+                    help="CPU harness test: stub scorer, gloo process group, no GPU")
     args = ap.parse_args()
+    from paper_1707_03268_b200 import synth
+
+    if args.rank is None:
+        ranks = synth.workload(args.config).ranks
+        args.rank = (8 if 8 in ranks else ranks[0]) if args.basis == "shared" else 32
+    if args.basis == "dense":
+        args.rank = 32
+    if args.images is None:
+        args.images = DEFAULT_IMAGES[args.config]
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -533,7 +533,10 @@ place_assemble_kernel(const float* __restrict__ S, const unsigned char* __restri
 
     // x pass: band row r (warp-strided), centre column = lane
     // band rows outside the map have no candidate (reference: (-inf, -r))
-    const int r_lo = max(0, -yb0), r_hi = min(nrows, pj.Hp - yb0);
+    // clamped so that a band entirely above or below the map (anchors far
+    // outside it) gives r_lo = r_hi and every row takes the no-candidate fill
+    const int r_lo = min(max(0, -yb0), nrows);
+    const int r_hi = max(min(nrows, pj.Hp - yb0), r_lo);
     const int n_out = r_lo + (nrows - r_hi);
     for (int i = tid; i < n_out * PT_W; i += PT_THREADS) {
       const int k = i / PT_W, l = i - k * PT_W;

@@ -189,6 +189,8 @@ class PyramidScorer:
         t = plan.torch
         if not hasattr(self, "_mix"):
             aj = plan._asm_jobs
+            if (aj["total_off"] < 0).any():
+                raise ValidationError("mixture() needs the totals of every assembly")
             groups = {}
             for idx in range(len(aj)):
                 key = (int(aj["image"][idx]), int(aj["level"][idx]))

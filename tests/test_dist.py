@@ -64,3 +64,37 @@ def test_gather_detections_world2_gloo():
     assert list(a["level"]) == [0, 0, 0, 1, 1, 1, 1]
     assert list(a["score"][3:]) == [100, 101, 102, 103]
     assert np.all(a["parts"][3:] == np.arange(16) + 1)
+
+
+def test_bench_self_launches_two_ranks_stub_gloo():
+    """``bench.py --gpus 2`` without torchrun re-launches itself with two
+    ranks (torch.distributed.run on 127.0.0.1); with the stub scorer the
+    ranks run gloo on CPU through the same harness: image sharding,
+    barrier + max-over-ranks timing, the detection gather and ONE JSON line
+    from rank 0 accounting for all 64 images."""
+    import hashlib
+    import json
+    import subprocess
+    import sys
+
+    from conftest import REPO
+
+    sys.path.insert(0, REPO)
+    import bench
+
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2", "--stub",
+                        "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                       timeout=240, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["steps"] == 2 and out["warmup"] == 3
+    assert out["config"]["images"] == 64
+    union = np.concatenate([bench.stub_detections(i) for i in range(64)])
+    union = np.sort(union, order=["image", "level", "component", "ry", "rx"])
+    g = out["e2e"]["gathered"]
+    assert g["detections"] == len(union) == out["e2e"]["detections_per_step"]
+    assert g["images"] == 64
+    assert g["sha16"] == hashlib.sha256(union.tobytes()).hexdigest()[:16]
+    assert out["value"] > 0 and out["e2e"]["value"] > 0
