@@ -15,7 +15,8 @@ from .errors import DeviceError, NumericError, ValidationError
 __all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "ASM_JOB", "SMAP_DESC",
            "DETECTION", "PLACE_RANGE", "PRUNE_JOB", "MIX_JOB", "LIB_PATH", "MAX_PARTS", "table_ptr"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdpm_b200.so")
+LIB_PATH = os.environ.get("DPM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                   "libdpm_b200.so")
 MAX_PARTS = 16
 ABI_VERSION = 2  # DPM_ABI_VERSION of include/dpm_b200.h
 

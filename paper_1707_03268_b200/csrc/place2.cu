@@ -1,0 +1,747 @@
+// K3 (part placement) + K4 (assembly), two-phase window screen.
+//
+// Reference: _placement_grid (detection.py:320-373), best_part_placement
+// (detection.py:180-207), the assembly of detect / dense_detect
+// (detection.py:449, 509-538; 590-613).  Same results as placement.cu (the
+// round-1 kernel, kept for A/B as DPM_K3=v1): bit-identical values and
+// argmaxes for a given FP32 map -- x pass then y pass, ties to the smallest
+// offset, the penalty subtracted in two stages with round-to-nearest FP64
+// operations.
+//
+// Inner screen + outer bound.  The unbounded transform is a window of
+// radius r* (App. A.2; r* ~ 10 at the benchmark's maps) but the winner
+// almost always lies a few cells from the centre.  Each window is screened
+// in FP32 over its inner part |d| <= R1 = min(r, 6) only.  The outer
+// candidates are bounded from above by
+//   x pass: max of the band row + max over outer d of the screen penalty,
+//   y pass: max of the column's x results + the same for y,
+// (FP32 rounding is monotone, so the bound dominates every outer screen
+// value).  The decoded inner winner is the exact winner of the whole window
+// when both the inner runner-up and the outer bound stay below m1 - E2;
+// otherwise the lane scans exactly in FP64, in the reference's order: the
+// inner window for a near tie, the whole window when the bound fails (rare:
+// ~0.1% of x rows at the benchmark's maps).
+//
+// Screen values carry the candidate's code in their 4 low mantissa bits
+// (16 ulps).  E2x = 2^-17 M and E2y = 2^-16 M (M = max|S| + the largest
+// penalties, E2 = 2^-15 M from the prologue) cover twice the FP32 error
+// plus the encodings, so m2 < m1 - E2 proves the winner exact.  The x result
+// of a row is one 32-bit word: the winner's screen value with the x code in
+// its low 4 bits (13 = no candidate, 14 = a row resolved by an exact scan,
+// whose dx the y pass recovers by the same exact scan from global memory),
+// so the x loop stores its screen maximum as is.
+//
+// Structure.  CTA = 8 warps, 32 x 64 root tile of one (image, component,
+// root level), two CTAs per SM.  Per part:
+//   wait for the part's S band (TMA boxes, NaN outside the map, mbarrier),
+//   x pass over the band rows (lane = centre column), per-warp column maxima,
+//   one CTA barrier (x words complete, band buffer free, the next part's job
+//   record and tables visible) -> thread 0 issues the next part's band,
+//   y pass for the thread's 8 roots: screen the x words of the column; the
+//   winner's exact FP64 value from its S value in global memory (L2
+//   resident: the TMA just streamed it), so the y pass never reads the band
+//   and the next band lands underneath it.
+// x words are double-buffered by part parity and job records / tables
+// triple-buffered, so one barrier per part orders everything.  Warp 0 copies
+// the next part's job record (cp.async) and builds its penalty tables (FP32
+// screen values, exact FP64 penalties) during the x pass.
+#include <math.h>
+
+#include "place_common.cuh"
+
+namespace dpm {
+namespace k3v2 {
+
+constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
+constexpr int TH = 48;                      // root rows per tile (32 columns)
+constexpr int RPT = TH * PT_W / THREADS;    // roots per thread (6)
+constexpr int BAND2 = (2 * (TH - 1) + 1 + 2 * RCAP + TMA_BH - 1) / TMA_BH * TMA_BH;  // 128 band rows
+constexpr int R1MAX = 6;                    // inner screen radius
+constexpr int CODE_NONE = 13;               // x word: no candidate in the window
+constexpr int CODE_RARE = 14;               // x word: winner from an exact scan
+constexpr int TD = 36;                      // table stride: index d + 16, d in [-16, 16]
+static_assert(2 * R1MAX + 1 <= CODE_NONE, "inner codes fit below the special codes");
+
+struct PartTab {
+  float npx[TD];    // FP32 screen penalty -pen_x(d) at [d + 16]
+  float npx1[TD];   // the same shifted by one element (8-byte aligned odd pairs)
+  float npy[TD];
+  double px[33];    // exact FP64 pen_x(d) at [d + 16] (reference expression)
+  double py[33];
+  float out_x, out_y;  // max screen penalty over the outer offsets
+  float E2x, E2y;
+};
+
+struct __align__(128) Smem {
+  float s[BAND2 * COLS_PITCH];     // S band (TMA, NaN outside the map)
+  float x32[2][BAND2 * PT_W];      // x words by part parity
+  double tot[RPT][THREADS];        // running totals of the roots, summed in part order
+  float cm[2][WARPS][PT_W];        // per-warp column maxima of the x words
+  uint32_t rmask[WARPS][32];       // x pass: lane masks of the rows to rescan exactly
+  PartTab tab[3];                  // tables of part q at slot q % 3
+  alignas(16) JobRange jr[3];
+  alignas(16) dpm_place_job pj[3];
+  dpm_asm_job aj;
+  alignas(8) uint64_t band_bar;
+};
+
+template <int CODE>
+__device__ __forceinline__ float enc4(float v, uint32_t mask) { return enc_idx<CODE>(v, mask); }
+__device__ __forceinline__ float enc_code(float v, int code) {
+  return __uint_as_float((__float_as_uint(v) & ~15u) | (uint32_t)code);
+}
+__device__ __forceinline__ int code_of(float w) { return (int)(__float_as_uint(w) & 15u); }
+// (bits(v) & mask) | code in one lop3; code is a constant after unrolling
+__device__ __forceinline__ float enc_idx_rt(float v, uint32_t mask, int code) {
+  return __uint_as_float((__float_as_uint(v) & mask) | (uint32_t)code);
+}
+
+// Top-2 reduction tree.  A node is (h, l): its best candidate and the best
+// of the others; NaN candidates (outside the map) drop out of both.  A
+// balanced tree keeps the dependency chain short (the screens run at 4 warps
+// per scheduler, so chain latency is not hidden).
+__device__ __forceinline__ void leaf2(float a, float b, float& h, float& l) {
+  h = fmaxf(a, b);
+  l = fmin_nan(a, b);
+}
+__device__ __forceinline__ void join2(float& h, float& l, float h2, float l2) {
+  l = fmaxf(fmaxf(l, l2), fmin_nan(h, h2));
+  h = fmaxf(h, h2);
+}
+template <int N>
+__device__ __forceinline__ void tree_reduce(float (&h)[N], float (&l)[N]) {
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int k = 0; k + w < N; k += 2 * w) join2(h[k], l[k], h[k + w], l[k + w]);
+}
+
+// Packed inner screen (x pass at scale 2): pairs (d0 + 2k, d0 + 2k + 1),
+// k < R1, 8-byte aligned at p0 + 2k (codes 2k, 2k + 1), then the single
+// candidate c (code 2 R1).  m1 = top encoded value, m2 = best of the others.
+template <int R1>
+__device__ __forceinline__ void scr_packed(const float* __restrict__ p0,
+                                           const unsigned long long (&pp)[R1 > 0 ? R1 : 1],
+                                           float single, uint32_t mask, float& m1, float& m2) {
+  const float c = enc4<2 * R1>(single, mask);
+  if constexpr (R1 == 0) {
+    m1 = fmaxf(c, -INFINITY);
+    m2 = -INFINITY;
+  } else {
+    float h[R1], l[R1];
+#pragma unroll
+    for (int k = 0; k < R1; ++k) {
+      const unsigned long long s2 = *reinterpret_cast<const unsigned long long*>(p0 + 2 * k);
+      unsigned long long v2;
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v2) : "l"(s2), "l"(pp[k]));
+      float va, vb;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(va), "=f"(vb) : "l"(v2));
+      leaf2(enc_idx_rt(va, mask, 2 * k), enc_idx_rt(vb, mask, 2 * k + 1), h[k], l[k]);
+    }
+    tree_reduce<R1>(h, l);
+    m2 = fmaxf(l[0], fmin_nan(h[0], c));
+    m1 = fmaxf(fmaxf(h[0], c), -INFINITY);  // all candidates outside the map: -inf, not NaN
+  }
+}
+
+// Strided inner screen (x pass at scale 1, y pass): candidates src[d*STRIDE]
+// + pr[d + R1], d = -R1..R1, code d + R1.
+template <int R1, int STRIDE>
+__device__ __forceinline__ void scr_strided(const float* __restrict__ src,
+                                            const float (&pr)[2 * R1 + 1], uint32_t mask,
+                                            float& m1, float& m2) {
+  const float c = enc_idx_rt(src[R1 * STRIDE] + pr[2 * R1], mask, 2 * R1);
+  if constexpr (R1 == 0) {
+    m1 = fmaxf(c, -INFINITY);
+    m2 = -INFINITY;
+  } else {
+    float h[R1], l[R1];
+#pragma unroll
+    for (int k = 0; k < R1; ++k) {
+      const int d = -R1 + 2 * k;
+      leaf2(enc_idx_rt(src[d * STRIDE] + pr[d + R1], mask, d + R1),
+            enc_idx_rt(src[(d + 1) * STRIDE] + pr[d + 1 + R1], mask, d + 1 + R1), h[k], l[k]);
+    }
+    tree_reduce<R1>(h, l);
+    m2 = fmaxf(l[0], fmin_nan(h[0], c));
+    m1 = fmaxf(fmaxf(h[0], c), -INFINITY);  // all candidates outside the map: -inf, not NaN
+  }
+}
+
+// Exact x window scan in the reference's order (ascending dx, strict '>')
+// over dx in [lo, hi], band cells (s0 = dx = 0; NaN = outside the map).
+// Returns the winner, lo when there is no candidate.  Rare: out of line.
+__device__ __noinline__ int x_exact_band(const float* s0, int lo, int hi, const double* px) {
+  double best = -INFINITY;
+  int bi = lo;
+  for (int d = lo; d <= hi; ++d) {
+    const float v = s0[d];
+    if (v != v) continue;
+    const double e = __dadd_rn((double)v, -px[d + 16]);
+    if (e > best) { best = e; bi = d; }
+  }
+  return bi;
+}
+
+// The same scan over the map in global memory (row pointer at column cx):
+// recovers the dx of an x word with CODE_RARE (the x pass found it with this
+// very scan over the band, so both agree).
+__device__ __noinline__ int x_exact_global(const float* __restrict__ srow, int cx, int Wp, int r,
+                                           const double* px) {
+  double best = -INFINITY;
+  int bi = -r;
+  const int lo = max(-r, -cx), hi = min(r, Wp - 1 - cx);
+  for (int d = lo; d <= hi; ++d) {
+    const double e = __dadd_rn((double)__ldg(srow + d), -px[d + 16]);
+    if (e > best) { best = e; bi = d; }
+  }
+  return bi;
+}
+
+struct XDec {  // decoding of the x codes of one part in one tile
+  int d0, ds, c2r1;
+};
+
+// Exact y scan over dy in [lo, hi] for one root in the reference's order:
+// x words of the root's column (xcol at dy = 0), exact x values from the S
+// values in global memory.  With thr > -inf (a near tie of the inner
+// screen) only the rows whose screen value -- recomputed bit for bit: same
+// add, same code -- reaches thr are candidates; the others are below the
+// winner by more than the screening error.  Returns (dy + 64) | (dx + 64)
+// << 8, or -1 when no row has a candidate.
+__device__ __noinline__ int y_exact(const float* xcol, const float* __restrict__ smap, int pitch,
+                                    int cy, int cx, int lo, int hi, int Wp, const PartTab* tb,
+                                    XDec xd, int rx, float thr, uint32_t mask, int r1) {
+  double best = -INFINITY;
+  int out = -1;
+  for (int dy = lo; dy <= hi; ++dy) {
+    const float w = xcol[dy * PT_W];
+    const int c = code_of(w);
+    if (c == CODE_NONE) continue;
+    if (enc_idx_rt(w + tb->npy[dy + 16], mask, dy + r1) < thr) continue;
+    const float* srow = smap + (int64_t)(cy + dy) * pitch;
+    const int dx = c == CODE_RARE ? x_exact_global(srow + cx, cx, Wp, rx, tb->px)
+                                  : (c == xd.c2r1 ? xd.ds : xd.d0 + c);
+    const double xv = __dadd_rn((double)__ldg(srow + cx + dx), -tb->px[dx + 16]);
+    const double e = __dadd_rn(xv, -tb->py[dy + 16]);
+    if (e > best) {
+      best = e;
+      out = (dy + 64) | ((dx + 64) << 8);
+    }
+  }
+  return out;
+}
+
+// x pass of one part over band rows rb0, rb0 + step, ... (< r_hi) at lane
+// centre xc (FULLW: one row per warp iteration, lane = column; else lpr
+// lanes per row, 32 / lpr rows per iteration).  Stores the x words and folds
+// the column maxima into cmaxv.  Rows whose screen is not conclusive (near
+// tie, failed outer bound, no inner candidate) are only flagged in the main
+// loop -- one ballot per iteration, its mask parked in shared memory when
+// non-zero -- and rescanned exactly afterwards, so the hot loop is straight
+// line code.
+template <int R1, bool PACKED, bool OUTER, bool FULLW>
+__device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __restrict__ band,
+                                       const PartTab& tb, uint32_t* __restrict__ rmask, int lane,
+                                       int rb0, int r_hi, int step, int xsub, int xc, int lpr,
+                                       int wt, int reach, int c0, int scale, XDec xd, int rx,
+                                       uint32_t mask, float& cmaxv) {
+  const float E2 = tb.E2x;
+  float pr[2 * R1 + 1];
+  unsigned long long pp[R1 > 0 ? R1 : 1];
+  if constexpr (PACKED) {
+    // pair k starts at d0 + 2k: table index d0 + 2k + 16, shifted table if odd
+    const float* tp = ((xd.d0 + 16) & 1) ? tb.npx1 + xd.d0 + 17 : tb.npx + xd.d0 + 16;
+#pragma unroll
+    for (int k = 0; k < R1; ++k) pp[k] = *reinterpret_cast<const unsigned long long*>(tp + 2 * k);
+    pr[0] = tb.npx[xd.ds + 16];
+  } else {
+#pragma unroll
+    for (int d = -R1; d <= R1; ++d) pr[d + R1] = tb.npx[d + 16];
+  }
+  const float out = tb.out_x;
+  const int xsh = c0 - rx;  // shared column of band column 0
+  const int cstep = PACKED ? 2 : scale;
+  uint32_t iters = 0;  // bit i: iteration i flagged a rare row
+  int it = 0;
+  for (int rb = rb0; rb < r_hi; rb += step, ++it) {
+    const int r = FULLW ? rb : min(rb + xsub, r_hi - 1);  // clamped: spare lanes still shuffle
+    const bool live = (FULLW || rb + xsub < r_hi) && xc < wt;
+    const float* row = band + r * COLS_PITCH;
+    const float* s0 = row + c0 + cstep * xc;  // dx = 0
+    float m1, m2;
+    if constexpr (PACKED) scr_packed<R1>(s0 + xd.d0, pp, s0[xd.ds] + pr[0], mask, m1, m2);
+    else scr_strided<R1, 1>(s0, pr, mask, m1, m2);
+    bool full = false;
+    if constexpr (OUTER) {
+      // maximum of the band row over the columns this row's windows reach
+      float mr;
+      if constexpr (FULLW) {
+        const float a = row[xsh + xc];
+        const float b = xc + 32 < reach ? row[xsh + xc + 32] : -INFINITY;
+        const float c = xc + 64 < reach ? row[xsh + xc + 64] : -INFINITY;
+        const float l = fmaxf(a, fmaxf(b, c));
+        asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(l));
+      } else {
+        mr = -INFINITY;
+        for (int c = xc; c < reach; c += lpr) mr = fmaxf(mr, row[xsh + c]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1)
+          if (o < lpr) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+      }
+      full = mr + out >= m1 - E2;
+    }
+    const bool rare = live && (full || m1 < NONE_BELOW || m2 >= m1 - E2);
+    const uint32_t bal = __ballot_sync(0xffffffffu, rare);
+    if (bal != 0u) {
+      iters |= 1u << it;
+      if (lane == 0) rmask[it] = bal;
+    }
+    if (live) {  // certified: the screen maximum, its code names the winner
+      x32[r * PT_W + xc] = m1;
+      cmaxv = fmaxf(cmaxv, m1);
+    }
+  }
+  if (iters == 0u) return;
+  __syncwarp();
+  // exact rescans of the flagged rows over the whole window (the reference's
+  // order); the winner's screen value with CODE_RARE, or no candidate
+  while (iters != 0u) {
+    const int i = __ffs(iters) - 1;
+    iters &= iters - 1;
+    if (!((rmask[i] >> lane) & 1u)) continue;
+    const int r = rb0 + i * step + xsub;
+    const float* s0 = band + r * COLS_PITCH + c0 + cstep * xc;
+    const int xi = x_exact_band(s0, -rx, rx, tb.px);
+    const float v = s0[xi];
+    const float word = v == v ? enc_code(v + tb.npx[xi + 16], CODE_RARE)
+                              : enc_code(OUT_SENTINEL, CODE_NONE);
+    x32[r * PT_W + xc] = word;
+    cmaxv = fmaxf(cmaxv, word);
+  }
+}
+
+// y pass of one part for the thread's roots (R1 = inner y radius).  Adds
+// the placed values to tot[] in part order, writes positions / placed.
+template <int R1, bool OUTER, int K0, int G, typename RootOf>
+__device__ __forceinline__ void y_group(const float* __restrict__ x32, const float* __restrict__ smap,
+                                       int pitch, const dpm_place_job* pjs, const PartTab& tb,
+                                       XDec xd, int rx, int ry, int yb0, int ty0, int tx0,
+                                       uint32_t mask, RootOf root_of, const dpm_asm_job& aj, int p,
+                                       int hr, int wr, double* __restrict__ tot, uint32_t* posb,
+                                       double* placedb, float cmax) {
+  const float E2 = tb.E2y;
+  float pr[2 * R1 + 1];
+#pragma unroll
+  for (int d = -R1; d <= R1; ++d) pr[d + R1] = tb.npy[d + 16];
+  const float bound = OUTER ? cmax + tb.out_y : -INFINITY;  // outer rows of this column
+  const int scale = pjs->scale, ay = pjs->ay, ax = pjs->ax;
+  // phase 1: screen every root, start the S loads of the certified winners.
+  // st = state (0 dead, 1 certified, 2 exact inner scan, 3 exact full scan,
+  // 4 no candidate, 5 certified dy whose x row was scanned exactly)
+  //      | (dy + 64) << 3 | (dx + 64) << 10
+  int st[G];
+  float sv[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int k = K0 + g;
+    int iyr, ixr;
+    int& stk = st[g];
+    stk = 0;
+    sv[g] = 0.f;
+    if (!root_of(k, iyr, ixr)) continue;
+    const int cy = scale * (aj.ry0 + ty0 + iyr) + ay;
+    const float* xcol = x32 + (cy - yb0) * PT_W + ixr;
+    float m1 = -INFINITY, m2 = -INFINITY;
+    scr_strided<R1, PT_W>(xcol, pr, mask, m1, m2);
+    const float lo = m1 - E2;
+    if (bound >= lo) {
+      stk = 3;
+    } else if (m1 < NONE_BELOW) {
+      stk = 4;
+    } else if (m2 >= lo) {
+      stk = 2;
+      sv[g] = lo;  // rescan only the rows whose screen value reaches lo
+    } else {
+      const int dy = code_of(m1) - R1;
+      const int c = code_of(xcol[dy * PT_W]);
+      if (c == CODE_RARE) {
+        stk = 5 | ((dy + 64) << 3);
+      } else {
+        const int dx = c == xd.c2r1 ? xd.ds : xd.d0 + c;
+        const int cx = scale * (aj.rx0 + tx0 + ixr) + ax;
+        stk = 1 | ((dy + 64) << 3) | ((dx + 64) << 10);
+        sv[g] = __ldg(smap + (int64_t)(cy + dy) * pitch + cx + dx);
+      }
+    }
+  }
+  // phase 2: exact FP64 values, totals and outputs
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int k = K0 + g;
+    int state = st[g] & 7;
+    if (state == 0) continue;
+    int iyr, ixr;
+    root_of(k, iyr, ixr);
+    const int iy = ty0 + iyr, ix = tx0 + ixr;
+    const int cy = scale * (aj.ry0 + iy) + ay;
+    const int cx = scale * (aj.rx0 + ix) + ax;
+    int dy = ((st[g] >> 3) & 127) - 64, dx = ((st[g] >> 10) & 127) - 64;
+    float s = sv[g];
+    if (state != 1) {
+      if (state == 5) {
+        dx = x_exact_global(smap + (int64_t)(cy + dy) * pitch + cx, cx, pjs->Wp, rx, tb.px);
+      } else if (state != 4) {
+        const float* xcol = x32 + (cy - yb0) * PT_W + ixr;
+        const int q = y_exact(xcol, smap, pitch, cy, cx, state == 2 ? -R1 : -ry,
+                              state == 2 ? R1 : ry, pjs->Wp, &tb, xd, rx,
+                              state == 2 ? sv[g] : -INFINITY, mask, R1);
+        if (q < 0) {
+          state = 4;
+        } else {
+          dy = (q & 255) - 64;
+          dx = (q >> 8) - 64;
+        }
+      }
+      if (state == 4) {  // no candidate: the reference's (-inf, first dy, first row's dx)
+        dy = -ry;
+        dx = -rx;
+      } else {
+        s = __ldg(smap + (int64_t)(cy + dy) * pitch + cx + dx);
+      }
+    }
+    double best = -INFINITY;
+    if (state != 4) best = __dadd_rn(__dadd_rn((double)s, -tb.px[dx + 16]), -tb.py[dy + 16]);
+    tot[k * THREADS] = __dadd_rn(tot[k * THREADS], best);
+    const int o = (p * hr + iy) * wr + ix;
+    if (posb) posb[o] = pack_pos(cy + dy, cx + dx);
+    if (placedb) placedb[o] = best;
+  }
+}
+
+// y pass of one part for the thread's RPT roots, in groups of 3 (the loads
+// of a group are in flight together; smaller groups keep the registers of
+// the screens in check)
+template <int R1, bool OUTER, typename RootOf>
+__device__ __forceinline__ void y_pass(const float* __restrict__ x32, const float* __restrict__ smap,
+                                       int pitch, const dpm_place_job* pjs, const PartTab& tb,
+                                       XDec xd, int rx, int ry, int yb0, int ty0, int tx0,
+                                       uint32_t mask, RootOf root_of, const dpm_asm_job& aj, int p,
+                                       int hr, int wr, double* __restrict__ tot, uint32_t* posb,
+                                       double* placedb, float cmax) {
+  y_group<R1, OUTER, 0, 3>(x32, smap, pitch, pjs, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj,
+                           p, hr, wr, tot, posb, placedb, cmax);
+  y_group<R1, OUTER, 3, 3>(x32, smap, pitch, pjs, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj,
+                           p, hr, wr, tot, posb, placedb, cmax);
+}
+
+// Penalty tables of a part (warp 0): FP32 screen values, exact FP64
+// penalties in the reference's expression, the outer maxima and the
+// screening bounds.
+__device__ __forceinline__ void build_tab(PartTab& tb, const dpm_place_job& pj, const JobRange& jr,
+                                          int lane) {
+  for (int i = lane; i < 33; i += 32) {
+    const int d = i - 16;
+    const double qx = pen(pj.cdx, pj.cdxx, d), qy = pen(pj.cdy, pj.cdyy, d);
+    tb.px[i] = qx;
+    tb.py[i] = qy;
+    tb.npx[i] = (float)(-qx);
+    tb.npx1[i + 1] = (float)(-qx);
+    tb.npy[i] = (float)(-qy);
+  }
+  __syncwarp();
+  const int d = lane - 16;  // lanes cover d = -16..15; d = 16 is lane 0's too
+  const bool ox = abs(d) > R1MAX && abs(d) <= jr.rx, oy = abs(d) > R1MAX && abs(d) <= jr.ry;
+  float mx = ox ? tb.npx[lane] : -INFINITY, my = oy ? tb.npy[lane] : -INFINITY;
+  if (16 <= jr.rx && lane == 0) mx = fmaxf(mx, tb.npx[32]);
+  if (16 <= jr.ry && lane == 0) my = fmaxf(my, tb.npy[32]);
+  float rmx, rmy;
+  asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(rmx) : "f"(mx));
+  asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(rmy) : "f"(my));
+  if (lane == 0) {
+    tb.out_x = rmx;
+    tb.out_y = rmy;
+    tb.E2x = jr.E2 * 0.25f;  // 2^-17 M
+    tb.E2y = jr.E2 * 0.5f;   // 2^-16 M
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
+place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ smaps,
+              const dpm_place_job* __restrict__ pjobs, const dpm_asm_job* __restrict__ ajobs,
+              int najobs, const dpm_place_range* __restrict__ prep, double* __restrict__ total,
+              uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
+              dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Smem& sh = *reinterpret_cast<Smem*>(smem_raw);
+  const int jid = find_job_warp(ajobs, najobs, blockIdx.x);
+  int tid_, lane_, warp_;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_));
+  asm volatile("and.b32 %0, %1, 31;" : "=r"(lane_) : "r"(tid_));
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp_) : "r"(tid_));
+  const int tid = tid_, lane = lane_, warp = __shfl_sync(0xffffffffu, warp_, 0);
+  const uint32_t band_bar = pl_smem(&sh.band_bar);
+  if (tid == 0) {
+    sh.aj = ajobs[jid];
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(band_bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const dpm_asm_job& aj = sh.aj;
+  const int hr = aj.ry1 - aj.ry0 + 1, wr = aj.rx1 - aj.rx0 + 1;
+  const int ntx = (wr + PT_W - 1) / PT_W;
+  const int tile = blockIdx.x - aj.block0;
+  const int ty0 = (tile / ntx) * TH, tx0 = (tile % ntx) * PT_W;
+  const int wt = min(PT_W, wr - tx0), h_tile = min(TH, hr - ty0);
+  const int lpr_log = wt > 16 ? 5 : wt > 8 ? 4 : wt > 4 ? 3 : wt > 2 ? 2 : wt > 1 ? 1 : 0;
+  const int lpr = 1 << lpr_log;
+  auto root_of = [=](int k, int& iyr, int& ixr) -> bool {
+    const int e = tid + THREADS * k;
+    iyr = e >> lpr_log;
+    ixr = e & (lpr - 1);
+    return iyr < h_tile && ixr < wt;
+  };
+  const int ry_lo = aj.ry0 + ty0;
+  const int ry_hi = aj.ry0 + ty0 + h_tile - 1;
+  const int rx_lo = aj.rx0 + tx0;
+  // ~15 from a value the compiler cannot fold (najobs > 0): the code, not the
+  // mask, is each encoding lop3's immediate
+  const uint32_t mask = ~15u | ((uint32_t)najobs >> 31);
+
+  double* const tot = &sh.tot[0][tid];  // tot[k * THREADS]: root k of this thread
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    int iyr, ixr;
+    double t = 0.0;
+    if (aj.root_off >= 0 && root_of(k, iyr, ixr))
+      t = (double)__ldg(S + aj.root_off + (int64_t)(ry_lo + iyr) * aj.root_pitch + rx_lo + ixr);
+    tot[k * THREADS] = t;
+  }
+
+  auto staged_ok = [&](const dpm_place_job& pj, const JobRange& jr) {
+    return jr.rx <= RCAP && jr.ry <= RCAP && pj.scale <= 2;
+  };
+  // job record + r*/E2 of part q into slot q % 3 (warp 0, cp.async)
+  auto fetch_job = [&](int q) {
+    const int slot = q % 3;
+    if (lane < (int)(sizeof(dpm_place_job) / 8)) {
+      const uint32_t sa = pl_smem(reinterpret_cast<unsigned char*>(&sh.pj[slot]) + 8 * lane);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                   "l"(reinterpret_cast<const unsigned char*>(pjobs + aj.part_job0 + q) + 8 * lane));
+    } else if (lane == 31) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(pl_smem(&sh.jr[slot])),
+                   "l"(prep + aj.part_job0 + q));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto finish_job = [&](int q) {  // warp 0: wait for the copy, build the tables
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncwarp();
+    build_tab(sh.tab[q % 3], sh.pj[q % 3], sh.jr[q % 3], lane);
+  };
+  // band of part q (thread 0): TMA boxes covering the band rows; the buffer's
+  // previous band was last read before the barrier preceding this call
+  auto issue_band = [&](int q) {
+    const dpm_place_job& pj = sh.pj[q % 3];
+    const JobRange& jr = sh.jr[q % 3];
+    if (tid != 0 || !staged_ok(pj, jr)) return;
+    const int yb0 = pj.scale * ry_lo + pj.ay - jr.ry;
+    const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
+    const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
+    const int nbox = (nrows + TMA_BH - 1) / TMA_BH;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(band_bar),
+                 "r"((uint32_t)nbox * TMA_BOX_BYTES)
+                 : "memory");
+    const void* map = smaps + (int64_t)pj.smap * DPM_SMAP_BYTES;
+    const uint32_t dst = pl_smem(sh.s);
+    for (int k = 0; k < nbox; ++k)
+      tma_band_box(dst + (uint32_t)k * TMA_BOX_BYTES, map, xb0 & ~3, yb0 + k * TMA_BH, pj.smap_z,
+                   band_bar);
+  };
+
+  uint32_t bands = 0;  // bands staged so far: band k completes barrier phase k
+  if (aj.nparts > 0) {
+    if (warp == 0) {
+      fetch_job(0);
+      finish_job(0);
+    }
+    __syncthreads();
+    issue_band(0);
+  }
+  uint32_t* const posb = aj.pos_off >= 0 ? pos + aj.pos_off : nullptr;
+  double* const placedb = aj.placed_off >= 0 ? placed + aj.placed_off : nullptr;
+  const int xsub = lane >> lpr_log, xc = lane & (lpr - 1);
+  for (int p = 0; p < aj.nparts; ++p) {
+    const int slot = p % 3, buf = p & 1;
+    const dpm_place_job& pj = sh.pj[slot];
+    const JobRange& jr = sh.jr[slot];
+    const PartTab& tb = sh.tab[slot];
+    // job p+1 into slot (p+1) % 3 = (p-2) % 3, whose last readers (part p-2's
+    // y pass) finished before the previous barrier
+    const bool have_next = p + 1 < aj.nparts;
+    if (warp == 0 && have_next) fetch_job(p + 1);
+    const bool staged = staged_ok(pj, jr);
+    const int rx = jr.rx, ry = jr.ry;
+    const int yb0 = pj.scale * ry_lo + pj.ay - ry;
+    const int xsh = (pj.scale * rx_lo + pj.ax - rx) & 3;  // band column 0's shared column
+    const int c0 = xsh + rx;                               // shared column of lane 0's dx = 0
+    const int r1x = min(rx, R1MAX), r1y = min(ry, R1MAX);
+    XDec xd;
+    if (pj.scale == 2) {  // packed pairs start on an even shared column
+      const int s = ((c0 & 1) + r1x) & 1;
+      xd.d0 = -r1x + s;
+      xd.ds = s ? -r1x : r1x;
+    } else {
+      xd.d0 = -r1x;
+      xd.ds = r1x;
+    }
+    xd.c2r1 = 2 * r1x;
+    float* x32 = sh.x32[buf];
+    if (staged) {
+      pl_mbar_wait(band_bar, bands++ & 1);
+      const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * ry;
+      // rows outside the map: no candidate (reference: (-inf, -r))
+      const int r_lo = min(max(0, -yb0), nrows);
+      const int r_hi = max(min(nrows, pj.Hp - yb0), r_lo);
+      const int n_out = r_lo + (nrows - r_hi);
+      const float sent = enc_code(OUT_SENTINEL, CODE_NONE);
+      for (int i = tid; i < n_out * PT_W; i += THREADS) {
+        const int k = i / PT_W, l = i - k * PT_W;
+        x32[(k < r_lo ? k : r_hi + (k - r_lo)) * PT_W + l] = sent;
+      }
+      const int rpw = PT_W >> lpr_log;
+      const int rb0 = r_lo + warp * rpw, step = WARPS * rpw;
+      const int reach = pj.scale * (wt - 1) + 1 + 2 * rx;  // band columns the windows reach
+      float cmaxv = n_out > 0 ? sent : -INFINITY;
+      const bool outer = rx > R1MAX;
+#define DPM_XARGS x32, sh.s, tb, sh.rmask[warp], lane, rb0, r_hi, step, xsub, xc, lpr, wt, reach, c0, pj.scale, xd, rx, mask, cmaxv
+      if (pj.scale == 2) {
+        if (outer) {
+          if (lpr == 32) x_pass<R1MAX, true, true, true>(DPM_XARGS);
+          else x_pass<R1MAX, true, true, false>(DPM_XARGS);
+        } else {
+          switch (r1x) {
+#define DPM_XC(R) case R: x_pass<R, true, false, false>(DPM_XARGS); break;
+            DPM_XC(0) DPM_XC(1) DPM_XC(2) DPM_XC(3) DPM_XC(4) DPM_XC(5) DPM_XC(6)
+#undef DPM_XC
+          }
+        }
+      } else {
+        if (outer) {
+          x_pass<R1MAX, false, true, false>(DPM_XARGS);
+        } else {
+          switch (r1x) {
+#define DPM_XC(R) case R: x_pass<R, false, false, false>(DPM_XARGS); break;
+            DPM_XC(0) DPM_XC(1) DPM_XC(2) DPM_XC(3) DPM_XC(4) DPM_XC(5) DPM_XC(6)
+#undef DPM_XC
+          }
+        }
+      }
+#undef DPM_XARGS
+      // column maxima: fold the row groups of a packed warp, group 0 writes
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1)
+        if (o >= lpr) cmaxv = fmaxf(cmaxv, __shfl_xor_sync(0xffffffffu, cmaxv, o));
+      if (xsub == 0) sh.cm[buf][warp][xc] = cmaxv;
+    }
+    if (warp == 0 && have_next) finish_job(p + 1);
+    __syncthreads();  // x(p) done: x words visible, band buffer free, tables of p+1 built
+    if (have_next) issue_band(p + 1);
+    const float* sm = S + pj.s_off;
+    const int pitch = s_pitch(pj.Wp);
+    if (!staged) {
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        int iyr, ixr;
+        if (!root_of(k, iyr, ixr)) continue;
+        const int iy = ty0 + iyr, ix = tx0 + ixr;
+        const int cy = pj.scale * (aj.ry0 + iy) + pj.ay;
+        const int cx = pj.scale * (aj.rx0 + ix) + pj.ax;
+        double best;
+        int bdy, bdx;
+        place_unstaged(sm, pj, cy, cx, rx, ry, best, bdy, bdx);
+        tot[k * THREADS] = __dadd_rn(tot[k * THREADS], best);
+        const int o = (p * hr + iy) * wr + ix;
+        if (posb) posb[o] = pack_pos(cy + bdy, cx + bdx);
+        if (placedb) placedb[o] = best;
+      }
+      continue;
+    }
+    // the column maximum of this thread's roots (every root of a thread has
+    // the column tid & (lpr - 1))
+    float cmax = -INFINITY;
+    if (ry > R1MAX) {
+      const int col = tid & (lpr - 1);
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) cmax = fmaxf(cmax, sh.cm[buf][w][col]);
+    }
+#define DPM_YARGS x32, sm, pitch, &pj, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj, p, hr, wr, tot, posb, placedb, cmax
+    if (ry > R1MAX) {
+      y_pass<R1MAX, true>(DPM_YARGS);
+    } else {
+      switch (r1y) {
+#define DPM_YC(R) case R: y_pass<R, false>(DPM_YARGS); break;
+        DPM_YC(0) DPM_YC(1) DPM_YC(2) DPM_YC(3) DPM_YC(4) DPM_YC(5) DPM_YC(6)
+#undef DPM_YC
+      }
+    }
+#undef DPM_YARGS
+  }
+
+  // bias, totals, tau compaction (part positions read back from `pos`)
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    int iyr, ixr;
+    const bool live = root_of(k, iyr, ixr);
+    const int iy = ty0 + iyr, ix = tx0 + ixr;
+    const double t = __dadd_rn(tot[k * THREADS], aj.bias);
+    if (live && aj.total_off >= 0) total[aj.total_off + (int64_t)iy * wr + ix] = t;
+    if (dets == nullptr) continue;
+    const bool hit = live && t >= tau;
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (bal == 0u) continue;
+    const int leader = __ffs(bal) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(det_count, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!hit) continue;
+    const int slot = base + __popc(bal & ((1u << lane) - 1u));
+    if (slot >= max_dets) continue;
+    dpm_detection d;
+    d.image = aj.image;
+    d.level = aj.level;
+    d.component = aj.component;
+    d.ry = aj.ry0 + iy;
+    d.rx = aj.rx0 + ix;
+    d.nparts = aj.nparts;
+    d.score = t;
+    for (int q = 0; q < DPM_MAX_PARTS; ++q)
+      d.parts[q] = (q < aj.nparts && aj.pos_off >= 0)
+                       ? pos[aj.pos_off + ((int64_t)q * hr + iy) * wr + ix]
+                       : 0u;
+    dets[slot] = d;
+  }
+}
+
+}  // namespace k3v2
+
+int k3v2_tile_rows() { return k3v2::TH; }
+
+// launched by dpm_assemble (placement.cu)
+int launch_place2(const float* S, const void* smaps, const dpm_place_job* pjobs,
+                  const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
+                  const dpm_place_range* prep, double* total, uint32_t* pos, double* placed,
+                  double tau, dpm_detection* dets, int max_dets, int* det_count, cudaStream_t st) {
+  const size_t smem = sizeof(k3v2::Smem);
+  DPM_CUDA(cudaFuncSetAttribute(k3v2::place2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  k3v2::place2_kernel<<<(unsigned)nblocks, k3v2::THREADS, smem, st>>>(
+      S, static_cast<const unsigned char*>(smaps), pjobs, ajobs, najobs, prep, total, pos, placed,
+      tau, dets, max_dets, det_count);
+  DPM_LAUNCHED("place2_kernel");
+  return DPM_OK;
+}
+
+}  // namespace dpm

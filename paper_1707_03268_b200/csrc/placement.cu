@@ -43,66 +43,16 @@
 // range, beyond which no maximiser lies.  Radii above RCAP use unstaged loops
 // with the same arithmetic.
 #include <math.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include "common.cuh"
+#include "place_common.cuh"
 
 namespace dpm {
-
-constexpr int RCAP = 16;                                  // staged-path radius cap
-constexpr int PT_W = 32;                                  // root columns per tile (lanes)
-constexpr int PT_H = 64;                                  // root rows per tile
-constexpr int PT_THREADS = 512;
-constexpr int PT_WARPS = PT_THREADS / 32;
-constexpr int BAND_ROWS = 2 * (PT_H - 1) + 1 + 2 * RCAP;  // 159 band rows (scale <= 2)
-constexpr int TMA_BH = DPM_SMAP_BOX_H;                      // band rows per TMA box
-constexpr int BAND_MAX = (BAND_ROWS + TMA_BH - 1) / TMA_BH * TMA_BH;  // 160: whole boxes
-// even, so band rows start 8-byte aligned (packed pairs in the x pass)
-// band row pitch in shared memory = the TMA box width (the box lands dense)
-constexpr int COLS_PITCH = DPM_SMAP_BOX_W;  // 100 >= 2 * (PT_W - 1) + 1 + 2 * RCAP = 95
-static_assert(COLS_PITCH >= 2 * (PT_W - 1) + 1 + 2 * RCAP && COLS_PITCH % 4 == 0, "band width");
-constexpr uint32_t TMA_BOX_BYTES = DPM_SMAP_BOX_W * DPM_SMAP_BOX_H * 4;
-
-__device__ __forceinline__ double pen(double c1, double c2, int d) {
-  const double dd = (double)d;
-  return __dadd_rn(__dmul_rn(c1, dd), __dmul_rn(__dmul_rn(c2, dd), dd));
-}
-
-__device__ __forceinline__ double pen_absmax(double c1, double c2, int r) {
-  double m = fmax(fabs(pen(c1, c2, -r)), fabs(pen(c1, c2, r)));
-  if (c2 > 0.0) m = fmax(m, c1 * c1 / (4.0 * c2));
-  return m;
-}
-
-// r* of App. A.2 for one axis from the map range; +1 guards the floor.
-__device__ __forceinline__ int radius_of(const dpm_place_job& j, float vmax, float vmin, bool x_axis) {
-  if (j.radius >= 0) return j.radius;
-  const double a = x_axis ? j.cdxx : j.cdyy, b = x_axis ? j.cdx : j.cdy;
-  const double ao = x_axis ? j.cdyy : j.cdxx, bo = x_axis ? j.cdy : j.cdx;
-  const double dprime = ((double)vmax - (double)vmin) + bo * bo / (4.0 * ao);
-  return (int)floor((fabs(b) + sqrt(b * b + 4.0 * a * dprime)) / (2.0 * a)) + 1;
-}
-
-using JobRange = dpm_place_range;
-
-__device__ __forceinline__ JobRange job_range(const dpm_place_job& pj, const uint32_t* ranges) {
-  JobRange jr;
-  const float vmax = key_float(ranges[2 * pj.range_idx]);
-  const float vmin = key_float(ranges[2 * pj.range_idx + 1]);
-  jr.rx = radius_of(pj, vmax, vmin, true);
-  jr.ry = radius_of(pj, vmax, vmin, false);
-  const double mabs = fmax(fabs((double)vmax), fabs((double)vmin));
-  // floor: the index code of values near 0 lives in denormals (< 64 * 2^-149)
-  jr.E2 = (float)fmax(ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, jr.rx) +
-                                pen_absmax(pj.cdy, pj.cdyy, jr.ry), -15),
-                      0x1p-120);
-  jr.pad = 0;
-  return jr;
-}
 
 // K3 prologue: r* and the screening bound of every placement job, once per
 // run (after K2 has filled the map ranges)
@@ -111,32 +61,6 @@ place_ranges_kernel(const dpm_place_job* __restrict__ pjobs, int njobs,
                     const uint32_t* __restrict__ ranges, dpm_place_range* __restrict__ prep) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i < njobs) prep[i] = job_range(pjobs[i], ranges);
-}
-
-__device__ __forceinline__ uint32_t pack_pos(int y, int x) {
-  return ((uint32_t)(uint16_t)(int16_t)y << 16) | (uint32_t)(uint16_t)(int16_t)x;
-}
-
-constexpr float OUT_SENTINEL = -1.0e37f;  // x-pass result of a band row without candidates
-constexpr float NONE_BELOW = -1.0e36f;    // m1 below this: no candidate inside the map
-
-// (bits(v) & mask) | code in ONE lop3 (LUT 0xEA = (a & b) | c): the mask
-// lives in a register so the code can be the instruction's immediate
-template <int CODE>
-__device__ __forceinline__ float enc_idx(float v, uint32_t mask) {
-  uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(__float_as_uint(v)), "r"(mask), "n"(CODE));
-  return __uint_as_float(r);
-}
-
-// min that propagates NaN (FMNMX.NAN): cells outside the map arrive as NaN
-// (TMA out-of-bounds fill); in the top-2 merge below a NaN candidate must
-// drop out of both m1 and m2 -- with the NaN-ignoring fminf it would make m2
-// equal to the winner and force a needless exact rescan.
-__device__ __forceinline__ float fmin_nan(float a, float b) {
-  float r;
-  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-  return r;
 }
 
 // Window of 2R+1 candidates src[d*STRIDE] + np[d], d = -R..R (pointers at
@@ -229,28 +153,6 @@ __device__ __forceinline__ void screen_dispatch(int r, const float* __restrict__
 }
 static_assert(2 * RCAP + 1 <= 63, "window index must fit the 6-bit code");
 
-// Placement of one part for one root via direct global loads (any radius).
-__device__ void place_unstaged(const float* __restrict__ sm, const dpm_place_job& pj, int cy,
-                               int cx, int rx_, int ry_, double& best, int& bdy, int& bdx) {
-  best = -INFINITY;
-  bdy = -ry_;
-  bdx = -rx_;
-  for (int dy = -ry_; dy <= ry_; ++dy) {
-    const int y = cy + dy;
-    if (y < 0 || y >= pj.Hp) continue;
-    double xb = -INFINITY;
-    int xd = -rx_;
-    const int lo = max(-rx_, -cx), hi = min(rx_, pj.Wp - 1 - cx);
-    for (int dx = lo; dx <= hi; ++dx) {
-      const double c = __dadd_rn((double)__ldg(sm + (int64_t)y * s_pitch(pj.Wp) + cx + dx),
-                                 -pen(pj.cdx, pj.cdxx, dx));
-      if (c > xb) { xb = c; xd = dx; }
-    }
-    const double cand = __dadd_rn(xb, -pen(pj.cdy, pj.cdyy, dy));
-    if (cand > best) { best = cand; bdy = dy; bdx = xd; }
-  }
-}
-
 // Exact rescans of a near-tie window in the reference's order (ascending
 // offset, strict '>'), over the candidates whose FP32 screen value reaches
 // lo.  Rare; kept out of line so the screening loops do not reserve their
@@ -330,32 +232,6 @@ __device__ __forceinline__ void x_rows(PlaceSmem& sh, int buf, const float* srow
     sh.xsv[r * PT_W + xc] = srow[xi];
     sh.xdx[r * PT_W + xc] = (int8_t)xi;
   }
-}
-
-__device__ __forceinline__ uint32_t pl_smem(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-// Band copy: one TMA tensor load of a DPM_SMAP_BOX_W x DPM_SMAP_BOX_H box of
-// map z starting at (x, y) (signed; cells outside the map arrive as NaN).
-__device__ __forceinline__ void tma_band_box(uint32_t dst, const void* map, int x, int y, int z,
-                                             uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void pl_mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (int spin = 0; spin < 2000 && !done; ++spin)  // each try suspends up to 10 ms
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity), "r"(10000000u)
-        : "memory");
-  if (!done) asm volatile("trap;");  // a band that never lands is a bug, not a hang
 }
 
 __global__ void __launch_bounds__(PT_THREADS, 2)
@@ -690,6 +566,16 @@ extern "C" int64_t dpm_place_prepare(dpm_place_job* jobs, int njobs) {
   return b;
 }
 
+// DPM_K3=v1 selects the round-1 kernel (A/B); its tiles are PT_H root rows
+// tall, the two-phase kernel's k3v2 tile rows (place2.cu)
+static bool k3_use_v1() {
+  static const bool v1 = [] {
+    const char* e = getenv("DPM_K3");
+    return e != nullptr && e[0] == 'v' && e[1] == '1';
+  }();
+  return v1;
+}
+
 extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_place_job* pjobs,
                                         int npjobs) {
   if (njobs < 0 || (njobs > 0 && !jobs) || npjobs < 0 || (npjobs > 0 && !pjobs)) {
@@ -720,7 +606,8 @@ extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_
                 j.nparts, (long long)hr, (long long)wr);
       return DPM_ERR_ARG;
     }
-    b += ((hr + PT_H - 1) / PT_H) * ((wr + PT_W - 1) / PT_W);
+    const int th = k3_use_v1() ? PT_H : k3v2_tile_rows();
+    b += ((hr + th - 1) / th) * ((wr + PT_W - 1) / PT_W);
   }
   if (b > INT32_MAX) {
     set_error("dpm_assemble_prepare: too many CTAs");
@@ -751,6 +638,9 @@ extern "C" int dpm_assemble(const float* S, const void* smaps, const dpm_place_j
   DPM_REQUIRE(!dets || (det_count && pos), "dpm_assemble: detections need a counter and positions");
   DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_assemble: nblocks");
   if (najobs == 0 || nblocks == 0) return DPM_OK;
+  if (!k3_use_v1())
+    return launch_place2(S, smaps, pjobs, ajobs, najobs, nblocks, prep, total, pos, placed, tau,
+                         dets, max_dets, det_count, as_stream(stream));
   const size_t smem = sizeof(PlaceSmem);
   DPM_CUDA(cudaFuncSetAttribute(place_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
