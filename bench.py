@@ -640,7 +640,7 @@ def run_ours(args):
 
     # ---- end to end through the public API: pinned H2D + run + D2H detections,
     # gathered over the ranks (the path's only collective)
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(0 if args.no_e2e else max(1, args.warmup // 2)):
         sc.score_batch(host, tau, chunk_images=args.chunk)
     rk.barrier()
     e2e_ev = [rk.event() for _ in range(2)]
@@ -648,7 +648,7 @@ def run_ours(args):
     with ClockSampler(rk.local, enabled=not args.stub) as clocks_e2e:
         rk.barrier()
         e2e_ev[0].record(stream)
-        for _ in range(args.steps):
+        for _ in range(0 if args.no_e2e else args.steps):
             d = sc.score_batch(host, tau, chunk_images=args.chunk)
             nmine.append(len(d))
             gathered = rk.gather(d)
@@ -656,8 +656,10 @@ def run_ours(args):
         e2e_ev[1].record(stream)
         rk.barrier()
     e2e_ms = rk.max(e2e_ev[0].elapsed_time(e2e_ev[1]))
-    e2e_value = evals_step * args.steps / (e2e_ms / 1e3)
+    e2e_value = evals_step * args.steps / (e2e_ms / 1e3) if not args.no_e2e else None
     from paper_1707_03268_b200._lib import DETECTION
+    if args.no_e2e:
+        nmine, ndets, gathered = [0], [0], np.zeros(0, dtype=DETECTION)
     d2h = 4 + int(statistics.mean(nmine)) * DETECTION.itemsize
     g_sorted = np.sort(gathered, order=["image", "level", "component", "ry", "rx"])
     gather_info = {"detections": int(len(gathered)),
@@ -774,6 +776,9 @@ def main():
     ap.add_argument("--tau", type=float, default=None)
     ap.add_argument("--max-dets", type=int, default=1 << 20)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="skip the end-to-end leg (profiling: the launch list then holds the "
+                         "device-resident steps only)")
     ap.add_argument("--chunk", type=int, default=2,
                     help="images per H2D/compute pipeline chunk of the e2e score_batch call")
     ap.add_argument("--k3", choices=("window", "envelope"), default="window",

@@ -110,16 +110,48 @@ __device__ __forceinline__ void join2(float& h, float& l, float h2, float l2) {
   h = fmaxf(h, h2);
 }
 template <int N>
-__device__ __forceinline__ void tree_reduce(float (&h)[N], float (&l)[N]) {
+__device__ __forceinline__ void tree_reduce(float (&h)[N > 0 ? N : 1], float (&l)[N > 0 ? N : 1]) {
 #pragma unroll
   for (int w = 1; w < N; w *= 2)
 #pragma unroll
     for (int k = 0; k + w < N; k += 2 * w) join2(h[k], l[k], h[k + w], l[k + w]);
 }
 
-// Packed inner screen (x pass at scale 2): pairs (d0 + 2k, d0 + 2k + 1),
-// k < R1, 8-byte aligned at p0 + 2k (codes 2k, 2k + 1), then the single
-// candidate c (code 2 R1).  m1 = top encoded value, m2 = best of the others.
+// Leaves of the packed screen: pair k = candidates (d0 + 2k, d0 + 2k + 1)
+// at p0 + 2k (8-byte aligned), codes 2k and 2k + 1 (compile-time: the
+// encoding lop3 takes the code as its immediate).
+template <int R1, int K>
+__device__ __forceinline__ void leaves_packed(const float* __restrict__ p0,
+                                              const unsigned long long (&pp)[R1 > 0 ? R1 : 1],
+                                              uint32_t mask, float (&h)[R1 > 0 ? R1 : 1],
+                                              float (&l)[R1 > 0 ? R1 : 1]) {
+  if constexpr (K < R1) {
+    const unsigned long long s2 = *reinterpret_cast<const unsigned long long*>(p0 + 2 * K);
+    unsigned long long v2;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v2) : "l"(s2), "l"(pp[K]));
+    float va, vb;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(va), "=f"(vb) : "l"(v2));
+    leaf2(enc4<2 * K>(va, mask), enc4<2 * K + 1>(vb, mask), h[K], l[K]);
+    leaves_packed<R1, K + 1>(p0, pp, mask, h, l);
+  }
+}
+// Leaves of the strided screen: pair k = offsets (-R1 + 2k, -R1 + 2k + 1),
+// codes d + R1.
+template <int R1, int STRIDE, int K>
+__device__ __forceinline__ void leaves_strided(const float* __restrict__ src,
+                                               const float (&pr)[2 * R1 + 1], uint32_t mask,
+                                               float (&h)[R1 > 0 ? R1 : 1],
+                                               float (&l)[R1 > 0 ? R1 : 1]) {
+  if constexpr (K < R1) {
+    constexpr int D = -R1 + 2 * K;
+    leaf2(enc4<D + R1>(src[D * STRIDE] + pr[D + R1], mask),
+          enc4<D + 1 + R1>(src[(D + 1) * STRIDE] + pr[D + 1 + R1], mask), h[K], l[K]);
+    leaves_strided<R1, STRIDE, K + 1>(src, pr, mask, h, l);
+  }
+}
+
+// Packed inner screen (x pass at scale 2): the pairs, then the single
+// candidate (code 2 R1).  m1 = top encoded value, m2 = best of the others.
 template <int R1>
 __device__ __forceinline__ void scr_packed(const float* __restrict__ p0,
                                            const unsigned long long (&pp)[R1 > 0 ? R1 : 1],
@@ -130,15 +162,7 @@ __device__ __forceinline__ void scr_packed(const float* __restrict__ p0,
     m2 = -INFINITY;
   } else {
     float h[R1], l[R1];
-#pragma unroll
-    for (int k = 0; k < R1; ++k) {
-      const unsigned long long s2 = *reinterpret_cast<const unsigned long long*>(p0 + 2 * k);
-      unsigned long long v2;
-      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(v2) : "l"(s2), "l"(pp[k]));
-      float va, vb;
-      asm("mov.b64 {%0, %1}, %2;" : "=f"(va), "=f"(vb) : "l"(v2));
-      leaf2(enc_idx_rt(va, mask, 2 * k), enc_idx_rt(vb, mask, 2 * k + 1), h[k], l[k]);
-    }
+    leaves_packed<R1, 0>(p0, pp, mask, h, l);
     tree_reduce<R1>(h, l);
     m2 = fmaxf(l[0], fmin_nan(h[0], c));
     m1 = fmaxf(fmaxf(h[0], c), -INFINITY);  // all candidates outside the map: -inf, not NaN
@@ -151,21 +175,16 @@ template <int R1, int STRIDE>
 __device__ __forceinline__ void scr_strided(const float* __restrict__ src,
                                             const float (&pr)[2 * R1 + 1], uint32_t mask,
                                             float& m1, float& m2) {
-  const float c = enc_idx_rt(src[R1 * STRIDE] + pr[2 * R1], mask, 2 * R1);
+  const float c = enc4<2 * R1>(src[R1 * STRIDE] + pr[2 * R1], mask);
   if constexpr (R1 == 0) {
     m1 = fmaxf(c, -INFINITY);
     m2 = -INFINITY;
   } else {
     float h[R1], l[R1];
-#pragma unroll
-    for (int k = 0; k < R1; ++k) {
-      const int d = -R1 + 2 * k;
-      leaf2(enc_idx_rt(src[d * STRIDE] + pr[d + R1], mask, d + R1),
-            enc_idx_rt(src[(d + 1) * STRIDE] + pr[d + 1 + R1], mask, d + 1 + R1), h[k], l[k]);
-    }
+    leaves_strided<R1, STRIDE, 0>(src, pr, mask, h, l);
     tree_reduce<R1>(h, l);
     m2 = fmaxf(l[0], fmin_nan(h[0], c));
-    m1 = fmaxf(fmaxf(h[0], c), -INFINITY);  // all candidates outside the map: -inf, not NaN
+    m1 = fmaxf(fmaxf(h[0], c), -INFINITY);
   }
 }
 
@@ -265,15 +284,13 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
   const int cstep = PACKED ? 2 : scale;
   uint32_t iters = 0;  // bit i: iteration i flagged a rare row
   int it = 0;
-  for (int rb = rb0; rb < r_hi; rb += step, ++it) {
-    const int r = FULLW ? rb : min(rb + xsub, r_hi - 1);  // clamped: spare lanes still shuffle
-    const bool live = (FULLW || rb + xsub < r_hi) && xc < wt;
+  // screen of band row r (m1, m2, outer bound failed)
+  auto screen = [&](int r, float& m1, float& m2, bool& full) {
     const float* row = band + r * COLS_PITCH;
     const float* s0 = row + c0 + cstep * xc;  // dx = 0
-    float m1, m2;
     if constexpr (PACKED) scr_packed<R1>(s0 + xd.d0, pp, s0[xd.ds] + pr[0], mask, m1, m2);
     else scr_strided<R1, 1>(s0, pr, mask, m1, m2);
-    bool full = false;
+    full = false;
     if constexpr (OUTER) {
       // maximum of the band row over the columns this row's windows reach
       float mr;
@@ -292,6 +309,9 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
       }
       full = mr + out >= m1 - E2;
     }
+  };
+  // flag / store the screen result of row r (loop iteration it)
+  auto finish = [&](int r, bool live, int it, float m1, float m2, bool full) {
     const bool rare = live && (full || m1 < NONE_BELOW || m2 >= m1 - E2);
     const uint32_t bal = __ballot_sync(0xffffffffu, rare);
     if (bal != 0u) {
@@ -302,6 +322,15 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
       x32[r * PT_W + xc] = m1;
       cmaxv = fmaxf(cmaxv, m1);
     }
+  };
+  int rb = rb0;
+  for (; rb < r_hi; rb += step, ++it) {
+    const int r = FULLW ? rb : min(rb + xsub, r_hi - 1);  // clamped: spare lanes still shuffle
+    const bool live = (FULLW || rb + xsub < r_hi) && xc < wt;
+    float m1, m2;
+    bool full;
+    screen(r, m1, m2, full);
+    finish(r, live, it, m1, m2, full);
   }
   if (iters == 0u) return;
   __syncwarp();

@@ -2,6 +2,9 @@
 
     python tools/ncu_summary.py <launches.csv> <full.ncu-rep> <images> <tag>
 
+(<images>: images per launch of the --set full capture; NCU_LAUNCH_CMD names
+the command of the launch list when it differs from the default.)
+
 Writes profiles/<tag>_launches.md (per-kernel share of the step from the
 `gpu__time_duration` launch list), profiles/<tag>_ncu_full.md (key counters and
 stall reasons per kernel from the `--set full` capture) and
@@ -106,7 +109,9 @@ def main(launch_csv, rep, images, tag):
     tot = sum(per_step.values())
     with open(os.path.join(prof, f"{tag}_launches.md"), "w") as fh:
         fh.write(f"# {tag}: ncu launch list (gpu__time_duration, --clock-control none)\n\n")
-        fh.write(f"Command: `bench.py --images {images} --steps 2 --warmup 3 --no-cpu` under ncu "
+        cmd = os.environ.get("NCU_LAUNCH_CMD",
+                             f"bench.py --images {images} --steps 2 --warmup 3 --no-cpu")
+        fh.write(f"Command: `{cmd}` under ncu "
                  "(cold-cache, serialised launches: compare shares, not absolutes).\n\n")
         fh.write("| kernel | launches | mean time / launch (us) | share of step |\n|---|---|---|---|\n")
         for k, v in sorted(per_step.items(), key=lambda kv: -kv[1]):
