@@ -450,6 +450,29 @@ def test_config5_large_roots_sample(R):
     _pyramid_parity(5, R, sel_levels={0, 19, 36})
 
 
+def test_config4_full_image_every_level_and_component():
+    """The benchmarked workload's unit: one whole config-4 image, all 39 root
+    levels x 6 components (234 assemblies).  Totals and every response map
+    to 1e-5 of the float64 oracle; part argmaxes bit-identical to the oracle
+    run on the GPU's own maps (ties <= 1e-4), and against the float64 oracle
+    only at ties (zero errors)."""
+    worst = _pyramid_parity(4, 8, sel_levels=None, images=(0,), n_images=1)
+    assert worst <= 1e-5
+
+
+def test_config5_every_level_R8():
+    """Config 5 (1920x1080, roots up to 15x15) at R = 8 on all 37 root levels."""
+    _pyramid_parity(5, 8, sel_levels=None)
+
+
+def test_config3_every_level_twelve_components():
+    """Config 3 (the 1080-filter bank on one shared rank-16 basis) on all 42
+    root levels for 12 components spread over the 20 models and the 3
+    mirrored pairs of each."""
+    _pyramid_parity(3, 16, sel_levels=None,
+                    comps=[0, 1, 7, 16, 29, 42, 59, 60, 83, 98, 111, 119])
+
+
 def test_tau_compaction_matches_totals():
     wl = synth.workload(2)
     C, G = _shared(2, 8)
