@@ -91,7 +91,7 @@ typedef struct {
   int32_t H, W, pitch, chan_off;
   int32_t h, w, R, nf;
   int32_t nf_pad;    /* filter stride of the core: nf rounded up to 8        */
-  int32_t mode;      /* reserved, 0                                          */
+  int32_t mode;      /* 0: nf filters; 1: rank prefixes (dpm_correlate_prefix) */
   int32_t range_idx; /* >= 0: fold per-map max/min into ranges[range_idx+f]  */
   int32_t pad;
 } dpm_corr_job;
@@ -142,6 +142,24 @@ int dpm_correlate_tc_stack(int h, int w, int R, int nf);
 int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
                      const dpm_corr_tile* strips, int nstrips, int h, int w, int R, int nf,
                      uint32_t* ranges, void* stream);
+
+/* K2 in rank-prefix mode (convolution shortening, paper Algorithm 1;
+ * replaces the reference's _term_stack + cumsum, correlation.py:115-180,
+ * behind cp_partial_stack / correlate3_cp and detect(pruning=True)).
+ * Jobs have mode == 1: the job's nf output maps (s_off, [nf][Ho][pitch]) are
+ * the cumulative rank prefixes 1..nf (nf <= R) of ONE filter whose core is
+ * column 0 of the [h][w][R][nf_pad] block at g_off:
+ *   T_r = sum_{j<w} sum_{i<h} G[i][j][r] P[chan_off + r][y+i][x+j],
+ *   map k-1 = T_0 + ... + T_{k-1}   (FP32, rank order),
+ * one pass over the ranks (the cost of one full correlation).  Tiles are
+ * (job, ty, tx) of dpm_correlate_prefix_tile() output positions; all tiles
+ * of one call have filter height h (1..16; width 1..16).  `ranges` as for
+ * dpm_correlate (slot range_idx + k for map k). */
+int dpm_correlate_prefix_tile(int* tile_w, int* tile_h);
+int dpm_correlate_prefix_check(const dpm_corr_job* jobs, int njobs);
+int dpm_correlate_prefix(const float* P, const float* G, float* S, const dpm_corr_job* jobs,
+                         const dpm_corr_tile* tiles, int ntiles, int h, uint32_t* ranges,
+                         void* stream);
 
 /* Initialise `n` range slots to (-inf, +inf). */
 int dpm_ranges_init(uint32_t* ranges, int n, void* stream);

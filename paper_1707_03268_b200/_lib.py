@@ -82,6 +82,9 @@ _SIGNATURES = {
     "dpm_correlate_tile_shape": (_i32, [_i32, _i32, _vp, _vp]),
     "dpm_correlate": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "dpm_ranges_init": (_i32, [_vp, _i32, _vp]),
+    "dpm_correlate_prefix_tile": (_i32, [_vp, _vp]),
+    "dpm_correlate_prefix_check": (_i32, [_vp, _i32]),
+    "dpm_correlate_prefix": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "dpm_correlate_tc_smem": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
     "dpm_correlate_tc": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "dpm_correlate_tc_core_floats": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),

@@ -71,7 +71,10 @@ def correlate3_cp(img, model, upto_rank=None):
     upto = _checked_upto(model, upto_rank)
     valid_support(img.shape, model.dims)
     C = np.asarray(model.factors_c, dtype=np.float32)
-    (m,) = _run_maps(img, C, [FilterDef(cp_core(model, keep=upto))])
+    # the rank-prefix kernel (one pass over the ranks) gives prefixes 1..upto;
+    # the last is the response -- bit-identical to cp_partial_stack's
+    core = cp_core(model)
+    m = _run_maps(img, C, [FilterDef(core, prefix=k + 1) for k in range(upto)])[-1]
     return ScoreMap(m, cp_multiplications(img.shape, model.dims, upto))
 
 
@@ -81,7 +84,8 @@ def cp_partial_stack(img, model, upto_rank=None):
     upto = _checked_upto(model, upto_rank)
     valid_support(img.shape, model.dims)
     C = np.asarray(model.factors_c, dtype=np.float32)
-    filters = [FilterDef(cp_core(model, keep=k + 1)) for k in range(upto)]
+    core = cp_core(model)
+    filters = [FilterDef(core, prefix=k + 1) for k in range(upto)]
     return np.stack(_run_maps(img, C, filters))
 
 

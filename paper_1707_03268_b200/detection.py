@@ -168,7 +168,10 @@ def _run_detect(levels, C, filters, root_f, part_fs, parts, bias, tau, model_id,
             stats.positions_examined += (rect[1] - rect[0] + 1) * (rect[3] - rect[2] + 1)
     if asms:
         L = levels[0].shape[2]
-        plan = Plan(L, [lv.shape[:2] for lv in levels], C, filters, assemblies=asms,
+        # every filter on every scored level: a rank-prefix family is computed
+        # whole (one pass over the ranks) even when only its last map is read
+        apps = [(a.level_tag, f) for a in asms for f in range(len(filters))]
+        plan = Plan(L, [lv.shape[:2] for lv in levels], C, filters, apps=apps, assemblies=asms,
                     outputs=("totals", "positions"))
         for k, lv in enumerate(levels):
             plan.x_view(0, k).copy_(_t().from_numpy(lv.astype(np.float32)))
@@ -196,15 +199,13 @@ def detect(dec, pyramid, tau, pruning=False, part_prune_mode="kill", model_id="m
         return _detect_pruned(dec, levels, tau, part_prune_mode, model_id, collect_maps)
     start = time.perf_counter()
     stats = DetectStats()
-    # per-filter CP: each filter projects onto its own c columns
+    # per-filter CP: each filter projects onto its own c columns; its
+    # response is the last rank prefix (cp_partial_stack(...)[-1], as the
+    # reference's detect and the pruned path read it)
     cps = [dec.root_cp] + [p.cp for p in dec.parts]
-    C = np.concatenate([np.asarray(cp.factors_c, dtype=np.float32) for cp in cps], axis=1)
-    filters, off = [], 0
-    for cp in cps:
-        filters.append(FilterDef(cp_core(cp), chan_off=off))
-        off += cp.rank
-    dets, rects = _run_detect(levels, C, filters, 0, list(range(1, len(cps))), dec.parts,
-                              dec.bias, tau, model_id, stats)
+    C, filters, pref = _prefix_filters(cps)
+    dets, rects = _run_detect(levels, C, filters, pref[0][-1], [pr[-1] for pr in pref[1:]],
+                              dec.parts, dec.bias, tau, model_id, stats)
     for lv, rect in zip(levels, rects):
         if rect is None:
             continue
@@ -277,12 +278,9 @@ def cp_score_hypothesis(dec, level, hypothesis):
     """Full-rank CP score of a fixed hypothesis (detection.py:164-177)."""
     level = check_feature_map(level, channels=dec.channels)
     cps = [dec.root_cp] + [p.cp for p in dec.parts]
-    C = np.concatenate([np.asarray(cp.factors_c, dtype=np.float32) for cp in cps], axis=1)
-    filters, off = [], 0
-    for cp in cps:
-        filters.append(FilterDef(cp_core(cp), chan_off=off))
-        off += cp.rank
-    maps = _maps_at(level, C, filters)
+    C, filters, pref = _prefix_filters(cps)
+    allmaps = _maps_at(level, C, filters)
+    maps = [allmaps[pr[-1]] for pr in pref]  # cp_partial_stack(...)[-1] (detection.py:164-177)
     ry, rx = hypothesis.root
     score = float(maps[0][ry, rx])
     for part, m, pos in zip(dec.parts, maps[1:], hypothesis.parts):
@@ -296,15 +294,17 @@ def cp_score_hypothesis(dec, level, hypothesis):
 
 def _prefix_filters(cps):
     """Every rank prefix of every CP filter over its own basis columns:
-    prefix k keeps ranks <= k (the cp_partial_stack order, bit-identical
-    prefixes).  Returns (C, filters, pref) with pref[i] the filter indices of
-    CP i's prefixes 1..R_i."""
+    prefix k keeps ranks < k (the cp_partial_stack order, bit-identical
+    prefixes), all of a filter's prefixes from one rank-prefix K2 pass.
+    Returns (C, filters, pref) with pref[i] the filter indices of CP i's
+    prefixes 1..R_i."""
     C = np.concatenate([np.asarray(cp.factors_c, dtype=np.float32) for cp in cps], axis=1)
     filters, pref, off = [], [], 0
     for cp in cps:
         idx = []
+        core = cp_core(cp)  # one family: the rank-prefix kernel writes all R maps in one pass
         for k in range(cp.rank):
-            filters.append(FilterDef(cp_core(cp, keep=k + 1), chan_off=off))
+            filters.append(FilterDef(core, chan_off=off, prefix=k + 1))
             idx.append(len(filters) - 1)
         pref.append(idx)
         off += cp.rank

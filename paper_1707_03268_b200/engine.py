@@ -29,10 +29,16 @@ MAX_GROUP = 48  # filters per K2 group (6 warps x 8 filters)
 
 @dataclass(frozen=True)
 class FilterDef:
-    """Core of one filter over ``R`` consecutive basis channels from ``chan_off``."""
+    """Core of one filter over ``R`` consecutive basis channels from ``chan_off``.
+
+    ``prefix = k >= 1`` makes it the rank-``k`` prefix of ``core`` (ranks < k),
+    computed by the rank-prefix kernel together with the family's other
+    prefixes: a plan must request prefixes 1..K of one core (the same array
+    object) together, and gets all K maps from one pass over the ranks."""
 
     core: np.ndarray  # (h, w, R) float32
     chan_off: int = 0
+    prefix: int = 0
 
     @property
     def h(self):
@@ -168,13 +174,24 @@ class Plan:
         for k, f in sorted(needed):
             by_level.setdefault(k, []).append(f)
         self.groups = []  # (level, (filters...))
+        self._prefix_groups = set()  # groups computed by the rank-prefix kernel
         for k in sorted(by_level):
             keyed = {}
             for f in by_level[k]:
                 fd = self.filters[f]
-                keyed.setdefault((fd.h, fd.w, fd.R, fd.chan_off), []).append(f)
+                fam = id(fd.core) if fd.prefix > 0 else 0  # one rank-prefix family per core
+                keyed.setdefault((fd.h, fd.w, fd.R, fd.chan_off, fam), []).append(f)
             for key in sorted(keyed):
                 fl = keyed[key]
+                if key[4]:  # prefixes 1..K of one core, in rank order, one group
+                    fl = sorted(fl, key=lambda f: self.filters[f].prefix)
+                    ks = [self.filters[f].prefix for f in fl]
+                    if ks != list(range(1, len(fl) + 1)) or len(fl) > MAX_GROUP:
+                        raise ValidationError(f"rank-prefix filters {ks}: a plan computes "
+                                              f"prefixes 1..K (K <= {MAX_GROUP}) of a core together")
+                    self._prefix_groups.add(tuple(fl))
+                    self.groups.append((k, tuple(fl)))
+                    continue
                 for s in range(0, len(fl), MAX_GROUP):
                     self.groups.append((k, tuple(fl[s:s + MAX_GROUP])))
 
@@ -217,7 +234,7 @@ class Plan:
         self.map_off = {}  # (image, level, filt) -> float offset
         self.map_shape = {}
         self.range_slot = {}
-        jobs, classes = [], {}
+        jobs, classes, prefix_classes = [], {}, {}
         job_image = []
         nslots = 0
         self.map_smap = {}  # (image, level, filt) -> (TMA descriptor, index in its group)
@@ -243,9 +260,17 @@ class Plan:
                         self.range_slot[(img, k, f)] = rng + i
                 jid = len(jobs)
                 job_image.append(img)
+                prefix = fl in self._prefix_groups
                 jobs.append((img * self.p_image_stride + self.p_level_off[k], s_off,
                              self.core_off[fl], H, W, self.pitch[k], fd.chan_off, fd.h, fd.w,
-                             fd.R, len(fl), _round_up(len(fl), 8), 0, rng, 0))
+                             fd.R, len(fl), _round_up(len(fl), 8), 1 if prefix else 0, rng, 0))
+                if prefix:  # rank-prefix kernel: tiles per filter height
+                    ptw, pth = self._prefix_tile()
+                    pt = prefix_classes.setdefault(fd.h, [])
+                    for ty in range((ho + pth - 1) // pth):
+                        for tx in range((wo + ptw - 1) // ptw):
+                            pt.append((jid, ty, tx, 0))
+                    continue
                 if fl in self.tc_core_off and wo >= self.tc_min_width:
                     tcc = tc_classes.setdefault(fl, [])
                     for sx in range((wo + 127) // 128):
@@ -269,6 +294,11 @@ class Plan:
             tl = sorted(cls["tiles"], key=lambda t: (jobs[t[0]][2], t[0], t[1], t[2]))
             self._classes.append((h, nf, cls["R"], cls["w_max"], np.array(tl, dtype=_lib.CORR_TILE)))
 
+        self._prefix_classes = [(h, np.array(tl, dtype=_lib.CORR_TILE))
+                                for h, tl in sorted(prefix_classes.items())]
+        if prefix_classes:
+            pjobs = np.ascontiguousarray(self._corr_jobs[self._corr_jobs["mode"] == 1])
+            _lib.check(lib.dpm_correlate_prefix_check(_lib.table_ptr(pjobs), len(pjobs)), "prefix")
         self._tc_classes = []
         for fl, strips in sorted(tc_classes.items()):
             strips = _snake_order(strips, key=lambda t: t[3], ctas=_sm_count())
@@ -348,7 +378,7 @@ class Plan:
         return True
 
     def _tc_eligible(self, fl):
-        if not self.tensor_cores:
+        if not self.tensor_cores or fl in self._prefix_groups:
             return False
         fd = self.filters[fl[0]]
         if fd.R % 8 or not (1 <= len(fl) <= 64) or fd.h + 2 > 16 or \
@@ -357,6 +387,16 @@ class Plan:
         return _lib.lib().dpm_correlate_tc_smem(fd.h, fd.w, fd.R, len(fl)) <= 227 * 1024
 
     _tile_cache = {}
+
+    def _prefix_tile(self):
+        import ctypes
+
+        if "prefix" not in self._tile_cache:
+            tw, th = ctypes.c_int(0), ctypes.c_int(0)
+            _lib.check(_lib.lib().dpm_correlate_prefix_tile(ctypes.byref(tw), ctypes.byref(th)),
+                       "prefix")
+            self._tile_cache["prefix"] = (tw.value, th.value)
+        return self._tile_cache["prefix"]
 
     def _tile_shape(self, h, nf):
         import ctypes
@@ -420,6 +460,10 @@ class Plan:
         for h, nf, R, w_max, tiles in self._classes:
             sub = np.ascontiguousarray(tiles[keep[tiles["job"]]])
             tb["ffma"].append((h, nf, R, w_max, len(sub), upload_table(sub, dev)))
+        tb["prefix"] = []
+        for h, tiles in self._prefix_classes:
+            sub = np.ascontiguousarray(tiles[keep[tiles["job"]]])
+            tb["prefix"].append((h, len(sub), upload_table(sub, dev)))
         in_chunk = np.isin(self._asm_jobs["image"], list(imgs))
         aj = np.ascontiguousarray(self._asm_jobs[in_chunk & ~self._asm_gdt])
         blocks = _lib.check(lib.dpm_assemble_prepare(
@@ -498,6 +542,13 @@ class Plan:
                 _lib.check(lib.dpm_correlate(ptr(self.P), ptr(self.G), ptr(self.S),
                                              ptr(self.corr_jobs_d), ptr(tiles_d), n, h,
                                              nf, R, w_max, rng, s), "correlate")
+            for h, n, tiles_d in tb["prefix"]:
+                if not n:
+                    continue
+                mark(f"k2_prefix_h{h}")
+                _lib.check(lib.dpm_correlate_prefix(ptr(self.P), ptr(self.G), ptr(self.S),
+                                                    ptr(self.corr_jobs_d), ptr(tiles_d), n, h, rng,
+                                                    s), "correlate prefix")
         place = "place" in stages and (tb["asm"][1] or tb["gdt"][4])
         if place and self.det_count is not None and reset_dets:
             with t.cuda.stream(stream if stream is not None else t.cuda.current_stream()):
@@ -567,7 +618,7 @@ class Plan:
     # ------------------------------------------------------------ accounting
     def launches_per_run(self):
         """Kernels of libdpm_b200 one full run() launches."""
-        n = 1 + len(self._tc_classes) + len(self._classes)  # K1, K2 classes
+        n = 1 + len(self._tc_classes) + len(self._classes) + len(self._prefix_classes)  # K1, K2
         n += 1 if self.n_ranges else 0
         if (~self._asm_gdt).any():
             n += 2  # prologue + placement/assembly
@@ -604,6 +655,12 @@ class Plan:
             out[f"k2_tcgen05_{h}x{w}_nf{nf}"] = fl(strips["job"].tolist())
         for h, nf, R, _, tiles in self._classes:
             out[f"k2_ffma_h{h}_nf{nf}"] = fl(tiles["job"].tolist())
+        for h, tiles in self._prefix_classes:
+            # one pass over the ranks: 2*h*w per rank and position (K ranks)
+            out[f"k2_prefix_h{h}"] = sum(
+                2 * int(jobs[j]["h"]) * int(jobs[j]["w"]) * int(jobs[j]["nf"]) *
+                (int(jobs[j]["H"]) - int(jobs[j]["h"]) + 1) * (int(jobs[j]["W"]) - int(jobs[j]["w"]) + 1)
+                for j in set(tiles["job"].tolist()))
         return out
 
     def k1_bytes(self):

@@ -1030,3 +1030,61 @@ def test_batched_apis_score_pyramid_and_detect_batch():
             for iy, ix in zip(*np.nonzero(r["scores"] >= tau)):
                 want.append((img, r["root_level"], r["component"], ry0 + int(iy), rx0 + int(ix)))
     assert got == sorted(want) and len(got) > 0
+
+
+def test_rank_prefix_kernel_one_pass_matches_oracle_and_costs_one_correlation():
+    """Convolution shortening (paper Algorithm 1): the rank-prefix K2 writes
+    every cumulative prefix of a CP filter from one pass over the ranks.
+    Prefixes match the float64 reference stack to 1e-5 (and the oracle's
+    term-then-cumsum restatement on the same FP32 inputs to 2e-6), the last
+    prefix equals correlate3_cp bit for bit, and on config 1 (9 per-filter
+    CP models at R = 8) computing all prefixes costs about one full
+    correlation, not R of them."""
+    import torch
+
+    from paper_1707_03268_b200.correlation import cp_core
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    rng = np.random.default_rng(11)
+    for ishape, dims, rank in [((40, 52, 32), (6, 6, 32), 8), ((30, 33, 7), (3, 5, 7), 5),
+                               ((19, 24, 32), (15, 15, 32), 3), ((9, 9, 4), (1, 1, 4), 4)]:
+        img = rng.normal(size=ishape).astype(np.float32).astype(np.float64)
+        cp = B.CPModel.from_factors(rng.normal(size=(dims[0], rank)), rng.normal(size=(dims[1], rank)),
+                                    rng.normal(size=(dims[2], rank)))
+        stack = B.cp_partial_stack(img, cp)
+        ref = O.cp_partial_stack(img, cp)
+        for r in range(rank):
+            assert_map_close(stack[r], ref[r], f"{dims} prefix {r + 1}")
+        assert np.array_equal(B.correlate3_cp(img, cp).scores, stack[-1])
+
+    # cost on config 1: all 8 prefixes of 9 filters vs the 9 full filters
+    g = load_golden("cfg1.npz")
+    level = synth.hog_level(1, 0, 0, 64, 48)
+    cps = [golden_cp(g, "root")] + [golden_cp(g, f"part{i}") for i in range(8)]
+    C = np.concatenate([np.asarray(c.factors_c, np.float32) for c in cps], axis=1)
+
+    def k2_ms(prefix):
+        filters, off = [], 0
+        for c in cps:
+            core = cp_core(c)
+            if prefix:
+                filters += [FilterDef(core, chan_off=off, prefix=k + 1) for k in range(c.rank)]
+            else:
+                filters.append(FilterDef(core, chan_off=off))
+            off += c.rank
+        plan = Plan(32, [(64, 48)], C, filters, apps=[(0, f) for f in range(len(filters))],
+                    outputs=(), tensor_cores=False)
+        plan.load_levels(0, [level])
+        for _ in range(3):
+            plan.run(stages=("correlate",))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for _ in range(50):
+            plan.run(stages=("correlate",))
+        ev[1].record()
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / 50
+
+    full, pref = k2_ms(False), k2_ms(True)
+    print(f"config 1 K2: full filters {full * 1e3:.1f} us, all rank prefixes {pref * 1e3:.1f} us")
+    assert pref <= 1.5 * full + 0.01, (pref, full)
