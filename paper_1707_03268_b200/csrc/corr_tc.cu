@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
     // Producer warp p stages input rows q = p, p+3, ... of every strip: each
     // lane issues all of its (up to PQ) quad-column loads before converting,
     // so one row costs one memory latency, and three rows are in flight.
-    constexpr int PQ = 10;  // quad-columns per lane: 2 quads x (128 + w - 1) <= 320
+    constexpr int PQ = 10;  // quad-columns per lane per batch (R = 8: one batch per row)
     const int pw = warp - 1;
     uint32_t q_glob = 0;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
@@ -533,31 +533,34 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
           if (lane == 0) mbar_arrive(full + slot);
           continue;
         }
-        float4 v[PQ];
+        // batches of 32 * PQ quad-columns (R > 8: more than one batch per row)
+        for (int e0 = 0; e0 < nelem; e0 += 32 * PQ) {
+          float4 v[PQ];
 #pragma unroll
-        for (int k = 0; k < PQ; ++k) {
-          const int e = lane + 32 * k;
-          v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (e < nelem) {
-            const int quad = e / tcols, c = e - quad * tcols;
-            const int x = x0 + c;
-            if (x < job.W) {
-              const float* p = prow + (int64_t)(4 * quad) * plane + x;
-              v[k].x = __ldg(p);
-              v[k].y = __ldg(p + plane);
-              v[k].z = __ldg(p + 2 * plane);
-              v[k].w = __ldg(p + 3 * plane);
+          for (int k = 0; k < PQ; ++k) {
+            const int e = e0 + lane + 32 * k;
+            v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < nelem) {
+              const int quad = e / tcols, c = e - quad * tcols;
+              const int x = x0 + c;
+              if (x < job.W) {
+                const float* p = prow + (int64_t)(4 * quad) * plane + x;
+                v[k].x = __ldg(p);
+                v[k].y = __ldg(p + plane);
+                v[k].z = __ldg(p + 2 * plane);
+                v[k].w = __ldg(p + 3 * plane);
+              }
             }
           }
-        }
 #pragma unroll
-        for (int k = 0; k < PQ; ++k) {
-          const int e = lane + 32 * k;
-          if (e < nelem) {
-            const float4 h = make_float4(tf32_hi(v[k].x), tf32_hi(v[k].y), tf32_hi(v[k].z),
-                                         tf32_hi(v[k].w));
-            hi[e] = h;
-            lo[e] = make_float4(v[k].x - h.x, v[k].y - h.y, v[k].z - h.z, v[k].w - h.w);
+          for (int k = 0; k < PQ; ++k) {
+            const int e = e0 + lane + 32 * k;
+            if (e < nelem) {
+              const float4 h = make_float4(tf32_hi(v[k].x), tf32_hi(v[k].y), tf32_hi(v[k].z),
+                                           tf32_hi(v[k].w));
+              hi[e] = h;
+              lo[e] = make_float4(v[k].x - h.x, v[k].y - h.y, v[k].z - h.z, v[k].w - h.w);
+            }
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -800,8 +803,7 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
                                 int nf, uint32_t* ranges, void* stream) {
   DPM_REQUIRE(P && Gtc && S && jobs && strips, "dpm_correlate_tc: null pointer");
   DPM_REQUIRE(R % 8 == 0 && R >= 8, "dpm_correlate_tc: R=%d must be a multiple of 8", R);
-  DPM_REQUIRE((R / 4) * (TC_M + w - 1) <= 320, "dpm_correlate_tc: R=%d w=%d exceed the producer "
-              "staging width", R, w);
+  DPM_REQUIRE(R <= 32 && w <= 64, "dpm_correlate_tc: R=%d w=%d outside the staged row", R, w);
   DPM_REQUIRE(nf >= 1 && nf <= 64, "dpm_correlate_tc: nf=%d outside [1, 64]", nf);
   DPM_REQUIRE(h >= 1 && w >= 1 && h + 2 <= TC_MAX_RING, "dpm_correlate_tc: filter %dx%d", h, w);
   if (nstrips == 0) return DPM_OK;

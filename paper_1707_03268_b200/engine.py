@@ -110,7 +110,7 @@ class Plan:
 
     def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
                  outputs=("totals", "positions"), max_dets=0, device=None, tensor_cores=True,
-                 tc_min_width=16, envelope=False):
+                 tc_min_width=16, envelope=False, tc_ranks=(8,)):
         import torch
 
         require_cuda()
@@ -130,6 +130,7 @@ class Plan:
         self.tensor_cores = bool(tensor_cores)
         self.tc_min_width = int(tc_min_width)
         self.envelope = bool(envelope)
+        self.tc_ranks = tuple(int(r) for r in tc_ranks)
         for k, f in enumerate(self.filters):
             if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
                 raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
@@ -192,8 +193,9 @@ class Plan:
                     self._prefix_groups.add(tuple(fl))
                     self.groups.append((k, tuple(fl)))
                     continue
-                for s in range(0, len(fl), MAX_GROUP):
-                    self.groups.append((k, tuple(fl[s:s + MAX_GROUP])))
+                g = self._group_size(*key[:3])
+                for s in range(0, len(fl), g):
+                    self.groups.append((k, tuple(fl[s:s + g])))
 
         # cores: one block per distinct filter tuple
         ga = _Arena()
@@ -377,14 +379,29 @@ class Plan:
                 return False
         return True
 
+    def _tc_fits(self, h, w, R, nf):
+        return (R in self.tc_ranks and R % 8 == 0 and R <= 32 and 1 <= nf <= 64 and
+                h + 2 <= 16 and w <= 64 and
+                _lib.lib().dpm_correlate_tc_smem(h, w, R, nf) <= 227 * 1024)
+
     def _tc_eligible(self, fl):
         if not self.tensor_cores or fl in self._prefix_groups:
             return False
         fd = self.filters[fl[0]]
-        if fd.R % 8 or not (1 <= len(fl) <= 64) or fd.h + 2 > 16 or \
-                (fd.R // 4) * (128 + fd.w - 1) > 320:
-            return False
-        return _lib.lib().dpm_correlate_tc_smem(fd.h, fd.w, fd.R, len(fl)) <= 227 * 1024
+        return self._tc_fits(fd.h, fd.w, fd.R, len(fl))
+
+    def _group_size(self, h, w, R):
+        """Filters per K2 group: MAX_GROUP, or -- when R > 8 is enabled for the
+        tensor cores (``tc_ranks``) -- the largest of 48 / 32 / 16 whose
+        resident tcgen05 core and input ring fit shared memory (R = 16 at
+        6 x 6: 16 filters).  Off by default: the generic-shape tcgen05 kernel
+        measured slower than FFMA there (config 3: 51.8 ms for the 6 x 6 class
+        in 60 16-filter launches against 11.5 ms FFMA)."""
+        if self.tensor_cores and R > 8:
+            for g in (48, 32, 16):
+                if self._tc_fits(h, w, R, g):
+                    return g
+        return MAX_GROUP
 
     _tile_cache = {}
 

@@ -495,16 +495,20 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
     from paper_1707_03268_b200.engine import FilterDef, Plan
 
     rng = np.random.default_rng(11)
+    # the last two: the generic-shape kernel at R = 16 (multi-batch input-row
+    # staging; enabled per plan with tc_ranks, off by default)
     for H, W, nf, h, w, R in [(40, 300, 48, 6, 6, 8), (23, 130, 16, 6, 6, 8),
                               (17, 200, 33, 5, 7, 8), (12, 70, 64, 3, 4, 8),
-                              (30, 150, 6, 6, 11, 8), (9, 90, 1, 2, 3, 8)]:
+                              (30, 150, 6, 6, 11, 8), (9, 90, 1, 2, 3, 8),
+                              (26, 260, 16, 6, 6, 16), (14, 140, 7, 5, 8, 16)]:
         level = rng.random((H, W, 32)).astype(np.float32)
         C = rng.normal(size=(32, R)).astype(np.float32)
         cores = [rng.normal(0, 0.05, (h, w, R)).astype(np.float32) for _ in range(nf)]
         plans = []
         for tc in (True, False):
             plan = Plan(32, [(H, W)], C, [FilterDef(c) for c in cores],
-                        apps=[(0, f) for f in range(nf)], outputs=(), tensor_cores=tc)
+                        apps=[(0, f) for f in range(nf)], outputs=(), tensor_cores=tc,
+                        tc_ranks=(8, 16))
             assert bool(plan._tc_classes) == tc
             plan.load_levels(0, [level])
             plan.run(stages=("project", "correlate"))
