@@ -161,6 +161,36 @@ int dpm_correlate_prefix(const float* P, const float* G, float* S, const dpm_cor
                          const dpm_corr_tile* tiles, int ntiles, int h, uint32_t* ranges,
                          void* stream);
 
+/* ------------------------------- HOG feature pyramid
+ * Generalises the reference's 9-bin demo extractor (features.py:16-68) to
+ * the 32-channel DPM v5 layout on the pyramid geometry the planner uses
+ * (oracle/hog_oracle.py states the algorithm).  Images are [H][W][C]
+ * (C = 1..4, uint8 or float32 in [0, 255]).
+ * dpm_resample: level image = box-filter resampling to Hs x Ws (Hs <= H,
+ * Ws <= W), float32 [Hs][Ws][C] at out_off.  dpm_hog: 4 x 4-pixel cells of
+ * a resampled image -> the level's X block [Hs/4][Ws/4][32] at x_off;
+ * `hist` is scratch of 20 floats per cell at h_off. */
+typedef struct {
+  int64_t img_off;  /* element offset of the image                          */
+  int64_t out_off;  /* float offset of the resampled level                  */
+  int32_t H, W, C, Hs, Ws;
+  int32_t block0;   /* set by dpm_resample_prepare                          */
+} dpm_resample_job;
+int64_t dpm_resample_prepare(dpm_resample_job* jobs_host, int njobs);
+int dpm_resample(const void* img, int u8, float* out, const dpm_resample_job* jobs, int njobs,
+                 int64_t nblocks, void* stream);
+
+typedef struct {
+  int64_t r_off;    /* float offset of the resampled level [Hs][Ws][C]      */
+  int64_t x_off;    /* float offset of the level's X block [Hs/4][Ws/4][32] */
+  int64_t h_off;    /* float offset of the histogram scratch (20 per cell)  */
+  int32_t Hs, Ws, C;
+  int32_t block0;   /* set by dpm_hog_prepare                               */
+} dpm_hog_job;
+int64_t dpm_hog_prepare(dpm_hog_job* jobs_host, int njobs);
+int dpm_hog(const float* R, float* hist, float* X, const dpm_hog_job* jobs, int njobs,
+            int64_t nblocks, void* stream);
+
 /* Initialise `n` range slots to (-inf, +inf). */
 int dpm_ranges_init(uint32_t* ranges, int n, void* stream);
 

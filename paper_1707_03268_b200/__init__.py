@@ -10,7 +10,8 @@ Reference-compatible entry points (``cpdetect.correlation`` /
   K4 assemble   - root + shifted parts + bias, tau compaction
 
 ``PyramidScorer`` batches whole pyramids of many images through one launch
-per kernel.  There is no CPU fallback.
+per kernel; ``features`` builds the 32-channel HOG pyramids of raw images
+on the device.  There is no CPU fallback.
 """
 
 from .correlation import (ScoreMap, correlate3_cp, correlate3_full, cp_multiplications,
@@ -22,6 +23,7 @@ from .detection import (_placement_grid, best_part_placement, calibrate_threshol
 from . import formats  # noqa: F401
 from .evaluation import RocPoint, match_detections, nms, nms_records, roc_eval
 from .errors import CpdetectError, DeviceError, FormatError, NumericError, ValidationError
+from .features import HogBuilder, extract_hog_pyramid
 from .pipeline import PyramidScorer, cores_from_stacked, detect_batch, score_pyramid
 from .types import (CPModel, DecomposedModel, DecomposedPart, Detection, DetectStats,
                     Hypothesis, PartModel, PartSpec)
@@ -37,5 +39,6 @@ __all__ = [
     "dense_detect", "detect",
     "calibrate_thresholds", "score_pyramid", "detect_batch", "nms", "nms_records", "match_detections", "roc_eval",
     "RocPoint", "full_multiplications", "score_hypothesis", "theoretical_gain",
+    "HogBuilder", "extract_hog_pyramid",
     "valid_support", "validate",
 ]

@@ -60,11 +60,16 @@ MIX_JOB = np.dtype([("out_off", "<i8"), ("ry0", "<i4"), ("ry1", "<i4"), ("rx0", 
 SMAP_DESC = np.dtype([("s_off", "<i8"), ("Ho", "<i4"), ("Wo", "<i4"), ("nf", "<i4"),
                       ("pad", "<i4")], align=True)
 SMAP_BYTES = 128
+RESAMPLE_JOB = np.dtype([("img_off", "<i8"), ("out_off", "<i8"), ("H", "<i4"), ("W", "<i4"),
+                         ("C", "<i4"), ("Hs", "<i4"), ("Ws", "<i4"), ("block0", "<i4")],
+                        align=True)
+HOG_JOB = np.dtype([("r_off", "<i8"), ("x_off", "<i8"), ("h_off", "<i8"), ("Hs", "<i4"),
+                    ("Ws", "<i4"), ("C", "<i4"), ("block0", "<i4")], align=True)
 
 _SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 96, "ASM_JOB": 88,
           "SMAP_DESC": 24,
           "DETECTION": 96, "PLACE_RANGE": 16, "PRUNE_JOB": 64,
-          "MIX_JOB": 40}
+          "MIX_JOB": 40, "RESAMPLE_JOB": 40, "HOG_JOB": 40}
 for _n, _s in _SIZES.items():
     assert globals()[_n].itemsize == _s, (_n, globals()[_n].itemsize)
 
@@ -105,6 +110,10 @@ _SIGNATURES = {
     "dpm_mixture_prepare": (_i64, [_vp, _i32]),
     "dpm_mixture_max": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
     "dpm_ffma_probe": (_i32, [_vp, _i32, _vp, _vp]),
+    "dpm_resample_prepare": (_i64, [_vp, _i32]),
+    "dpm_resample": (_i32, [_vp, _i32, _vp, _vp, _i32, _i64, _vp]),
+    "dpm_hog_prepare": (_i64, [_vp, _i32]),
+    "dpm_hog": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp]),
 }
 
 _lib = None

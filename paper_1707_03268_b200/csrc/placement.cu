@@ -655,6 +655,7 @@ extern "C" int dpm_assemble(const float* S, const void* smaps, const dpm_place_j
 // link); host only, no context work.
 extern "C" int dpm_smap_encode(const float* S, const dpm_smap_desc* descs, int n, void* maps_host) {
   DPM_REQUIRE(S && (n == 0 || (descs && maps_host)), "dpm_smap_encode: null pointer");
+  if (n == 0) return DPM_OK;
   DPM_REQUIRE((reinterpret_cast<uintptr_t>(S) & 15) == 0, "dpm_smap_encode: S must be 16-byte aligned");
   DPM_REQUIRE((reinterpret_cast<uintptr_t>(maps_host) & 63) == 0,
               "dpm_smap_encode: maps_host must be 64-byte aligned");
