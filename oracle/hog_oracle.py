@@ -9,11 +9,12 @@ energy normalisation), which this generalises to the DPM v5 feature layout
 geometry.build_pyramid.  The algorithm, restated here and in
 csrc/hog.cu:
 
-pyramid   level k of an H x W image: the image resampled to
-          floor(H 2^-k/10) x floor(W 2^-k/10) pixels (area averaging), cut
-          into 4 x 4-pixel cells -> floor(H 2^-k/10 / 4) x ... cells, the
-          shape build_pyramid gives level k (root levels 8-px cells of the
-          same image are levels k + 10);
+pyramid   level k of an H x W image: resampled to floor(H 2^-k/10) x
+          floor(W 2^-k/10) pixels (area averaging; levels 0..9 from the
+          image, level k >= 10 from level k-10's resampled image, one octave
+          up), cut into 4 x 4-pixel cells -> floor(H 2^-k/10 / 4) x ...
+          cells, the shape build_pyramid gives level k (root levels 8-px
+          cells of the same image are levels k + 10);
 resample  separable box filter: output pixel o of an axis covers the input
           interval [o s, (o+1) s), s = n_in / n_out; input pixel i weighs
           min(i+1, (o+1)s) - max(i, o s); rows first, then columns, then
@@ -189,13 +190,17 @@ def hog32(R):
 
 
 def hog_pyramid(img, n_levels, interval=10):
-    """Levels 0..n_levels-1 of the pyramid of img (H, W[, C]) in [0, 255]."""
+    """Levels 0..n_levels-1 of the pyramid of img (H, W[, C]) in [0, 255].
+    Octave-recursive resampling: levels 0..interval-1 from the image, level
+    k >= interval from level k - interval's resampled image."""
     img = np.asarray(img, dtype=np.float32)
     if img.ndim == 2:
         img = img[:, :, None]
     H, W, _ = img.shape
-    out = []
+    res, out = [], []
     for k in range(n_levels):
         Hs, Ws = level_size(H, W, k, interval)
-        out.append(hog32(resample_area(img, Hs, Ws)))
+        src = img if k < interval else res[k - interval]
+        res.append(resample_area(src, Hs, Ws))
+        out.append(hog32(res[k]))
     return out

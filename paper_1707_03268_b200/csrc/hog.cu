@@ -5,9 +5,10 @@
 // pyramid geometry of geometry.build_pyramid; oracle/hog_oracle.py states
 // the algorithm and is the parity checker.
 //
-//   dpm_resample : level k = the image box-filter resampled to
-//                  floor(H 2^-k/10) x floor(W 2^-k/10) pixels (uint8 or
-//                  float32 input, all levels from the original image);
+//   dpm_resample : level k = box-filter resampled to floor(H 2^-k/10) x
+//                  floor(W 2^-k/10) pixels -- levels 0..9 from the image
+//                  (uint8 or float32), level k >= 10 from level k-10's
+//                  resampled image (one launch per octave wave);
 //   dpm_hog      : per-pixel gradient (max-magnitude colour channel,
 //                  clamped central differences) and 18-way orientation,
 //                  bilinear soft binning into 4x4-pixel cells, the 4

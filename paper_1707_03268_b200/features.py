@@ -56,7 +56,7 @@ class HogBuilder:
             raise ValidationError(f"HOG features have 32 channels, the plan expects {plan.L}")
         self.H, self.W, self.C = H, W, C
         n = plan.n_images
-        rs, hg = [], []
+        rs, hg, wave, lvl_off = [], [], [], {}
         r_off = h_off = 0
         for img in range(n):
             for k, (hc, wc) in enumerate(plan.levels):
@@ -65,31 +65,43 @@ class HogBuilder:
                     raise ValidationError(
                         f"pyramid level {k}: {hc}x{wc} cells, but a {H}x{W} image gives "
                         f"{Hs // SBIN}x{Ws // SBIN} at 2^-{k}/{interval}")
-                rs.append((img * H * W * C, r_off, H, W, C, Hs, Ws, 0))
+                # octave-recursive: levels 0..interval-1 from the image, level
+                # k from level k - interval (wave k // interval)
+                if k < interval:
+                    rs.append((img * H * W * C, r_off, H, W, C, Hs, Ws, 0))
+                else:
+                    src, sh, sw = lvl_off[(img, k - interval)]
+                    rs.append((src, r_off, sh, sw, C, Hs, Ws, 0))
+                lvl_off[(img, k)] = (r_off, Hs, Ws)
+                wave.append(k // interval)
                 hg.append((r_off, img * plan.x_image_stride + plan.x_level_off[k], h_off, Hs, Ws,
                            C, 0))
                 r_off += Hs * Ws * C
                 h_off += hc * wc * 20
         self._rs = np.array(rs, dtype=_lib.RESAMPLE_JOB)
         self._hg = np.array(hg, dtype=_lib.HOG_JOB)
+        self._wave = np.array(wave, dtype=np.int64)
         self._img_of = np.repeat(np.arange(n), len(plan.levels))
         self._tables = {}
         self.R = torch.empty(max(r_off, 1), dtype=torch.float32, device=plan.device)
         self.hist = torch.empty(max(h_off, 1), dtype=torch.float32, device=plan.device)
 
     def _table(self, images):
-        """Job tables of an image range (cached): (resample, n, blocks, hog, n, blocks)."""
+        """Job tables of an image range (cached): ([(resample wave table, n,
+        blocks)], hog table, n, blocks)."""
         key = (images.start, images.stop)
         if key not in self._tables:
             lib = _lib.lib()
-            sel = (self._img_of >= images.start) & (self._img_of < images.stop)
-            rs = np.ascontiguousarray(self._rs[sel])
-            hg = np.ascontiguousarray(self._hg[sel])
-            rb = _lib.check(lib.dpm_resample_prepare(_lib.table_ptr(rs), len(rs)), "resample")
-            hb = _lib.check(lib.dpm_hog_prepare(_lib.table_ptr(hg), len(hg)), "hog")
             dev = self.plan.device
-            self._tables[key] = (upload_table(rs, dev), len(rs), rb, upload_table(hg, dev),
-                                 len(hg), hb)
+            sel = (self._img_of >= images.start) & (self._img_of < images.stop)
+            waves = []
+            for w in range(int(self._wave.max()) + 1 if len(self._wave) else 0):
+                rs = np.ascontiguousarray(self._rs[sel & (self._wave == w)])
+                rb = _lib.check(lib.dpm_resample_prepare(_lib.table_ptr(rs), len(rs)), "resample")
+                waves.append((upload_table(rs, dev), len(rs), rb))
+            hg = np.ascontiguousarray(self._hg[sel])
+            hb = _lib.check(lib.dpm_hog_prepare(_lib.table_ptr(hg), len(hg)), "hog")
+            self._tables[key] = (waves, upload_table(hg, dev), len(hg), hb)
         return self._tables[key]
 
     def image_bytes(self, dtype="uint8"):
@@ -109,9 +121,11 @@ class HogBuilder:
                                   "plan's device")
         lib = _lib.lib()
         s = stream_handle(stream)
-        rs_d, nrs, rb, hg_d, nhg, hb = self._table(chunk or range(self.plan.n_images))
-        _lib.check(lib.dpm_resample(images.data_ptr(), int(images.dtype == t.uint8),
-                                    self.R.data_ptr(), rs_d.data_ptr(), nrs, rb, s), "resample")
+        waves, hg_d, nhg, hb = self._table(chunk or range(self.plan.n_images))
+        for w, (rs_d, nrs, rb) in enumerate(waves):  # wave 0 reads the images, wave w > 0 wave w-1
+            src, u8 = (images, int(images.dtype == t.uint8)) if w == 0 else (self.R, 0)
+            _lib.check(lib.dpm_resample(src.data_ptr(), u8, self.R.data_ptr(), rs_d.data_ptr(),
+                                        nrs, rb, s), "resample")
         _lib.check(lib.dpm_hog(self.R.data_ptr(), self.hist.data_ptr(), self.plan.X.data_ptr(),
                                hg_d.data_ptr(), nhg, hb, s), "hog")
         return self
