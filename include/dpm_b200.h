@@ -260,12 +260,14 @@ int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs, const dpm_place_
                              int npjobs);
 
 /* K3 prologue, once per run after K2: per placement job, the radius on each
- * axis (the job's radius, or r* from its map range when radius < 0) and the
- * FP32 screening bound E2 (see placement.cu). */
+ * axis (the job's radius, or r* from its map range when radius < 0), the
+ * FP32 screening bound E2 = 2^-15 (max|S| + max |pen_x| + max |pen_y|) over
+ * the whole window (see placement.cu) and E2in, the same over the inner
+ * window |d| <= min(r, 6) that place2.cu screens. */
 typedef struct {
   int32_t rx, ry;
   float E2;
-  int32_t pad;
+  float E2in;
 } dpm_place_range;
 int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uint32_t* ranges,
                      dpm_place_range* prep, void* stream);

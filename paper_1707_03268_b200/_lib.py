@@ -47,7 +47,7 @@ DETECTION = np.dtype([("image", "<i4"), ("level", "<i4"), ("component", "<i4"), 
                       ("rx", "<i4"), ("nparts", "<i4"), ("score", "<f8"),
                       ("parts", "<u4", (MAX_PARTS,))], align=True)
 
-PLACE_RANGE = np.dtype([("rx", "<i4"), ("ry", "<i4"), ("E2", "<f4"), ("pad", "<i4")], align=True)
+PLACE_RANGE = np.dtype([("rx", "<i4"), ("ry", "<i4"), ("E2", "<f4"), ("E2in", "<f4")], align=True)
 PRUNE_JOB = np.dtype([("out_off", "<i8"), ("offs0", "<i4"), ("thr0", "<i4"), ("R", "<i4"),
                       ("Hp", "<i4"), ("Wp", "<i4"), ("ry0", "<i4"), ("ry1", "<i4"),
                       ("rx0", "<i4"), ("rx1", "<i4"), ("ay", "<i4"), ("ax", "<i4"),

@@ -24,8 +24,9 @@
 //
 // Screen values carry the candidate's code in their 4 low mantissa bits
 // (16 ulps).  E2x = 2^-17 M and E2y = 2^-16 M (M = max|S| + the largest
-// penalties, E2 = 2^-15 M from the prologue) cover twice the FP32 error
-// plus the encodings, so m2 < m1 - E2 proves the winner exact.  The x result
+// penalties of the inner windows, E2in = 2^-15 M from the prologue) cover
+// twice the FP32 error plus the encodings, so m2 < m1 - E2 proves the winner
+// exact; the outer-bound comparisons add the full-window margin.  The x result
 // of a row is one 32-bit word: the winner's screen value with the x code in
 // its low 4 bits (13 = no candidate, 14 = a row resolved by an exact scan,
 // whose dx the y pass recovers by the same exact scan from global memory),
@@ -62,6 +63,7 @@ constexpr int CODE_NONE = 13;               // x word: no candidate in the windo
 constexpr int CODE_RARE = 14;               // x word: winner from an exact scan
 constexpr int TD = 36;                      // table stride: index d + 16, d in [-16, 16]
 static_assert(2 * R1MAX + 1 <= CODE_NONE, "inner codes fit below the special codes");
+static_assert(R1MAX == 6, "the prologue's E2in (place_common.cuh) is computed for |d| <= 6");
 
 struct PartTab {
   float npx[TD];    // FP32 screen penalty -pen_x(d) at [d + 16]
@@ -70,7 +72,7 @@ struct PartTab {
   double px[33];    // exact FP64 pen_x(d) at [d + 16] (reference expression)
   double py[33];
   float out_x, out_y;  // max screen penalty over the outer offsets
-  float E2x, E2y;
+  float E2x, E2y, E2o;
 };
 
 struct __align__(128) Smem {
@@ -265,7 +267,7 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
                                        const PartTab& tb, uint32_t* __restrict__ rmask, int lane,
                                        int rb0, int r_hi, int step, int xsub, int xc, int lpr,
                                        int wt, int reach, int c0, int scale, XDec xd, int rx,
-                                       uint32_t mask, float& cmaxv) {
+                                       uint32_t mask, float& cmaxv, int rin_lo, int rin_hi) {
   const float E2 = tb.E2x;
   float pr[2 * R1 + 1];
   unsigned long long pp[R1 > 0 ? R1 : 1];
@@ -284,6 +286,25 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
   const int cstep = PACKED ? 2 : scale;
   uint32_t iters = 0;  // bit i: iteration i flagged a rare row
   int it = 0;
+  // maximum of band row r over the columns this row's windows reach
+  auto rowmax = [&](int r) {
+    const float* row = band + r * COLS_PITCH;
+    float mr;
+    if constexpr (FULLW) {
+      const float a = row[xsh + xc];
+      const float b = xc + 32 < reach ? row[xsh + xc + 32] : -INFINITY;
+      const float c = xc + 64 < reach ? row[xsh + xc + 64] : -INFINITY;
+      const float l = fmaxf(a, fmaxf(b, c));
+      asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(l));
+    } else {
+      mr = -INFINITY;
+      for (int c = xc; c < reach; c += lpr) mr = fmaxf(mr, row[xsh + c]);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1)
+        if (o < lpr) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    }
+    return mr;
+  };
   // screen of band row r (m1, m2, outer bound failed)
   auto screen = [&](int r, float& m1, float& m2, bool& full) {
     const float* row = band + r * COLS_PITCH;
@@ -291,24 +312,7 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
     if constexpr (PACKED) scr_packed<R1>(s0 + xd.d0, pp, s0[xd.ds] + pr[0], mask, m1, m2);
     else scr_strided<R1, 1>(s0, pr, mask, m1, m2);
     full = false;
-    if constexpr (OUTER) {
-      // maximum of the band row over the columns this row's windows reach
-      float mr;
-      if constexpr (FULLW) {
-        const float a = row[xsh + xc];
-        const float b = xc + 32 < reach ? row[xsh + xc + 32] : -INFINITY;
-        const float c = xc + 64 < reach ? row[xsh + xc + 64] : -INFINITY;
-        const float l = fmaxf(a, fmaxf(b, c));
-        asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(l));
-      } else {
-        mr = -INFINITY;
-        for (int c = xc; c < reach; c += lpr) mr = fmaxf(mr, row[xsh + c]);
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1)
-          if (o < lpr) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
-      }
-      full = mr + out >= m1 - E2;
-    }
+    if constexpr (OUTER) full = rowmax(r) + out + tb.E2o >= m1 - E2;
   };
   // flag / store the screen result of row r (loop iteration it)
   auto finish = [&](int r, bool live, int it, float m1, float m2, bool full) {
@@ -364,7 +368,7 @@ __device__ __forceinline__ void y_group(const float* __restrict__ x32, const flo
   float pr[2 * R1 + 1];
 #pragma unroll
   for (int d = -R1; d <= R1; ++d) pr[d + R1] = tb.npy[d + 16];
-  const float bound = OUTER ? cmax + tb.out_y : -INFINITY;  // outer rows of this column
+  const float bound = OUTER ? cmax + tb.out_y + tb.E2o : -INFINITY;  // outer rows of this column
   const int scale = pjs->scale, ay = pjs->ay, ax = pjs->ax;
   // phase 1: screen every root, start the S loads of the certified winners.
   // st = state (0 dead, 1 certified, 2 exact inner scan, 3 exact full scan,
@@ -491,8 +495,13 @@ __device__ __forceinline__ void build_tab(PartTab& tb, const dpm_place_job& pj, 
   if (lane == 0) {
     tb.out_x = rmx;
     tb.out_y = rmy;
-    tb.E2x = jr.E2 * 0.25f;  // 2^-17 M
-    tb.E2y = jr.E2 * 0.5f;   // 2^-16 M
+    // screened values are bounded by M = max|S| + the inner windows' largest
+    // penalties (E2in = 2^-15 M from the prologue; the full-window E2 covers
+    // the outer-bound comparisons): E2x = 2^-17 M (4-bit codes), E2y =
+    // 2^-16 M (the x words' codes too)
+    tb.E2x = jr.E2in * 0.25f;
+    tb.E2y = jr.E2in * 0.5f;
+    tb.E2o = jr.E2 * 0.25f;
   }
 }
 
@@ -645,7 +654,9 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
       const int reach = pj.scale * (wt - 1) + 1 + 2 * rx;  // band columns the windows reach
       float cmaxv = n_out > 0 ? sent : -INFINITY;
       const bool outer = rx > R1MAX;
-#define DPM_XARGS x32, sh.s, tb, sh.rmask[warp], lane, rb0, r_hi, step, xsub, xc, lpr, wt, reach, c0, pj.scale, xd, rx, mask, cmaxv
+      // band rows some root's inner y window (|dy| <= min(ry, R1MAX)) reaches
+      const int rin_lo = ry - r1y, rin_hi = nrows - 1 - (ry - r1y);
+#define DPM_XARGS x32, sh.s, tb, sh.rmask[warp], lane, rb0, r_hi, step, xsub, xc, lpr, wt, reach, c0, pj.scale, xd, rx, mask, cmaxv, rin_lo, rin_hi
       if (pj.scale == 2) {
         if (outer) {
           if (lpr == 32) x_pass<R1MAX, true, true, true>(DPM_XARGS);

@@ -60,7 +60,9 @@ __device__ __forceinline__ JobRange job_range(const dpm_place_job& pj, const uin
   jr.E2 = (float)fmax(ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, jr.rx) +
                                 pen_absmax(pj.cdy, pj.cdyy, jr.ry), -15),
                       0x1p-120);
-  jr.pad = 0;
+  jr.E2in = (float)fmax(ldexp(mabs + pen_absmax(pj.cdx, pj.cdxx, min(jr.rx, 6)) +
+                                  pen_absmax(pj.cdy, pj.cdyy, min(jr.ry, 6)), -15),
+                        0x1p-120);
   return jr;
 }
 

@@ -47,7 +47,7 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
         "dpm_smap_desc": ("s_off", "Ho", "Wo", "nf", "pad"),
         "dpm_asm_job": ("root_off", "placed_off", "root_pitch", "block0", "bias"),
         "dpm_detection": ("image", "score", "parts"),
-        "dpm_place_range": ("rx", "ry", "E2", "pad"),
+        "dpm_place_range": ("rx", "ry", "E2", "E2in"),
         "dpm_prune_job": ("out_off", "offs0", "thr0", "R", "Hp", "ry0", "rx1", "scale", "radius",
                           "block0"),
     }
