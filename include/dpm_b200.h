@@ -28,7 +28,11 @@
  *    pitch = (Wo + 3) & ~3 (rows padded to 16 bytes; the padding is never
  *    read as data).  Map offsets (s_off) are multiples of 4 floats.  Every
  *    kernel that reads or writes S uses this pitch; descriptor fields named
- *    Wp / Wo hold the valid width.  (ABI version 2.)
+ *    Wp / Wo hold the valid width.  (Since ABI version 2.)
+ *
+ * ABI version 3: dpm_place_range carries E2in (was a pad field); added the
+ * rank-prefix K2 (dpm_correlate_prefix*, dpm_corr_job.mode = 1) and the HOG
+ * pyramid builder (dpm_resample*, dpm_hog*).
  */
 #ifndef DPM_B200_H
 #define DPM_B200_H
@@ -40,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DPM_ABI_VERSION 2
+#define DPM_ABI_VERSION 3
 #define DPM_MAX_PARTS 16
 
 typedef enum {

@@ -18,7 +18,7 @@ __all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "AS
 LIB_PATH = os.environ.get("DPM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                                                    "libdpm_b200.so")
 MAX_PARTS = 16
-ABI_VERSION = 2  # DPM_ABI_VERSION of include/dpm_b200.h
+ABI_VERSION = 3  # DPM_ABI_VERSION of include/dpm_b200.h
 
 DPM_OK, DPM_ERR_ARG, DPM_ERR_UNSUPPORTED, DPM_ERR_CUDA, DPM_ERR_NUMERIC = 0, -1, -2, -3, -4
 

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 11
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.dpm_abi_version() == _lib.ABI_VERSION == 2
+    assert lib.dpm_abi_version() == _lib.ABI_VERSION == 3
 
 
 def test_struct_sizes_match_header_comments():
