@@ -233,7 +233,35 @@ struct XDec {  // decoding of the x codes of one part in one tile
 // << 8, or -1 when no row has a candidate.
 __device__ __noinline__ int y_exact(const float* xcol, const float* __restrict__ smap, int pitch,
                                     int cy, int cx, int lo, int hi, int Wp, const PartTab* tb,
-                                    XDec xd, int rx, float thr, uint32_t mask, int r1) {
+                                    XDec xd, int rx, float thr, uint32_t mask, int r1, int ta,
+                                    int tb2) {
+  // Two-row near tie (the common case): when exactly rows ta and tb2 (the
+  // screen's top two) reach thr and both carry inner x codes, their two S
+  // loads are issued together -- one L2 round trip, not one per row.
+  if (ta <= hi && tb2 <= hi) {
+    int n = 0;
+    for (int dy = lo; dy <= hi; ++dy) {
+      const float w = xcol[dy * PT_W];
+      if (code_of(w) != CODE_NONE && enc_idx_rt(w + tb->npy[dy + 16], mask, dy + r1) >= thr) ++n;
+    }
+    const float wa = xcol[ta * PT_W], wb = xcol[tb2 * PT_W];
+    const int ca = code_of(wa), cb = code_of(wb);
+    if (n == 2 && ca <= 12 && cb <= 12 && ta != tb2) {
+      const int da = ca == xd.c2r1 ? xd.ds : xd.d0 + ca;
+      const int db = cb == xd.c2r1 ? xd.ds : xd.d0 + cb;
+      const float sa = __ldg(smap + (int64_t)(cy + ta) * pitch + cx + da);
+      const float sb = __ldg(smap + (int64_t)(cy + tb2) * pitch + cx + db);
+      const double ea = __dadd_rn(__dadd_rn((double)sa, -tb->px[da + 16]), -tb->py[ta + 16]);
+      const double eb = __dadd_rn(__dadd_rn((double)sb, -tb->px[db + 16]), -tb->py[tb2 + 16]);
+      // the reference's order: ascending dy, strict '>'
+      const bool a_first = ta < tb2;
+      const double e1 = a_first ? ea : eb, e2 = a_first ? eb : ea;
+      const int d1 = a_first ? ta : tb2, d2 = a_first ? tb2 : ta;
+      const int x1 = a_first ? da : db, x2 = a_first ? db : da;
+      if (e2 > e1) return (d2 + 64) | ((x2 + 64) << 8);
+      if (e1 > -INFINITY) return (d1 + 64) | ((x1 + 64) << 8);
+    }
+  }
   double best = -INFINITY;
   int out = -1;
   for (int dy = lo; dy <= hi; ++dy) {
@@ -394,8 +422,10 @@ __device__ __forceinline__ void y_group(const float* __restrict__ x32, const flo
     } else if (m1 < NONE_BELOW) {
       stk = 4;
     } else if (m2 >= lo) {
-      stk = 2;
-      sv[g] = lo;  // rescan only the rows whose screen value reaches lo
+      // rescan only the rows whose screen value reaches lo; the two top rows
+      // (codes of m1, m2) ride along for the common two-row near tie
+      stk = 2 | ((code_of(m1) - R1 + 64) << 3) | ((code_of(m2) - R1 + 64) << 10);
+      sv[g] = lo;
     } else {
       const int dy = code_of(m1) - R1;
       const int c = code_of(xcol[dy * PT_W]);
@@ -429,7 +459,8 @@ __device__ __forceinline__ void y_group(const float* __restrict__ x32, const flo
         const float* xcol = x32 + (cy - yb0) * PT_W + ixr;
         const int q = y_exact(xcol, smap, pitch, cy, cx, state == 2 ? -R1 : -ry,
                               state == 2 ? R1 : ry, pjs->Wp, &tb, xd, rx,
-                              state == 2 ? sv[g] : -INFINITY, mask, R1);
+                              state == 2 ? sv[g] : -INFINITY, mask, R1,
+                              state == 2 ? dy : 1000, state == 2 ? dx : 1000);
         if (q < 0) {
           state = 4;
         } else {
