@@ -32,13 +32,15 @@
 // whose dx the y pass recovers by the same exact scan from global memory),
 // so the x loop stores its screen maximum as is.
 //
-// Structure.  CTA = 8 warps, 32 x 64 root tile of one (image, component,
-// root level), two CTAs per SM.  Per part:
+// Structure.  CTA = 12 warps, 32 x 48 root tile of one (image, component,
+// root level), two CTAs per SM (80 registers: 24 warps per SM measured
+// faster than 16 warps at 128 registers -- 7.77 against 8.05 ms -- and than
+// 32 at 64, which spills).  Per part:
 //   wait for the part's S band (TMA boxes, NaN outside the map, mbarrier),
 //   x pass over the band rows (lane = centre column), per-warp column maxima,
 //   one CTA barrier (x words complete, band buffer free, the next part's job
 //   record and tables visible) -> thread 0 issues the next part's band,
-//   y pass for the thread's 8 roots: screen the x words of the column; the
+//   y pass for the thread's 4 roots: screen the x words of the column; the
 //   winner's exact FP64 value from its S value in global memory (L2
 //   resident: the TMA just streamed it), so the y pass never reads the band
 //   and the next band lands underneath it.
@@ -53,10 +55,11 @@
 namespace dpm {
 namespace k3v2 {
 
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;
 constexpr int WARPS = THREADS / 32;
 constexpr int TH = 48;                      // root rows per tile (32 columns)
-constexpr int RPT = TH * PT_W / THREADS;    // roots per thread (6)
+constexpr int RPT = TH * PT_W / THREADS;    // roots per thread
+static_assert(RPT * THREADS == TH * PT_W, "whole roots per thread");
 constexpr int BAND2 = (2 * (TH - 1) + 1 + 2 * RCAP + TMA_BH - 1) / TMA_BH * TMA_BH;  // 128 band rows
 constexpr int R1MAX = 6;                    // inner screen radius
 constexpr int CODE_NONE = 13;               // x word: no candidate in the window
@@ -494,10 +497,12 @@ __device__ __forceinline__ void y_pass(const float* __restrict__ x32, const floa
                                        uint32_t mask, RootOf root_of, const dpm_asm_job& aj, int p,
                                        int hr, int wr, double* __restrict__ tot, uint32_t* posb,
                                        double* placedb, float cmax) {
-  y_group<R1, OUTER, 0, 3>(x32, smap, pitch, pjs, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj,
-                           p, hr, wr, tot, posb, placedb, cmax);
-  y_group<R1, OUTER, 3, 3>(x32, smap, pitch, pjs, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj,
-                           p, hr, wr, tot, posb, placedb, cmax);
+  constexpr int G0 = (RPT + 1) / 2;
+  y_group<R1, OUTER, 0, G0>(x32, smap, pitch, pjs, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj,
+                            p, hr, wr, tot, posb, placedb, cmax);
+  if constexpr (RPT > G0)
+    y_group<R1, OUTER, G0, RPT - G0>(x32, smap, pitch, pjs, tb, xd, rx, ry, yb0, ty0, tx0, mask,
+                                     root_of, aj, p, hr, wr, tot, posb, placedb, cmax);
 }
 
 // Penalty tables of a part (warp 0): FP32 screen values, exact FP64
