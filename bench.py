@@ -504,8 +504,9 @@ def _rooflines(plan, n, kernel_ms, stream, traffic_ok):
     k34_ms = sum(k34_parts.values())
     k34_traffic = [traffic.get(k) for k in ("gdt_x_kernel", "gdt_y_kernel")
                    if "k3x_gdt_rows" in kernel_ms]
-    if "k3k4_place_assemble" in kernel_ms:
-        k34_traffic.append(traffic.get("place_assemble_kernel"))
+    if "k3k4_place_assemble" in kernel_ms:  # the two-phase kernel, or the round-1 one (DPM_K3=v1)
+        k34_traffic.append(traffic.get("place_assemble_kernel" if os.environ.get("DPM_K3") == "v1"
+                                       else "k3v2::place2_kernel"))
     k34_traffic = (sum(k34_traffic) if k34_traffic and None not in k34_traffic else None)
     k1_bytes = n * plan.k1_bytes()
     k1_ms = kernel_ms.get("k1_project", 0.0)

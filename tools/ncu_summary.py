@@ -123,9 +123,13 @@ def main(launch_csv, rep, images, tag):
         fh.write("| kernel | time (us) | DRAM read+write (MB) | per image (MB) | tensor pipe % | "
                  "FMA pipe % | FP64 pipe % | issue active % | occupancy % | regs | top stalls |\n")
         fh.write("|---|---|---|---|---|---|---|---|---|---|---|\n")
+        seen = set()
         for rec in fu:
             dram = rec.get("dram_read", 0) + rec.get("dram_write", 0)
             name = rec["kernel"]
+            if name in seen:  # the capture's -c may wrap into the next run: one launch each
+                continue
+            seen.add(name)
             # ncu reports bytes in the unit of the column (MB in --csv raw for these metrics)
             # one entry per kernel family (template instantiations summed: a
             # step launches each family's instantiations once)
