@@ -35,160 +35,15 @@
 // Each CTA walks 128-wide column strips of levels top to bottom; every input
 // row is staged once per strip.  The group's core B (hi | lo) stays resident
 // in shared memory for the whole launch.
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace dpm {
-
-constexpr int TC_M = 128;
-constexpr int TC_THREADS = 256;
-constexpr int TC_PRODUCERS = 3;  // warps 1..3
-constexpr int TC_MAX_RING = 16;
-constexpr int TC_MAX_ACC = 4;
-
-struct TcArgs {
-  const float* P;
-  const float* Gtc;  // [h*w][R/4][2N][4] fp32: rows < N hi, rows >= N lo
-  float* S;
-  const dpm_corr_job* jobs;
-  const dpm_corr_tile* strips;  // (job, -, strip index)
-  int nstrips;
-  int h, w, R, N;               // N: padded filter count (multiple of 16)
-  int ring, acc_cols, nacc;
-  uint32_t* ranges;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Wait for the phase with parity `parity`; traps (instead of hanging the GPU)
-// if it has not completed after ~20 s, which can only be a pipeline bug.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  for (int spin = 0; spin < 2000 && !done; ++spin) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t"
-        "}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity), "r"(10000000u)
-        : "memory");
-  }
-  if (!done) asm volatile("trap;");
-}
 
 #ifdef DPM_TC_PROBE
 // MMA-warp wait cycles (debug builds only, tools/tc_probe.py): accumulator
 // free, input rows staged, output rows, total loop cycles
 __device__ unsigned long long dpm_tc_probe[4];
 #endif
-
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-
-// K-major, no-swizzle smem matrix descriptor (SM100 UMMA):
-// start >> 4 in [0,14), LBO >> 4 in [16,30), SBO >> 4 in [32,46), version 1 at 46.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
-
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128.
-__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-
-// kind::f16 with bf16 A/B, f32 D, K-major, M = 128
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(TC_M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, 1, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc));
-}
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-  uint32_t r[8];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7])
-      : "r"(taddr));
-#pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
-}
-
-__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-#pragma unroll
-  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
-}
-
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t"
-      ".reg .pred P;\n\t"
-      "elect.sync _|P, 0xffffffff;\n\t"
-      "selp.b32 %0, 1, 0, P;\n\t"
-      "}"
-      : "=r"(pred));
-  return pred != 0;
-}
-
-__device__ __forceinline__ float tf32_hi(float a) {
-  return __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-}
 
 // NMAX: max filters held by the epilogue registers.  FH, FW > 0: filter
 // extent fixed at compile time (R == 8), fully unrolled MMA issue.
@@ -777,6 +632,14 @@ static int tc_ring(int h, int w, int R, int nf) {
   return ring;
 }
 
+// CTA-pair kernel for the part shape (corr_tc2.cu), opt-in with
+// DPM_TC_PAIR=1: bit-identical maps, but not faster (DESIGN.md section 3,
+// "K2 on CTA pairs")
+static bool tc_pairs() {
+  const char* e = getenv("DPM_TC_PAIR");
+  return e && e[0] == '1';
+}
+
 extern "C" int dpm_correlate_tc_stack(int h, int w, int R, int nf) { return tc_stack(h, w, R, nf); }
 
 extern "C" size_t dpm_correlate_tc_smem(int h, int w, int R, int nf) {
@@ -827,6 +690,8 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
     a.acc_cols = 16 * ks;
     a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
     fn = w == 11 ? corr_tc_kernel<8, 6, 11, 4, 6> : corr_tc_kernel<8, 6, 6, 4, 6>;
+  } else if (h == 6 && w == 6 && R == 8 && tc_pairs()) {
+    return launch_tc_pair(a, as_stream(stream));  // DPM part filters: cta_group::2 pairs
   } else if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps (12 measured slower)
     fn = N <= 16 ? corr_tc_kernel<16, 6, 6, 8>
        : N <= 32 ? corr_tc_kernel<32, 6, 6, 8>

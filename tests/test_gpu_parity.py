@@ -500,6 +500,7 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
     for H, W, nf, h, w, R in [(40, 300, 48, 6, 6, 8), (23, 130, 16, 6, 6, 8),
                               (17, 200, 33, 5, 7, 8), (12, 70, 64, 3, 4, 8),
                               (30, 150, 6, 6, 11, 8), (9, 90, 1, 2, 3, 8),
+                              (6, 140, 40, 6, 6, 8), (7, 261, 64, 6, 6, 8), (31, 520, 20, 6, 6, 8),
                               (26, 260, 16, 6, 6, 16), (14, 140, 7, 5, 8, 16)]:
         level = rng.random((H, W, 32)).astype(np.float32)
         C = rng.normal(size=(32, R)).astype(np.float32)
@@ -520,6 +521,36 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
             g_ff = plans[1].map(0, 0, f).double().cpu().numpy()
             assert_map_close(g_tc, ref, f"tc {H}x{W} filter {f}")
             assert_map_close(g_tc, g_ff, f"tc vs ffma {H}x{W} filter {f}")
+
+
+def test_part_correlation_cta_pairs_bit_identical_to_one_cta_kernel(monkeypatch):
+    """The part shape (6 x 6 taps, R = 8) on CTA pairs (cta_group::2, M =
+    256, corr_tc2.cu, opt-in with DPM_TC_PAIR=1): the same MMAs in the same
+    order as the one-CTA kernel, so the maps are bit-identical -- odd and
+    even output heights, one-row levels, 16..64 filters, more strips than
+    SM pairs."""
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    rng = np.random.default_rng(12)
+    levels = [(40, 300), (6, 140), (7, 261), (23, 1100), (12, 9000)]
+    for nf in (12, 30, 48, 64):
+        C = rng.normal(size=(32, 8)).astype(np.float32)
+        cores = [rng.normal(0, 0.05, (6, 6, 8)).astype(np.float32) for _ in range(nf)]
+        data = [rng.random((H, W, 32)).astype(np.float32) for H, W in levels]
+        maps = []
+        for pair in ("1", "0"):
+            monkeypatch.setenv("DPM_TC_PAIR", pair)
+            plan = Plan(32, levels, C, [FilterDef(c) for c in cores],
+                        apps=[(k, f) for k in range(len(levels)) for f in range(nf)], outputs=(),
+                        tensor_cores=True)
+            plan.load_levels(0, data)
+            plan.run(stages=("project", "correlate"))
+            maps.append([[plan.map(0, k, f).cpu().numpy().copy() for f in range(nf)]
+                         for k in range(len(levels))])
+        for k in range(len(levels)):
+            for f in range(nf):
+                np.testing.assert_array_equal(maps[0][k][f], maps[1][k][f],
+                                              err_msg=f"nf {nf} level {levels[k]} filter {f}")
 
 
 def test_score_batch_pipelined_matches_full_run():
