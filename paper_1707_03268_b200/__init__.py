@@ -25,6 +25,7 @@ from .evaluation import RocPoint, match_detections, nms, nms_records, roc_eval
 from .errors import CpdetectError, DeviceError, FormatError, NumericError, ValidationError
 from .features import HogBuilder, extract_hog_pyramid
 from .pipeline import PyramidScorer, cores_from_stacked, detect_batch, score_pyramid
+from .plancache import clear_plan_cache, plan_cache_info
 from .types import (CPModel, DecomposedModel, DecomposedPart, Detection, DetectStats,
                     Hypothesis, PartModel, PartSpec)
 
@@ -39,6 +40,6 @@ __all__ = [
     "dense_detect", "detect",
     "calibrate_thresholds", "score_pyramid", "detect_batch", "nms", "nms_records", "match_detections", "roc_eval",
     "RocPoint", "full_multiplications", "score_hypothesis", "theoretical_gain",
-    "HogBuilder", "extract_hog_pyramid",
+    "HogBuilder", "extract_hog_pyramid", "clear_plan_cache", "plan_cache_info",
     "valid_support", "validate",
 ]

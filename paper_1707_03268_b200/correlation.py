@@ -17,10 +17,11 @@ map's max |score|).
 
 import numpy as np
 
-from .engine import FilterDef, Plan
+from .engine import FilterDef
 from .errors import ValidationError, check_feature_map, check_tensor3
 from .geometry import (cp_multiplications, full_multiplications, theoretical_gain,
                        valid_support)
+from .plancache import lease
 from .types import ScoreMap
 
 __all__ = [
@@ -56,13 +57,14 @@ def cp_core(model, keep=None):
 
 
 def _run_maps(img, C, filters):
+    """Maps of every filter on one level, through a cached plan of this
+    layout (plancache: repeated calls rebind basis / cores instead of
+    building a plan)."""
     H, W, L = img.shape
-    plan = Plan(L, [(H, W)], C, filters, apps=[(0, f) for f in range(len(filters))],
-                outputs=())
-    plan.load_levels(0, [img.astype(np.float32)])
-    plan.run(stages=("project", "correlate"))
-    maps = [plan.map(0, 0, f).double().cpu().numpy() for f in range(len(filters))]
-    return maps
+    with lease(L, [(H, W)], C, filters, [(0, f) for f in range(len(filters))]) as plan:
+        plan.load_levels(0, [img.astype(np.float32)])
+        plan.run(stages=("project", "correlate"))
+        return [plan.map(0, 0, f).double().cpu().numpy() for f in range(len(filters))]
 
 
 def correlate3_cp(img, model, upto_rank=None):

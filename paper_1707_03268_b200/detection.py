@@ -24,6 +24,7 @@ from .correlation import cp_core
 from .engine import AssemblyDef, FilterDef, PartDef, Plan, unpack_positions
 from .errors import ValidationError, check_feature_map
 from .geometry import cp_multiplications, full_multiplications, hypothesis_rect
+from .plancache import lease
 from .types import Detection, DetectStats, Hypothesis
 
 __all__ = [
@@ -240,10 +241,10 @@ def dense_detect(model, pyramid, tau, model_id="model"):
 
 def _maps_at(level, C, filters):
     H, W, L = level.shape
-    plan = Plan(L, [(H, W)], C, filters, apps=[(0, f) for f in range(len(filters))], outputs=())
-    plan.load_levels(0, [level.astype(np.float32)])
-    plan.run(stages=("project", "correlate"))
-    return [plan.map(0, 0, f).double().cpu().numpy() for f in range(len(filters))]
+    with lease(L, [(H, W)], C, filters, [(0, f) for f in range(len(filters))]) as plan:
+        plan.load_levels(0, [level.astype(np.float32)])
+        plan.run(stages=("project", "correlate"))
+        return [plan.map(0, 0, f).double().cpu().numpy() for f in range(len(filters))]
 
 
 def _check_pos(level, dims, pos):

@@ -135,6 +135,7 @@ class Plan:
             if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
                 raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
                                       f"outside the basis of rank {self.Rtot}")
+        self._apps_key = tuple(sorted(set((int(a), int(b)) for a, b in apps)))
         self._layout(apps)
         self._upload(C)
 
@@ -197,38 +198,9 @@ class Plan:
                 for s in range(0, len(fl), g):
                     self.groups.append((k, tuple(fl[s:s + g])))
 
-        # cores: one block per distinct filter tuple
-        ga = _Arena()
-        self.core_off = {}
-        core_blocks = []
-        for _, fl in self.groups:
-            if fl in self.core_off:
-                continue
-            fd0 = self.filters[fl[0]]
-            nfp = _round_up(len(fl), 8)
-            block = np.zeros((fd0.h, fd0.w, fd0.R, nfp), dtype=np.float32)
-            for i, f in enumerate(fl):
-                block[:, :, :, i] = self.filters[f].core
-            self.core_off[fl] = ga.take(block.size, align=4)
-            core_blocks.append((self.core_off[fl], block))
-        self._core_host = np.zeros(max(ga.size, 4), dtype=np.float32)
-        for off, block in core_blocks:
-            self._core_host[off:off + block.size] = block.ravel()
-
-        # tensor-core eligible groups (tcgen05 3xTF32 path) and their cores in
-        # the [tap][R/4][2N][4] hi|lo layout
-        tca = _Arena()
-        self.tc_core_off = {}
-        tc_blocks = []
-        for _, fl in self.groups:
-            if fl in self.tc_core_off or not self._tc_eligible(fl):
-                continue
-            block = _tc_core([self.filters[f].core for f in fl])
-            self.tc_core_off[fl] = tca.take(block.size, align=64)
-            tc_blocks.append((self.tc_core_off[fl], block))
-        self._tc_core_host = np.zeros(max(tca.size, 4), dtype=np.float32)
-        for off, block in tc_blocks:
-            self._tc_core_host[off:off + block.size] = block.ravel()
+        # cores: one block per distinct filter tuple; tensor-core eligible
+        # groups (tcgen05 path) also in the [tap][R/4][2N][4] hi|lo layout
+        self._pack_cores()
 
         # S arena, K2 jobs, tiles, range slots
         sa = _Arena()
@@ -383,6 +355,65 @@ class Plan:
         return (R in self.tc_ranks and R % 8 == 0 and R <= 32 and 1 <= nf <= 64 and
                 h + 2 <= 16 and w <= 64 and
                 _lib.lib().dpm_correlate_tc_smem(h, w, R, nf) <= 227 * 1024)
+
+    def _pack_cores(self):
+        """Host core arrays (FP32 blocks [h][w][R][nf_pad] per group, and the
+        tcgen05 layout of the eligible groups) with their offsets."""
+        ga, tca = _Arena(), _Arena()
+        self.core_off, self.tc_core_off = {}, {}
+        blocks, tc_blocks = [], []
+        for _, fl in self.groups:
+            if fl in self.core_off:
+                continue
+            fd0 = self.filters[fl[0]]
+            block = np.zeros((fd0.h, fd0.w, fd0.R, _round_up(len(fl), 8)), dtype=np.float32)
+            for i, f in enumerate(fl):
+                block[:, :, :, i] = self.filters[f].core
+            self.core_off[fl] = ga.take(block.size, align=4)
+            blocks.append((self.core_off[fl], block))
+            if self._tc_eligible(fl):
+                tcb = _tc_core([self.filters[f].core for f in fl])
+                self.tc_core_off[fl] = tca.take(tcb.size, align=64)
+                tc_blocks.append((self.tc_core_off[fl], tcb))
+        self._core_host = np.zeros(max(ga.size, 4), dtype=np.float32)
+        for off, block in blocks:
+            self._core_host[off:off + block.size] = block.ravel()
+        self._tc_core_host = np.zeros(max(tca.size, 4), dtype=np.float32)
+        for off, block in tc_blocks:
+            self._tc_core_host[off:off + block.size] = block.ravel()
+
+    def _opts(self):
+        return (self.tensor_cores, self.tc_min_width, self.tc_ranks, self.envelope,
+                tuple(sorted(self.outputs)), self.max_dets, str(self.device))
+
+    def signature(self):
+        """Layout key of a correlation plan (no assemblies): plans with equal
+        signatures differ only in basis and core VALUES, which rebind() swaps."""
+        return plan_signature(self.L, self.levels, self.n_images, self.Rtot, self.filters,
+                              self._apps_key, self._opts())
+
+    def rebind(self, C, filters):
+        """Swap the basis and the filter cores for ones of the same layout
+        (same signature), re-uploading them in place; levels are reloaded by
+        the caller.  Lets a cached plan serve repeated drop-in calls (the
+        reference's loops over images and models) without rebuilding tables."""
+        if self.assemblies:
+            raise ValidationError("rebind: plans with assemblies are not rebindable")
+        C = np.ascontiguousarray(C, dtype=np.float32)
+        filters = list(filters)
+        if plan_signature(self.L, self.levels, self.n_images, C.shape[1] if C.ndim == 2 else -1,
+                          filters, self._apps_key, self._opts()) != self.signature() or \
+                C.shape != tuple(self.C.shape):
+            raise ValidationError("rebind: basis / filters do not match the plan's layout")
+        core_off, tc_core_off = self.core_off, self.tc_core_off
+        self.filters = filters
+        self._pack_cores()
+        assert self.core_off == core_off and self.tc_core_off == tc_core_off
+        t = self.torch
+        self.C.copy_(t.from_numpy(C))
+        self.G.copy_(t.from_numpy(self._core_host))
+        self.Gtc.copy_(t.from_numpy(self._tc_core_host))
+        return self
 
     def _tc_eligible(self, fl):
         if not self.tensor_cores or fl in self._prefix_groups:
@@ -694,6 +725,18 @@ def _sm_count():
     except Exception:  # planning without a usable device
         pass
     return 148
+
+
+def plan_signature(L, levels, n_images, Rtot, filters, apps_key, opts=()):
+    """Everything a plan's layout depends on: geometry, filter shapes and
+    rank-prefix families (by first member, not by array identity), the maps
+    requested and the plan options."""
+    fams, fsig = {}, []
+    for i, f in enumerate(filters):
+        fam = fams.setdefault(id(f.core), i) if f.prefix > 0 else -1
+        fsig.append((f.h, f.w, f.R, f.chan_off, f.prefix, fam))
+    return (int(L), tuple(tuple(int(v) for v in lv) for lv in levels), int(n_images), int(Rtot),
+            tuple(fsig), tuple(apps_key), tuple(opts))
 
 
 def _spitch(w):
