@@ -146,6 +146,16 @@ int dpm_correlate_tc_stack(int h, int w, int R, int nf);
 int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
                      const dpm_corr_tile* strips, int nstrips, int h, int w, int R, int nf,
                      uint32_t* ranges, void* stream);
+/* Several filter groups of one shape in one launch (the generic-shape
+ * kernel: any (h, w, R) but the compile-time DPM shapes above): every group
+ * has at most nf filters and its own core block in the tf32 hi|lo layout at
+ * float offset tc_off[job] of Gtc (device array indexed by job id, 16-byte
+ * aligned blocks).  Strips of different groups may interleave; a persistent
+ * CTA reloads the core (one bulk copy) when a strip's group differs from
+ * the resident one. */
+int dpm_correlate_tc_groups(const float* P, const float* Gtc, const int64_t* tc_off, float* S,
+                            const dpm_corr_job* jobs, const dpm_corr_tile* strips, int nstrips,
+                            int h, int w, int R, int nf, uint32_t* ranges, void* stream);
 
 /* K2 in rank-prefix mode (convolution shortening, paper Algorithm 1;
  * replaces the reference's _term_stack + cumsum, correlation.py:115-180,

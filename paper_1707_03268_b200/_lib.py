@@ -92,6 +92,8 @@ _SIGNATURES = {
     "dpm_correlate_prefix": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "dpm_correlate_tc_smem": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
     "dpm_correlate_tc": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "dpm_correlate_tc_groups": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32,
+                                       _vp, _vp]),
     "dpm_correlate_tc_core_floats": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
     "dpm_correlate_tc_stack": (_i32, [_i32, _i32, _i32, _i32]),
     "dpm_place_prepare": (_i64, [_vp, _i32]),

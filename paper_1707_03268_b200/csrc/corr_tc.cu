@@ -79,9 +79,11 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
   uint64_t* tfull = bars + 2 * TC_MAX_RING;
   uint64_t* tempty = tfull + TC_MAX_ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_MAX_ACC);
+  uint64_t* bdone = tempty + TC_MAX_ACC + 1;  // multi-group: issued MMAs complete
+  uint64_t* bload = bdone + 1;                // multi-group: core B landed
 
   // ---- setup: core B -> smem (all threads), barriers, TMEM
-  {
+  if (a.tc_off == nullptr) {
     const float4* src = reinterpret_cast<const float4*>(a.Gtc);
     float4* dst = reinterpret_cast<float4*>(sB);
     for (uint32_t e = threadIdx.x; e < b_bytes / 16u; e += blockDim.x) dst[e] = __ldg(src + e);
@@ -100,6 +102,8 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, EPI);
     }
+    mbar_init(bdone, 1);
+    mbar_init(bload, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -289,10 +293,37 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         atomicAdd(&dpm_tc_probe[3], (unsigned long long)(clock64() - pr_t0));
       }
 #endif
-    } else
+    } else {
+    int64_t b_res = -1;              // Gtc offset of the resident core (multi-group)
+    uint32_t bdone_ph = 0, bload_ph = 0;
+    bool issued = false;
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
       const int ho = job.H - a.h + 1;
+      if (a.tc_off != nullptr) {
+        const int64_t off = a.tc_off[a.strips[st].job];
+        if (off != b_res) {
+          // every MMA that read the old core has completed, then one bulk
+          // copy brings the strip's core (the ring and TMEM are untouched)
+          if (issued) {
+            if (elect_one()) tc_commit(bdone);
+            __syncwarp();
+            mbar_wait(bdone, bdone_ph);
+            bdone_ph ^= 1;
+          }
+          if (elect_one()) {
+            mbar_expect_tx(bload, b_bytes);
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(a.Gtc + off);
+            for (uint32_t o = 0; o < b_bytes; o += 32768u)
+              bulk_g2s(sB + o, src + o, min(32768u, b_bytes - o), bload);
+          }
+          __syncwarp();
+          mbar_wait(bload, bload_ph);
+          bload_ph ^= 1;
+          b_res = off;
+        }
+        issued = true;
+      }
       for (int y = 0; y < ho; ++y, ++row_glob) {
         const int b = row_glob & (TC_MAX_ACC - 1);
         mbar_wait(tempty + b, ((row_glob / TC_MAX_ACC) & 1) ^ 1);
@@ -330,6 +361,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         for (int rr = ho; rr < job.H; ++rr) tc_commit(empty + (q_glob + rr) % a.ring);
       __syncwarp();
       q_glob += job.H;
+    }
     }
   } else if (warp <= TC_PRODUCERS) {
     // =================== producers ===================
@@ -625,7 +657,7 @@ static size_t tc_slot(int h, int w, int R) {
 static int tc_ring(int h, int w, int R, int nf) {
   const size_t slot = tc_slot(h, w, R);
   const size_t fixed = tc_b_bytes(h, w, R, nf) + tc_b2_bytes(h, w, R, nf) +
-                       (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16 + 15;
+                       (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 32 + 15;
   const int need = h + tc_stack(h, w, R, nf) + 1;
   int ring = need <= TC_MAX_RING ? need : TC_MAX_RING;
   while (ring < TC_MAX_RING && fixed + (ring + 1) * slot <= 227 * 1024) ++ring;
@@ -643,13 +675,15 @@ static bool tc_pairs() {
 extern "C" int dpm_correlate_tc_stack(int h, int w, int R, int nf) { return tc_stack(h, w, R, nf); }
 
 extern "C" size_t dpm_correlate_tc_smem(int h, int w, int R, int nf) {
+  if (tc16_shape(h, w, R, (nf + 15) & ~15)) return tc16_smem(nullptr);
   const int ring = tc_ring(h, w, R, nf);
   const size_t slot = tc_slot(h, w, R);
   return tc_b_bytes(h, w, R, nf) + tc_b2_bytes(h, w, R, nf) + ((ring * slot + 15) & ~(size_t)15) +
-         (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 16;
+         (2 * TC_MAX_RING + 2 * TC_MAX_ACC) * 8 + 32;
 }
 
 extern "C" size_t dpm_correlate_tc_core_floats(int h, int w, int R, int nf) {
+  if (tc16_shape(h, w, R, (nf + 15) & ~15)) return tc16_core_floats();
   const int ks = tc_stack(h, w, R, nf);
   if (ks > 1) {
     const size_t nb = (size_t)h + 2 * (ks - 1);
@@ -661,9 +695,9 @@ extern "C" size_t dpm_correlate_tc_core_floats(int h, int w, int R, int nf) {
   return f;
 }
 
-extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
-                                const dpm_corr_tile* strips, int nstrips, int h, int w, int R,
-                                int nf, uint32_t* ranges, void* stream) {
+static int tc_launch(const float* P, const float* Gtc, const int64_t* tc_off, float* S,
+                     const dpm_corr_job* jobs, const dpm_corr_tile* strips, int nstrips, int h,
+                     int w, int R, int nf, uint32_t* ranges, void* stream) {
   DPM_REQUIRE(P && Gtc && S && jobs && strips, "dpm_correlate_tc: null pointer");
   DPM_REQUIRE(R % 8 == 0 && R >= 8, "dpm_correlate_tc: R=%d must be a multiple of 8", R);
   DPM_REQUIRE(R <= 32 && w <= 64, "dpm_correlate_tc: R=%d w=%d outside the staged row", R, w);
@@ -676,7 +710,7 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
   int dev = 0, sms = 148;
   DPM_CUDA(cudaGetDevice(&dev));
   DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  TcArgs a{P, Gtc, S, jobs, strips, nstrips, h, w, R, N, tc_ring(h, w, R, nf), 0, 0, ranges};
+  TcArgs a{P, Gtc, S, jobs, strips, nstrips, h, w, R, N, tc_ring(h, w, R, nf), 0, 0, ranges, tc_off};
   a.acc_cols = 2 * N <= 32 ? 32 : 2 * N <= 64 ? 64 : 2 * N <= 128 ? 128 : 256;
   a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
   void (*fn)(const TcArgs) = N <= 16 ? corr_tc_kernel<16, 0, 0>
@@ -685,7 +719,12 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
                                        : corr_tc_kernel<64, 0, 0>;
   int threads = TC_THREADS;
   const int ks = tc_stack(h, w, R, nf);
-  if (ks > 1) {  // <= 8 filters (DPM roots: 3 mirrored pairs): rows stacked 6 per group
+  if (tc16_shape(h, w, R, N)) {
+    return launch_tc16(a, as_stream(stream));  // 6 x 6 at R = 16: compile-time kernel
+  } else if (tc_off != nullptr) {
+    // several groups per launch: the generic-shape kernel (runtime taps, B
+    // reloaded per group by one bulk copy)
+  } else if (ks > 1) {  // <= 8 filters (DPM roots: 3 mirrored pairs): rows stacked 6 per group
     a.N = 8;
     a.acc_cols = 16 * ks;
     a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
@@ -708,6 +747,23 @@ extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, cons
   fn<<<grid, threads, smem, as_stream(stream)>>>(a);
   DPM_LAUNCHED("corr_tc_kernel");
   return DPM_OK;
+}
+
+extern "C" int dpm_correlate_tc(const float* P, const float* Gtc, float* S, const dpm_corr_job* jobs,
+                                const dpm_corr_tile* strips, int nstrips, int h, int w, int R,
+                                int nf, uint32_t* ranges, void* stream) {
+  return tc_launch(P, Gtc, nullptr, S, jobs, strips, nstrips, h, w, R, nf, ranges, stream);
+}
+
+extern "C" int dpm_correlate_tc_groups(const float* P, const float* Gtc, const int64_t* tc_off,
+                                       float* S, const dpm_corr_job* jobs,
+                                       const dpm_corr_tile* strips, int nstrips, int h, int w,
+                                       int R, int nf, uint32_t* ranges, void* stream) {
+  DPM_REQUIRE(tc_off, "dpm_correlate_tc_groups: null tc_off");
+  DPM_REQUIRE(!tc_bf16(h, w, R),
+              "dpm_correlate_tc_groups: %dx%d at R=%d has a compile-time kernel; launch its "
+              "groups with dpm_correlate_tc", h, w, R);
+  return tc_launch(P, Gtc, tc_off, S, jobs, strips, nstrips, h, w, R, nf, ranges, stream);
 }
 
 #ifdef DPM_TC_PROBE

@@ -22,6 +22,10 @@ struct TcArgs {
   int h, w, R, N;               // N: padded filter count (multiple of 16)
   int ring, acc_cols, nacc;
   uint32_t* ranges;
+  // several filter groups in one launch (generic-shape kernel only): the
+  // float offset in Gtc of the core of each job's group, indexed by job; the
+  // MMA warp reloads B whenever a strip's group differs from the resident one
+  const int64_t* tc_off;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -52,6 +56,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
   if (!done) asm volatile("trap;");
+}
+
+// global -> shared bulk copy (async proxy), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
 }
 
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
@@ -154,5 +173,10 @@ __device__ __forceinline__ float tf32_hi(float a) {
 
 // corr_tc2.cu: the part shape (6 x 6 taps, R = 8) on CTA pairs
 int launch_tc_pair(const TcArgs& a, cudaStream_t stream);
+// corr_tc16.cu: 6 x 6 taps at R = 16, 16 filters per group, multi-group
+bool tc16_shape(int h, int w, int R, int N);
+size_t tc16_core_floats();
+size_t tc16_smem(int* ring_out);
+int launch_tc16(TcArgs a, cudaStream_t stream);
 
 }  // namespace dpm

@@ -110,7 +110,7 @@ class Plan:
 
     def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
                  outputs=("totals", "positions"), max_dets=0, device=None, tensor_cores=True,
-                 tc_min_width=16, envelope=False, tc_ranks=(8,)):
+                 tc_min_width=16, envelope=False, tc_ranks=(8, 16), tc_generic=False):
         import torch
 
         require_cuda()
@@ -131,6 +131,7 @@ class Plan:
         self.tc_min_width = int(tc_min_width)
         self.envelope = bool(envelope)
         self.tc_ranks = tuple(int(r) for r in tc_ranks)
+        self.tc_generic = bool(tc_generic)
         for k, f in enumerate(self.filters):
             if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
                 raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
@@ -273,12 +274,33 @@ class Plan:
         if prefix_classes:
             pjobs = np.ascontiguousarray(self._corr_jobs[self._corr_jobs["mode"] == 1])
             _lib.check(lib.dpm_correlate_prefix_check(_lib.table_ptr(pjobs), len(pjobs)), "prefix")
-        self._tc_classes = []
+        # tcgen05 launches: one per group for the compile-time DPM shapes (R = 8,
+        # 6 x 6 / 6 x 11); the generic-shape groups of one (h, w, R, N) share
+        # ONE launch (dpm_correlate_tc_groups: per-job core offsets, the core
+        # reloaded by a bulk copy when a CTA's strip changes group)
+        self._tc_classes = []  # (name, h, w, R, nf, core offset or -1, strips, tc_off or None)
+        merged = {}
         for fl, strips in sorted(tc_classes.items()):
-            strips = _snake_order(strips, key=lambda t: t[3], ctas=_sm_count())
             fd = self.filters[fl[0]]
-            arr = np.array([(j, 0, sx, 0) for j, _, sx, _ in strips], dtype=_lib.CORR_TILE)
-            self._tc_classes.append((fd.h, fd.w, fd.R, len(fl), self.tc_core_off[fl], arr))
+            if _tc_compiled(fd.h, fd.w, fd.R):
+                strips = _snake_order(strips, key=lambda t: t[3], ctas=_sm_count())
+                arr = np.array([(j, 0, sx, 0) for j, _, sx, _ in strips], dtype=_lib.CORR_TILE)
+                self._tc_classes.append((f"k2_tcgen05_{fd.h}x{fd.w}_nf{len(fl)}", fd.h, fd.w,
+                                         fd.R, len(fl), self.tc_core_off[fl], arr, None))
+            else:
+                m = merged.setdefault((fd.h, fd.w, fd.R, _round_up(len(fl), 16)), [])
+                m.append((fl, strips))
+        for (h, w, R, npad), members in sorted(merged.items()):
+            tc_off = np.full(max(len(jobs), 1), -1, dtype=np.int64)
+            allstrips = []
+            for fl, strips in members:
+                for st in strips:
+                    tc_off[st[0]] = self.tc_core_off[fl]
+                allstrips.extend(strips)
+            allstrips = _snake_order(allstrips, key=lambda t: t[3], ctas=_sm_count())
+            arr = np.array([(j, 0, sx, 0) for j, _, sx, _ in allstrips], dtype=_lib.CORR_TILE)
+            self._tc_classes.append((f"k2_tcgen05_{h}x{w}_R{R}_groups{len(members)}", h, w, R,
+                                     npad, -1, arr, tc_off))
 
         # K1 jobs
         pj = [(img * self.x_image_stride + self.x_level_off[k],
@@ -352,6 +374,8 @@ class Plan:
         return True
 
     def _tc_fits(self, h, w, R, nf):
+        if R > 8 and not self.tc_generic and not _tc16(h, w, R, nf):
+            return False  # generic shapes at R > 8 measured slower than FFMA
         return (R in self.tc_ranks and R % 8 == 0 and R <= 32 and 1 <= nf <= 64 and
                 h + 2 <= 16 and w <= 64 and
                 _lib.lib().dpm_correlate_tc_smem(h, w, R, nf) <= 227 * 1024)
@@ -383,7 +407,7 @@ class Plan:
             self._tc_core_host[off:off + block.size] = block.ravel()
 
     def _opts(self):
-        return (self.tensor_cores, self.tc_min_width, self.tc_ranks, self.envelope,
+        return (self.tensor_cores, self.tc_min_width, self.tc_ranks, self.tc_generic, self.envelope,
                 tuple(sorted(self.outputs)), self.max_dets, str(self.device))
 
     def signature(self):
@@ -422,12 +446,13 @@ class Plan:
         return self._tc_fits(fd.h, fd.w, fd.R, len(fl))
 
     def _group_size(self, h, w, R):
-        """Filters per K2 group: MAX_GROUP, or -- when R > 8 is enabled for the
-        tensor cores (``tc_ranks``) -- the largest of 48 / 32 / 16 whose
-        resident tcgen05 core and input ring fit shared memory (R = 16 at
-        6 x 6: 16 filters).  Off by default: the generic-shape tcgen05 kernel
-        measured slower than FFMA there (config 3: 51.8 ms for the 6 x 6 class
-        in 60 16-filter launches against 11.5 ms FFMA)."""
+        """Filters per K2 group: MAX_GROUP, or -- when R > 8 goes to the tensor
+        cores (``tc_ranks``) -- the largest of 48 / 32 / 16 whose resident
+        tcgen05 core and input ring fit shared memory: 16 for 6 x 6 at R = 16,
+        the compile-time kernel of corr_tc16.cu, whose groups share one launch
+        (config 3: 4.7 ms for the 6 x 6 class against 11.5 ms FFMA).  Other
+        shapes at R > 8 (the generic-shape kernel) only with ``tc_generic``:
+        they measured slower than FFMA."""
         if self.tensor_cores and R > 8:
             for g in (48, 32, 16):
                 if self._tc_fits(h, w, R, g):
@@ -501,9 +526,10 @@ class Plan:
         tb["proj"] = (upload_table(pj, dev), len(pj), nblk)  # upload after block0 is filled
         keep = np.isin(self._corr_job_image, list(imgs))
         tb["tc"] = []
-        for h, w, R, nf, goff, strips in self._tc_classes:
+        for name, h, w, R, nf, goff, strips, tc_off in self._tc_classes:
             sub = np.ascontiguousarray(strips[keep[strips["job"]]])
-            tb["tc"].append((h, w, R, nf, goff, len(sub), upload_table(sub, dev)))
+            off_d = None if tc_off is None else self.torch.from_numpy(tc_off).to(dev)
+            tb["tc"].append((name, h, w, R, nf, goff, len(sub), upload_table(sub, dev), off_d))
         tb["ffma"] = []
         for h, nf, R, w_max, tiles in self._classes:
             sub = np.ascontiguousarray(tiles[keep[tiles["job"]]])
@@ -576,13 +602,20 @@ class Plan:
                 mark("ranges_init")
                 _lib.check(lib.dpm_ranges_init(ptr(self.ranges), self.n_ranges, s), "ranges")
             rng = ptr(self.ranges) if self.n_ranges else None
-            for h, w, R, nf, goff, n, strips_d in tb["tc"]:
+            for name, h, w, R, nf, goff, n, strips_d, off_d in tb["tc"]:
                 if not n:
                     continue
-                mark(f"k2_tcgen05_{h}x{w}_nf{nf}")
-                _lib.check(lib.dpm_correlate_tc(ptr(self.P), ptr(self.Gtc) + 4 * goff, ptr(self.S),
-                                                ptr(self.corr_jobs_d), ptr(strips_d), n,
-                                                h, w, R, nf, rng, s), "correlate_tc")
+                mark(name)
+                if off_d is None:
+                    _lib.check(lib.dpm_correlate_tc(ptr(self.P), ptr(self.Gtc) + 4 * goff,
+                                                    ptr(self.S), ptr(self.corr_jobs_d),
+                                                    ptr(strips_d), n, h, w, R, nf, rng, s),
+                               "correlate_tc")
+                else:
+                    _lib.check(lib.dpm_correlate_tc_groups(ptr(self.P), ptr(self.Gtc), ptr(off_d),
+                                                           ptr(self.S), ptr(self.corr_jobs_d),
+                                                           ptr(strips_d), n, h, w, R, nf, rng, s),
+                               "correlate_tc")
             for h, nf, R, w_max, n, tiles_d in tb["ffma"]:
                 if not n:
                     continue
@@ -699,8 +732,8 @@ class Plan:
             return sum(2 * int(jobs[j]["h"]) * int(jobs[j]["w"]) * int(jobs[j]["R"]) *
                        int(jobs[j]["nf"]) * (int(jobs[j]["H"]) - int(jobs[j]["h"]) + 1) *
                        (int(jobs[j]["W"]) - int(jobs[j]["w"]) + 1) for j in set(jids))
-        for h, w, R, nf, _, strips in self._tc_classes:
-            out[f"k2_tcgen05_{h}x{w}_nf{nf}"] = fl(strips["job"].tolist())
+        for name, h, w, R, nf, _, strips, _ in self._tc_classes:
+            out[name] = fl(strips["job"].tolist())
         for h, nf, R, _, tiles in self._classes:
             out[f"k2_ffma_h{h}_nf{nf}"] = fl(tiles["job"].tolist())
         for h, tiles in self._prefix_classes:
@@ -713,6 +746,16 @@ class Plan:
 
     def k1_bytes(self):
         return sum(4 * (self.L + self.Rtot) * H * W for H, W in self.levels)
+
+
+def _tc16(h, w, R, nf):
+    """6 x 6 filters at R = 16, <= 16 per group: corr_tc16.cu (tc16_shape)."""
+    return h == 6 and w == 6 and R == 16 and nf <= 16
+
+
+def _tc_compiled(h, w, R):
+    """Shapes with a compile-time tcgen05 kernel (tc_bf16 in corr_tc.cu)."""
+    return R == 8 and h == 6 and w in (6, 11)
 
 
 def _sm_count():
@@ -787,7 +830,15 @@ def _tc_core(cores):
         out[:, :, base:base + nf, :] = t
     out = out.ravel()
     total = int(_lib.lib().dpm_correlate_tc_core_floats(h, w, R, nf))
-    if total > out.size:
+    if total > out.size and R == 16:
+        # 6 x 6 at R = 16 (corr_tc16.cu): bf16 block [tap][2][N][8], plane c =
+        # ranks 8c..8c+7 of the truncated values
+        b2 = np.zeros((h * w, 2, N, 8), dtype=np.uint16)
+        bits = _bf16_rn(hi).reshape(h * w, 2, 8, nf)  # (tap, plane, rank, nf)
+        b2[:, :, :nf, :] = bits.transpose(0, 1, 3, 2)
+        out = np.concatenate([out, b2.ravel().view(np.float32)])
+        assert out.size == total, (out.size, total)
+    elif total > out.size:
         npairs = (w + 1) // 2
         b2 = np.zeros((h, npairs, 2, N, 8), dtype=np.uint16)
         bits = _bf16_rn(hi)  # (h, w, R, nf)

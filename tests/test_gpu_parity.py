@@ -509,7 +509,7 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
         for tc in (True, False):
             plan = Plan(32, [(H, W)], C, [FilterDef(c) for c in cores],
                         apps=[(0, f) for f in range(nf)], outputs=(), tensor_cores=tc,
-                        tc_ranks=(8, 16))
+                        tc_ranks=(8, 16), tc_generic=True)
             assert bool(plan._tc_classes) == tc
             plan.load_levels(0, [level])
             plan.run(stages=("project", "correlate"))
@@ -521,6 +521,43 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
             g_ff = plans[1].map(0, 0, f).double().cpu().numpy()
             assert_map_close(g_tc, ref, f"tc {H}x{W} filter {f}")
             assert_map_close(g_tc, g_ff, f"tc vs ffma {H}x{W} filter {f}")
+
+
+@pytest.mark.parametrize("shape,generic,name", [
+    ((6, 6), False, "k2_tcgen05_6x6_R16_groups4"),   # corr_tc16.cu (the default)
+    ((5, 7), True, "k2_tcgen05_5x7_R16_groups4"),    # generic-shape kernel, tc_generic
+])
+def test_tensor_core_multi_group_launch_matches_oracle(shape, generic, name):
+    """tcgen05 groups of one (h, w, R, N) share one launch
+    (dpm_correlate_tc_groups): 50 R = 16 filters in groups of 16 over three
+    levels -- strips of different groups interleave on the persistent CTAs,
+    which reload the core per group -- against the oracle and FFMA."""
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    rng = np.random.default_rng(13)
+    levels = [(30, 300), (17, 140), (9, 600)]
+    C = rng.normal(size=(32, 16)).astype(np.float32)
+    cores = [rng.normal(0, 0.05, shape + (16,)).astype(np.float32) for _ in range(50)]
+    data = [rng.random((H, W, 32)).astype(np.float32) for H, W in levels]
+    plans = []
+    for tc in (True, False):
+        plan = Plan(32, levels, C, [FilterDef(c) for c in cores],
+                    apps=[(k, f) for k in range(3) for f in range(50)], outputs=(),
+                    tensor_cores=tc, tc_ranks=(8, 16), tc_generic=generic)
+        if tc:
+            names = [c[0] for c in plan._tc_classes]
+            assert names == [name], names
+        plan.load_levels(0, data)
+        plan.run(stages=("project", "correlate"))
+        plans.append(plan)
+    for k, lv in enumerate(data):
+        P = O.project(lv, C.astype(np.float64))
+        for f in range(0, 50, 7):
+            ref = O.correlate3_full(P, cores[f])
+            g_tc = plans[0].map(0, k, f).double().cpu().numpy()
+            g_ff = plans[1].map(0, k, f).double().cpu().numpy()
+            assert_map_close(g_tc, ref, f"tc level {k} filter {f}")
+            assert_map_close(g_tc, g_ff, f"tc vs ffma level {k} filter {f}")
 
 
 def test_part_correlation_cta_pairs_bit_identical_to_one_cta_kernel(monkeypatch):

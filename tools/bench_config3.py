@@ -24,7 +24,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--tc-ranks", default="8,16",
+                    help="ranks routed to tcgen05 (comma list; '8,16' adds the multi-group "
+                         "generic-shape launch for the R = 16 groups)")
     args = ap.parse_args()
+    tc_ranks = tuple(int(v) for v in args.tc_ranks.split(","))
 
     import torch
 
@@ -54,7 +58,8 @@ def main():
     levels = synth.hog_pyramid(3, 0, pyr)
     out = []
     for name, C, filters, R in variants:
-        plan = Plan(32, pyr.levels, C, filters, apps=apps, n_images=1, outputs=())
+        plan = Plan(32, pyr.levels, C, filters, apps=apps, n_images=1, outputs=(),
+                    tc_ranks=tc_ranks)
         plan.load_levels(0, levels)
         for _ in range(args.warmup):
             plan.run(stages=("project", "correlate"))
@@ -69,7 +74,7 @@ def main():
         rec = {"variant": name, "rank": R, "filters": len(bank.filters), "applications": len(apps),
                "ms": ms, "evals_per_s": evals / (ms / 1e3),
                "k2_flops": plan.k2_flops(), "tflops": plan.k2_flops() / (ms / 1e3) / 1e12,
-               "tensor_core_classes": len(plan._tc_classes)}
+               "tensor_core_classes": [c[0] for c in plan._tc_classes], "tc_ranks": list(tc_ranks)}
         out.append(rec)
         print(json.dumps(rec), flush=True)
         del plan
