@@ -106,11 +106,18 @@ class Plan:
         instead of the windowed r* kernel (dpm_assemble).  Both give the same
         placements (up to exact ties); the window is the default because it
         is faster at the r* (~10) of the benchmark maps.
+    tc_ranks : ranks R whose filter groups may run on tcgen05: R = 8 (the
+        compile-time DPM shapes), R = 16 (6 x 6 filters, corr_tc16.cu).
+    tc_generic : also route other shapes at R > 8 to the generic-shape
+        tcgen05 kernel (measured slower than FFMA; off by default).
+    tc_min_strips : fewest 128-column strips for which a 6 x 6 R = 16 class
+        goes to corr_tc16 (default 2 per SM; below that FFMA is faster).
     """
 
     def __init__(self, L, levels, C, filters, apps=(), assemblies=(), n_images=1,
                  outputs=("totals", "positions"), max_dets=0, device=None, tensor_cores=True,
-                 tc_min_width=16, envelope=False, tc_ranks=(8, 16), tc_generic=False):
+                 tc_min_width=16, envelope=False, tc_ranks=(8, 16), tc_generic=False,
+                 tc_min_strips=None):
         import torch
 
         require_cuda()
@@ -132,6 +139,7 @@ class Plan:
         self.envelope = bool(envelope)
         self.tc_ranks = tuple(int(r) for r in tc_ranks)
         self.tc_generic = bool(tc_generic)
+        self.tc_min_strips = None if tc_min_strips is None else int(tc_min_strips)
         for k, f in enumerate(self.filters):
             if f.chan_off < 0 or f.chan_off + f.R > self.Rtot:
                 raise ValidationError(f"filter {k}: channels [{f.chan_off}, {f.chan_off + f.R}) "
@@ -178,6 +186,25 @@ class Plan:
             by_level.setdefault(k, []).append(f)
         self.groups = []  # (level, (filters...))
         self._prefix_groups = set()  # groups computed by the rank-prefix kernel
+        # corr_tc16 (6 x 6, R = 16, 16-filter groups) pays off only with enough
+        # 128-column strips to fill the SMs (one strip per persistent CTA at a
+        # time; a small pyramid leaves most SMs idle behind its tallest strips):
+        # fewer than 2 per SM -> FFMA with 48-filter groups (config 2 at R = 16:
+        # 90 strips, 0.32 ms tcgen05 against 0.29 ms FFMA)
+        strips16 = {}
+        for k in by_level:
+            H, W = self.levels[k]
+            cnt = {}
+            for f in by_level[k]:
+                fd = self.filters[f]
+                if fd.prefix == 0 and _tc16(fd.h, fd.w, fd.R, 16):
+                    cnt[(fd.h, fd.w, fd.R)] = cnt.get((fd.h, fd.w, fd.R), 0) + 1
+            for key, n in cnt.items():
+                wo = W - key[1] + 1
+                if wo >= self.tc_min_width:
+                    strips16[key] = strips16.get(key, 0) + nimg * ((n + 15) // 16) * ((wo + 127) // 128)
+        min_strips = 2 * _sm_count() if self.tc_min_strips is None else self.tc_min_strips
+        self._tc16_off = {key for key, n in strips16.items() if n < min_strips}
         for k in sorted(by_level):
             keyed = {}
             for f in by_level[k]:
@@ -374,7 +401,8 @@ class Plan:
         return True
 
     def _tc_fits(self, h, w, R, nf):
-        if R > 8 and not self.tc_generic and not _tc16(h, w, R, nf):
+        if R > 8 and not self.tc_generic and (not _tc16(h, w, R, nf) or
+                                               (h, w, R) in getattr(self, "_tc16_off", ())):
             return False  # generic shapes at R > 8 measured slower than FFMA
         return (R in self.tc_ranks and R % 8 == 0 and R <= 32 and 1 <= nf <= 64 and
                 h + 2 <= 16 and w <= 64 and
@@ -407,7 +435,8 @@ class Plan:
             self._tc_core_host[off:off + block.size] = block.ravel()
 
     def _opts(self):
-        return (self.tensor_cores, self.tc_min_width, self.tc_ranks, self.tc_generic, self.envelope,
+        return (self.tensor_cores, self.tc_min_width, self.tc_ranks, self.tc_generic,
+                self.tc_min_strips, self.envelope,
                 tuple(sorted(self.outputs)), self.max_dets, str(self.device))
 
     def signature(self):

@@ -71,7 +71,7 @@ def test_map_error_within_bar_on_both_k2_paths(cfg, basis, lv):
     rows = []
     for tc in (True, False):
         plan = Plan(32, pyr.levels, C, [FilterDef(c) for c in cores], apps=apps, outputs=(),
-                    tensor_cores=tc)
+                    tensor_cores=tc, tc_min_strips=0)
         plan.load_levels(0, levels)
         plan.run(stages=("project", "correlate"))
         worst, where = 0.0, None

@@ -509,7 +509,7 @@ def test_tensor_core_correlation_matches_oracle_and_ffma():
         for tc in (True, False):
             plan = Plan(32, [(H, W)], C, [FilterDef(c) for c in cores],
                         apps=[(0, f) for f in range(nf)], outputs=(), tensor_cores=tc,
-                        tc_ranks=(8, 16), tc_generic=True)
+                        tc_ranks=(8, 16), tc_generic=True, tc_min_strips=0)
             assert bool(plan._tc_classes) == tc
             plan.load_levels(0, [level])
             plan.run(stages=("project", "correlate"))
@@ -543,7 +543,8 @@ def test_tensor_core_multi_group_launch_matches_oracle(shape, generic, name):
     for tc in (True, False):
         plan = Plan(32, levels, C, [FilterDef(c) for c in cores],
                     apps=[(k, f) for k in range(3) for f in range(50)], outputs=(),
-                    tensor_cores=tc, tc_ranks=(8, 16), tc_generic=generic)
+                    tensor_cores=tc, tc_ranks=(8, 16), tc_generic=generic,
+                    tc_min_strips=0)
         if tc:
             names = [c[0] for c in plan._tc_classes]
             assert names == [name], names
