@@ -20,6 +20,10 @@
 // Persistent CTAs walk the tile list with a grid stride; a group's core is
 // re-staged only when the group changes (all part tiles of a DPM model
 // share one group, so it is staged once per CTA when R <= 8).
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace dpm {
@@ -403,6 +407,18 @@ static bool pick(int h, int nf, Shape* s) {
 
 typedef void (*corr_fn)(const CorrArgs);
 
+int launch_corr_few(const float* P, const float* G, float* S, const dpm_corr_job* jobs,
+                    const dpm_corr_tile* tiles, int ntiles, int h, int nf, int w_max,
+                    uint32_t* ranges, cudaStream_t st);
+// DPM_K2FEW=0 keeps few-filter groups on corr_kernel (A/B)
+static bool few_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DPM_K2FEW");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int FH>
 static corr_fn by_nf(int nfk) {
   switch (nfk) {
@@ -462,6 +478,11 @@ extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm
   int dev = 0, sms = 148;
   DPM_CUDA(cudaGetDevice(&dev));
   DPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (nf <= 8 && few_enabled()) {  // few-filter groups: correlate_few.cu
+    const int rc = launch_corr_few(P, G, S, jobs, tiles, ntiles, h, nf, w_max, ranges,
+                                   as_stream(stream));
+    if (rc != DPM_ERR_UNSUPPORTED) return rc;
+  }
   CorrArgs a{P, G, S, jobs, tiles, ntiles, 1, 1, w_max, R, nf, ranges};
   Shape s;
   if (!pick(h, nf, &s)) {
