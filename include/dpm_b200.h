@@ -368,6 +368,61 @@ int dpm_prune_ranks(const float* S, const int64_t* map_offs, const double* thr,
                     const dpm_prune_job* jobs, int njobs, int64_t nblocks, uint8_t* out,
                     void* stream);
 
+/* Pruned detection, composition (detection.py:433-542 after the per-rank
+ * checks): per root of an assembly, in part order, the hypotheses alive when
+ * each part is checked (kill: a part failure removes the root; lenient: it
+ * only drops the part's term), the reference's counters as histograms, and
+ * the detections (score >= tau among the alive roots: the assembled total in
+ * kill mode; root + alive parts' placed values + bias, in part order, in
+ * lenient mode; a lenient part that failed reports root + anchor).  Job =
+ * one assembly of dpm_assemble.  Outputs per root: lim[i] = the rank bound
+ * of part i's alive window (0: not alive when part i is checked; R_i: never
+ * fails; else its failing rank), prank[i] = part i's failing rank or 0.
+ * Histograms (uint32, 256 bins each, at hist + hist_off): row 0 the root
+ * ranks (0 = never fails), row 1 + i part i's failing ranks among the roots
+ * alive at part i (bin 0: how many roots are alive at part i).  Detections
+ * are appended (count in *det_count). */
+typedef struct {
+  int64_t rank_off;   /* dpm_prune_ranks output: role k (0 root, 1+i part i) at rank_off + k hr wr */
+  int64_t lim_off;    /* uint8 outputs: lim [nparts][hr][wr] at lim_off, prank right after      */
+  int64_t total_off, pos_off, placed_off;  /* dpm_assemble outputs of the assembly (all required) */
+  int64_t root_off;   /* float offset in S of the root map                                      */
+  int32_t root_pitch;
+  int32_t ry0, ry1, rx0, rx1;
+  int32_t nparts;
+  int32_t image, level;
+  int32_t hist_off;   /* uint32 offset of the job's (1 + nparts) x 256 histogram               */
+  int32_t block0;     /* first CTA; set by dpm_prune_compose_prepare                            */
+  double bias;
+  int32_t part_R[DPM_MAX_PARTS];
+  int32_t ay[DPM_MAX_PARTS], ax[DPM_MAX_PARTS];
+} dpm_prune_asm;
+int64_t dpm_prune_compose_prepare(dpm_prune_asm* jobs_host, int njobs);
+int dpm_prune_compose(const uint8_t* ranks, const float* S, const double* total,
+                      const uint32_t* pos, const double* placed, const dpm_prune_asm* jobs,
+                      int njobs, int64_t nblocks, int kill_mode, double tau, uint8_t* lim,
+                      uint32_t* hist, dpm_detection* dets, int max_dets, int* det_count,
+                      void* stream);
+
+/* The multiplication counter of the pruned part stage (detection.py:474-486,
+ * 545-567): per (assembly, part), every part-support cell of the union of the
+ * roots' search windows gets M = max over the roots whose window holds it of
+ * lim; hist[hist_off + M] counts the cells (so the work of rank r is the
+ * number of cells with M > r).  Job = one (assembly, part). */
+typedef struct {
+  int64_t lim_off;    /* the part's lim map [hr][wr] (dpm_prune_compose)     */
+  int32_t hr, wr;     /* root rectangle extent                               */
+  int32_t y0, y1, x0, x1;  /* covered box in part-support coordinates        */
+  int32_t oy, ox;     /* root index of box cell (y0, x0)'s window centre: iy = y - oy */
+  int32_t radius;
+  int32_t hist_off;   /* uint32 offset of the job's 256 bins                 */
+  int32_t block0;     /* first CTA; set by dpm_prune_cover_prepare           */
+  int32_t pad;
+} dpm_cover_job;
+int64_t dpm_prune_cover_prepare(dpm_cover_job* jobs_host, int njobs);
+int dpm_prune_cover(const uint8_t* lim, const dpm_cover_job* jobs, int njobs, int64_t nblocks,
+                    uint32_t* hist, void* stream);
+
 /* ------------------------------------------------------- mixture max
  * SURVEY.md §8(f) row 3 (the reference has no combination rule; SPEC asks
  * for a max).  Job = one (image, root level): the union rectangle of its

@@ -13,7 +13,7 @@ import numpy as np
 from .errors import DeviceError, NumericError, ValidationError
 
 __all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "ASM_JOB", "SMAP_DESC",
-           "DETECTION", "PLACE_RANGE", "PRUNE_JOB", "MIX_JOB", "LIB_PATH", "MAX_PARTS", "table_ptr"]
+           "DETECTION", "PLACE_RANGE", "PRUNE_JOB", "PRUNE_ASM", "COVER_JOB", "MIX_JOB", "LIB_PATH", "MAX_PARTS", "table_ptr"]
 
 LIB_PATH = os.environ.get("DPM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                                                    "libdpm_b200.so")
@@ -53,6 +53,18 @@ PRUNE_JOB = np.dtype([("out_off", "<i8"), ("offs0", "<i4"), ("thr0", "<i4"), ("R
                       ("rx0", "<i4"), ("rx1", "<i4"), ("ay", "<i4"), ("ax", "<i4"),
                       ("scale", "<i4"), ("radius", "<i4"), ("block0", "<i4")], align=True)
 
+PRUNE_ASM = np.dtype([("rank_off", "<i8"), ("lim_off", "<i8"), ("total_off", "<i8"),
+                      ("pos_off", "<i8"), ("placed_off", "<i8"), ("root_off", "<i8"),
+                      ("root_pitch", "<i4"), ("ry0", "<i4"), ("ry1", "<i4"), ("rx0", "<i4"),
+                      ("rx1", "<i4"), ("nparts", "<i4"), ("image", "<i4"), ("level", "<i4"),
+                      ("hist_off", "<i4"), ("block0", "<i4"), ("bias", "<f8"),
+                      ("part_R", "<i4", (MAX_PARTS,)), ("ay", "<i4", (MAX_PARTS,)),
+                      ("ax", "<i4", (MAX_PARTS,))], align=True)
+COVER_JOB = np.dtype([("lim_off", "<i8"), ("hr", "<i4"), ("wr", "<i4"), ("y0", "<i4"),
+                      ("y1", "<i4"), ("x0", "<i4"), ("x1", "<i4"), ("oy", "<i4"), ("ox", "<i4"),
+                      ("radius", "<i4"), ("hist_off", "<i4"), ("block0", "<i4"), ("pad", "<i4")],
+                     align=True)
+
 MIX_JOB = np.dtype([("out_off", "<i8"), ("ry0", "<i4"), ("ry1", "<i4"), ("rx0", "<i4"),
                     ("rx1", "<i4"), ("member0", "<i4"), ("nmembers", "<i4"), ("block0", "<i4"),
                     ("pad", "<i4")], align=True)
@@ -68,7 +80,7 @@ HOG_JOB = np.dtype([("r_off", "<i8"), ("x_off", "<i8"), ("h_off", "<i8"), ("Hs",
 
 _SIZES = {"PROJ_JOB": 32, "CORR_JOB": 72, "CORR_TILE": 16, "PLACE_JOB": 96, "ASM_JOB": 88,
           "SMAP_DESC": 24,
-          "DETECTION": 96, "PLACE_RANGE": 16, "PRUNE_JOB": 64,
+          "DETECTION": 96, "PLACE_RANGE": 16, "PRUNE_JOB": 64, "PRUNE_ASM": 288, "COVER_JOB": 56,
           "MIX_JOB": 40, "RESAMPLE_JOB": 40, "HOG_JOB": 40}
 for _n, _s in _SIZES.items():
     assert globals()[_n].itemsize == _s, (_n, globals()[_n].itemsize)
@@ -109,6 +121,11 @@ _SIGNATURES = {
                          _vp, _vp]),
     "dpm_prune_prepare": (_i64, [_vp, _i32]),
     "dpm_prune_ranks": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp]),
+    "dpm_prune_compose_prepare": (_i64, [_vp, _i32]),
+    "dpm_prune_compose": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i64, _i32, _dbl, _vp, _vp,
+                                 _vp, _i32, _vp, _vp]),
+    "dpm_prune_cover_prepare": (_i64, [_vp, _i32]),
+    "dpm_prune_cover": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
     "dpm_mixture_prepare": (_i64, [_vp, _i32]),
     "dpm_mixture_max": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp]),
     "dpm_ffma_probe": (_i32, [_vp, _i32, _vp, _vp]),

@@ -85,6 +85,165 @@ extern "C" int dpm_prune_ranks(const float* S, const int64_t* map_offs, const do
   return DPM_OK;
 }
 
+// ------------------------------------------------ pruned-detection composition
+// detect(pruning=True) after the per-rank checks (detection.py:433-542), per
+// root in the reference's part order; see dpm_b200.h (dpm_prune_compose).
+namespace dpm {
+__device__ __forceinline__ uint32_t pack_yx(int y, int x) {
+  return ((uint32_t)(uint16_t)(int16_t)y << 16) | (uint32_t)(uint16_t)(int16_t)x;
+}
+
+__global__ void __launch_bounds__(256)
+prune_compose_kernel(const uint8_t* __restrict__ ranks, const float* __restrict__ S,
+                     const double* __restrict__ total, const uint32_t* __restrict__ pos,
+                     const double* __restrict__ placed, const dpm_prune_asm* __restrict__ jobs,
+                     int njobs, int kill_mode, double tau, uint8_t* __restrict__ lim,
+                     uint32_t* __restrict__ hist, dpm_detection* __restrict__ dets, int max_dets,
+                     int* __restrict__ det_count) {
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
+  const dpm_prune_asm& j = jobs[jid];
+  const int hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
+  const int64_t n = (int64_t)hr * wr;
+  const int64_t e = (int64_t)(blockIdx.x - j.block0) * 256 + threadIdx.x;
+  const bool live = e < n;
+  const int iy = live ? (int)(e / wr) : 0, ix = live ? (int)(e - (int64_t)iy * wr) : 0;
+  const int ry = j.ry0 + iy, rx = j.rx0 + ix;
+  bool alive = false, hit = false;
+  uint32_t part_alive = 0u;  // bit i: part i's term counts (lenient)
+  double score = 0.0;
+  if (live) {
+    const int rr = ranks[j.rank_off + e];
+    atomicAdd(hist + j.hist_off + rr, 1u);  // root (detection.py:452-460)
+    alive = rr == 0;
+    for (int i = 0; i < j.nparts; ++i) {  // parts in order (detection.py:462-503)
+      const int pr = ranks[j.rank_off + (int64_t)(1 + i) * n + e];
+      const bool pa0 = alive;  // alive when part i is checked
+      lim[j.lim_off + i * n + e] = (uint8_t)(pa0 ? (pr == 0 ? j.part_R[i] : pr) : 0);
+      lim[j.lim_off + (j.nparts + i) * n + e] = (uint8_t)(pa0 && pr >= 1 ? pr : 0);
+      if (pa0) atomicAdd(hist + j.hist_off + (1 + i) * 256, 1u);  // bin 0: alive at part i
+      if (pa0 && pr >= 1) {
+        atomicAdd(hist + j.hist_off + (1 + i) * 256 + pr, 1u);
+        if (kill_mode) alive = false;  // positions_killed_by_parts
+      }
+      if (pa0 && pr == 0) part_alive |= 1u << i;
+    }
+    if (kill_mode) {
+      score = total[j.total_off + e];
+    } else {  // root + sum_i (alive_i ? placed_i : 0) + bias, in the reference's order
+      score = (double)S[j.root_off + (int64_t)ry * j.root_pitch + rx];
+      for (int i = 0; i < j.nparts; ++i)
+        score = __dadd_rn(score, (part_alive >> i) & 1u ? placed[j.placed_off + i * n + e] : 0.0);
+      score = __dadd_rn(score, j.bias);
+    }
+    hit = alive && score >= tau;
+  }
+  if (dets == nullptr) return;
+  const unsigned bal = __ballot_sync(0xffffffffu, hit);
+  if (bal == 0u) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(det_count, __popc(bal));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!hit) return;
+  const int slot = base + __popc(bal & ((1u << lane) - 1u));
+  if (slot >= max_dets) return;
+  dpm_detection d;
+  d.image = j.image;
+  d.level = j.level;
+  d.component = 0;
+  d.ry = ry;
+  d.rx = rx;
+  d.nparts = j.nparts;
+  d.score = score;
+  for (int q = 0; q < DPM_MAX_PARTS; ++q) {
+    uint32_t v = 0u;
+    if (q < j.nparts)
+      v = (!kill_mode && !((part_alive >> q) & 1u)) ? pack_yx(ry + j.ay[q], rx + j.ax[q])
+                                                    : pos[j.pos_off + q * n + e];
+    d.parts[q] = v;
+  }
+  dets[slot] = d;
+}
+
+__global__ void __launch_bounds__(256)
+prune_cover_kernel(const uint8_t* __restrict__ lim, const dpm_cover_job* __restrict__ jobs,
+                   int njobs, uint32_t* __restrict__ hist) {
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
+  const dpm_cover_job& j = jobs[jid];
+  const int bw = j.x1 - j.x0 + 1;
+  const int64_t e = (int64_t)(blockIdx.x - j.block0) * 256 + threadIdx.x;
+  if (e >= (int64_t)(j.y1 - j.y0 + 1) * bw) return;
+  const int y = j.y0 + (int)(e / bw), x = j.x0 + (int)(e % bw);
+  const int cy = y - j.oy, cx = x - j.ox;  // root index whose window centre is the cell
+  const int iy0 = max(cy - j.radius, 0), iy1 = min(cy + j.radius, j.hr - 1);
+  const int ix0 = max(cx - j.radius, 0), ix1 = min(cx + j.radius, j.wr - 1);
+  int m = 0;
+  for (int iy = iy0; iy <= iy1; ++iy)
+    for (int ix = ix0; ix <= ix1; ++ix) m = max(m, (int)lim[j.lim_off + (int64_t)iy * j.wr + ix]);
+  if (m > 0) atomicAdd(hist + j.hist_off + m, 1u);
+}
+}  // namespace dpm
+
+extern "C" int64_t dpm_prune_compose_prepare(dpm_prune_asm* jobs, int njobs) {
+  DPM_REQUIRE(njobs >= 0 && (njobs == 0 || jobs), "dpm_prune_compose_prepare: bad table");
+  int64_t blocks = 0;
+  for (int i = 0; i < njobs; ++i) {
+    dpm_prune_asm& j = jobs[i];
+    DPM_REQUIRE(j.ry1 >= j.ry0 && j.rx1 >= j.rx0 && j.nparts >= 0 && j.nparts <= DPM_MAX_PARTS &&
+                    j.rank_off >= 0 && j.lim_off >= 0 && j.hist_off >= 0 && j.total_off >= 0 &&
+                    (j.nparts == 0 || (j.pos_off >= 0 && j.placed_off >= 0)) && j.root_off >= 0,
+                "dpm_prune_compose_prepare: job %d has a bad rectangle / part count / offset", i);
+    for (int q = 0; q < j.nparts; ++q)
+      DPM_REQUIRE(j.part_R[q] >= 1 && j.part_R[q] <= 255,
+                  "dpm_prune_compose_prepare: job %d part %d rank %d", i, q, j.part_R[q]);
+    j.block0 = (int32_t)blocks;
+    blocks += ((int64_t)(j.ry1 - j.ry0 + 1) * (j.rx1 - j.rx0 + 1) + 255) / 256;
+  }
+  DPM_REQUIRE(blocks <= INT32_MAX, "dpm_prune_compose_prepare: too many CTAs");
+  return blocks;
+}
+
+extern "C" int dpm_prune_compose(const uint8_t* ranks, const float* S, const double* total,
+                                 const uint32_t* pos, const double* placed,
+                                 const dpm_prune_asm* jobs, int njobs, int64_t nblocks,
+                                 int kill_mode, double tau, uint8_t* lim, uint32_t* hist,
+                                 dpm_detection* dets, int max_dets, int* det_count, void* stream) {
+  DPM_REQUIRE(ranks && S && total && jobs && lim && hist, "dpm_prune_compose: null pointer");
+  DPM_REQUIRE(!dets || det_count, "dpm_prune_compose: detections need a counter");
+  DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_prune_compose: nblocks");
+  if (njobs == 0 || nblocks == 0) return DPM_OK;
+  prune_compose_kernel<<<(unsigned)nblocks, 256, 0, as_stream(stream)>>>(
+      ranks, S, total, pos, placed, jobs, njobs, kill_mode, tau, lim, hist, dets, max_dets,
+      det_count);
+  DPM_LAUNCHED("prune_compose_kernel");
+  return DPM_OK;
+}
+
+extern "C" int64_t dpm_prune_cover_prepare(dpm_cover_job* jobs, int njobs) {
+  DPM_REQUIRE(njobs >= 0 && (njobs == 0 || jobs), "dpm_prune_cover_prepare: bad table");
+  int64_t blocks = 0;
+  for (int i = 0; i < njobs; ++i) {
+    dpm_cover_job& j = jobs[i];
+    DPM_REQUIRE(j.hr >= 1 && j.wr >= 1 && j.radius >= 0 && j.lim_off >= 0 && j.hist_off >= 0,
+                "dpm_prune_cover_prepare: job %d has a bad extent / radius / offset", i);
+    j.block0 = (int32_t)blocks;
+    if (j.y1 >= j.y0 && j.x1 >= j.x0)
+      blocks += ((int64_t)(j.y1 - j.y0 + 1) * (j.x1 - j.x0 + 1) + 255) / 256;
+  }
+  DPM_REQUIRE(blocks <= INT32_MAX, "dpm_prune_cover_prepare: too many CTAs");
+  return blocks;
+}
+
+extern "C" int dpm_prune_cover(const uint8_t* lim, const dpm_cover_job* jobs, int njobs,
+                               int64_t nblocks, uint32_t* hist, void* stream) {
+  DPM_REQUIRE(lim && jobs && hist, "dpm_prune_cover: null pointer");
+  DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_prune_cover: nblocks");
+  if (njobs == 0 || nblocks == 0) return DPM_OK;
+  prune_cover_kernel<<<(unsigned)nblocks, 256, 0, as_stream(stream)>>>(lim, jobs, njobs, hist);
+  DPM_LAUNCHED("prune_cover_kernel");
+  return DPM_OK;
+}
+
 // ------------------------------------------------------------ mixture max
 // Per (image, root level): for every root position of the union rectangle
 // of the level's component assemblies, the max over components of their

@@ -404,10 +404,70 @@ def _detect_pruned(dec, levels, tau, mode, model_id, collect_maps):
     _lib.check(lib.dpm_prune_ranks(plan.S.data_ptr(), offs_d.data_ptr(), thr_d.data_ptr(),
                                    jobs_d.data_ptr(), len(jobs), nblk, ranks_d.data_ptr(),
                                    stream_handle(None)), "prune")
-    ranks = ranks_d.cpu().numpy()
+    # composition on the device (dpm_prune_compose / dpm_prune_cover): alive
+    # sets in part order, lenient scores, detections, and the counters as
+    # histograms; the host only sums the histograms in the reference's order
+    nparts = len(dec.parts)
+    cj = np.zeros(len(asms), dtype=_lib.PRUNE_ASM)
+    covs, lim_size, hist_size = [], 0, 0
+    for ai, a in enumerate(asms):
+        k = a.level_tag
+        ry0, ry1, rx0, rx1 = a.rect
+        hr, wr = ry1 - ry0 + 1, rx1 - rx0 + 1
+        n = hr * wr
+        t_off, p_off, pl_off, _, _ = plan.asm_index[(0, ai)]
+        j = cj[ai]
+        j["rank_off"], j["lim_off"] = out_at[(ai, 0)], lim_size
+        j["total_off"], j["pos_off"], j["placed_off"] = t_off, max(p_off, 0), max(pl_off, 0)
+        j["root_off"] = plan.map_off[(0, k, root_f)]
+        j["root_pitch"] = (plan.map_shape[(k, root_f)][1] + 3) & ~3
+        j["ry0"], j["ry1"], j["rx0"], j["rx1"] = ry0, ry1, rx0, rx1
+        j["nparts"], j["image"], j["level"], j["hist_off"] = nparts, 0, k, hist_size
+        j["bias"] = float(dec.bias)
+        sy_, sx_ = levels[k].shape[0], levels[k].shape[1]
+        for pi, part in enumerate(dec.parts):
+            j["part_R"][pi] = part.cp.rank
+            j["ay"][pi], j["ax"][pi] = part.anchor
+            nn, mm, _ = part.cp.dims
+            rad = int(part.search_radius)
+            ay, ax = (int(v) for v in part.anchor)
+            sy, sx = sy_ - nn + 1, sx_ - mm + 1
+            covs.append((lim_size + pi * n, hr, wr, max(0, ry0 + ay - rad), min(sy - 1, ry1 + ay + rad),
+                         max(0, rx0 + ax - rad), min(sx - 1, rx1 + ax + rad), ry0 + ay, rx0 + ax,
+                         rad, 0, 0, 0))
+        lim_size += 2 * nparts * n
+        hist_size += (1 + nparts) * 256
+    cov = np.array(covs, dtype=_lib.COVER_JOB) if covs else np.zeros(0, _lib.COVER_JOB)
+    cov_hist0 = hist_size
+    cov["hist_off"] = cov_hist0 + 256 * np.arange(len(cov))
+    hist_size += 256 * len(cov)
+    cblk = _lib.check(lib.dpm_prune_compose_prepare(_lib.table_ptr(cj), len(cj)), "prune compose")
+    vblk = _lib.check(lib.dpm_prune_cover_prepare(_lib.table_ptr(cov), len(cov)), "prune cover")
+    cj_d, cov_d = upload_table(cj, dev), upload_table(cov, dev)
+    lim_d = t.zeros(max(lim_size, 1), dtype=t.uint8, device=dev)
+    hist_d = t.zeros(max(hist_size, 1), dtype=t.int32, device=dev)
+    n_roots = int(sum((a.rect[1] - a.rect[0] + 1) * (a.rect[3] - a.rect[2] + 1) for a in asms))
+    dets_d = t.empty(max(n_roots, 1) * _lib.DETECTION.itemsize, dtype=t.uint8, device=dev)
+    cnt_d = t.zeros(1, dtype=t.int32, device=dev)
+    s = stream_handle(None)
+    _lib.check(lib.dpm_prune_compose(
+        ranks_d.data_ptr(), plan.S.data_ptr(), plan.totals.data_ptr(), plan.positions.data_ptr(),
+        plan.placed.data_ptr(), cj_d.data_ptr(), len(cj), cblk, 1 if mode == "kill" else 0,
+        float(tau), lim_d.data_ptr(), hist_d.data_ptr(), dets_d.data_ptr(), max(n_roots, 1),
+        cnt_d.data_ptr(), s), "prune compose")
+    _lib.check(lib.dpm_prune_cover(lim_d.data_ptr(), cov_d.data_ptr(), len(cov), vblk,
+                                   hist_d.data_ptr(), s), "prune cover")
+    hist = hist_d.cpu().numpy().astype(np.int64)
+    ndet = int(cnt_d.item())
+    recs = np.frombuffer(dets_d[:ndet * _lib.DETECTION.itemsize].cpu().numpy().tobytes(),
+                         dtype=_lib.DETECTION)
+    if collect_maps:
+        ranks = ranks_d.cpu().numpy()
+        lims = lim_d.cpu().numpy()
 
     ai_of = {a.level_tag: ai for ai, a in enumerate(asms)}
-    for li, (lv, rect) in enumerate(zip(levels, rects)):
+    n0, m0, l0 = dec.root_cp.dims
+    for li, rect in enumerate(rects):
         lm = {"rect": rect} if collect_maps else None
         if collect_maps:
             stats.prune_maps.append(lm)
@@ -417,66 +477,40 @@ def _detect_pruned(dec, levels, tau, mode, model_id, collect_maps):
         ry0, ry1, rx0, rx1 = rect
         hr, wr = ry1 - ry0 + 1, rx1 - rx0 + 1
         stats.positions_examined += hr * wr
-        rank_of = {role: ranks[out_at[(ai, role)]:out_at[(ai, role)] + hr * wr].reshape(hr, wr)
-                   .astype(np.int64) for role in range(len(cps))}
+        h0 = int(cj[ai]["hist_off"])
+        hroot = hist[h0:h0 + 256]
         # root: first failing rank (detection.py:452-460)
-        rr = rank_of[0]
-        n0, m0, l0 = dec.root_cp.dims
         for r in range(dec.root_cp.rank):
-            alive_r = (rr == 0) | (rr > r)
-            stats.multiplications += int(alive_r.sum()) * (n0 + m0 + l0)
-            _bump(stats.positions_pruned_at_rank, r + 1, (rr == r + 1).sum())
-        alive = rr == 0
-        if collect_maps:
-            lm["root_prune_rank"] = rr.copy()
-        out = plan.assembly_outputs(0, ai)
-        placed = out["placed"].cpu().numpy()
-        py, px = unpack_positions(out["positions"].cpu().numpy())
-        part_rank = np.zeros((len(dec.parts), hr, wr), dtype=np.int64)
-        part_alive = []
-        for pi, part in enumerate(dec.parts):
-            if mode == "kill" and not alive.any():
-                break
-            pr = rank_of[pi + 1]
+            stats.multiplications += int(hroot[0] + hroot[r + 1:].sum()) * (n0 + m0 + l0)
+            _bump(stats.positions_pruned_at_rank, r + 1, hroot[r + 1])
+        for pi, part in enumerate(dec.parts):  # parts in order (detection.py:462-503)
+            hp = hist[h0 + (1 + pi) * 256:h0 + (2 + pi) * 256]
+            hc = hist[cov_hist0 + 256 * (ai * nparts + pi):cov_hist0 + 256 * (ai * nparts + pi + 1)]
             n, m, l = part.cp.dims
-            rad = int(part.search_radius)
-            support = (lv.shape[0] - n + 1, lv.shape[1] - m + 1)
-            pa0 = alive.copy()
+            alive_r = int(hp[0])  # alive when the part is checked
             for r in range(part.cp.rank):
-                pa_r = pa0 & ~((pr >= 1) & (pr <= r))
-                if not pa_r.any():
+                if alive_r == 0:
                     break
-                stats.multiplications += _covered_count(_dilate_any(pa_r, rad), rect,
-                                                        part.anchor, rad, support) * (n + m + l)
-                newly = pa_r & (pr == r + 1)
-                if newly.any():
-                    _bump(stats.part_pruned_at_rank, r + 1, newly.sum())
-                    part_rank[pi][newly] = r + 1
-                    if mode == "kill":
-                        stats.positions_killed_by_parts += int((alive & newly).sum())
-                        alive &= ~newly
-            part_alive.append(pa0 & (pr == 0))
+                # support cells of the windows still alive at rank r
+                stats.multiplications += int(hc[r + 1:].sum()) * (n + m + l)
+                alive_r -= int(hp[r + 1])
+                _bump(stats.part_pruned_at_rank, r + 1, hp[r + 1])
+                if mode == "kill":
+                    stats.positions_killed_by_parts += int(hp[r + 1])
         if collect_maps:
-            lm["part_prune_rank"] = part_rank
-        if mode == "lenient":
-            # root + sum_i (alive_i ? placed_i : 0) + bias, reference order
-            scores = plan.map(0, li, root_f).double().cpu().numpy()[ry0:ry1 + 1, rx0:rx1 + 1]
-            for pi in range(len(part_alive)):
-                scores = scores + np.where(part_alive[pi], placed[pi], 0.0)
-            scores = scores + dec.bias
-        else:
-            scores = out["totals"].cpu().numpy()
-        for iy, ix in zip(*np.nonzero(alive & (scores >= tau))):
-            gy, gx = ry0 + int(iy), rx0 + int(ix)
-            pp = []
-            for pi, part in enumerate(dec.parts):
-                if mode == "lenient" and not part_alive[pi][iy, ix]:
-                    pp.append((gy + int(part.anchor[0]), gx + int(part.anchor[1])))
-                else:
-                    pp.append((int(py[pi, iy, ix]), int(px[pi, iy, ix])))
-            score = float(scores[iy, ix])
-            hyp = Hypothesis(level=li, root=(gy, gx), parts=tuple(pp), score=score)
-            detections.append(Detection(hyp, model_id=model_id, score=score, tau=tau))
+            n = hr * wr
+            o = out_at[(ai, 0)]
+            lo = int(cj[ai]["lim_off"])
+            lm["root_prune_rank"] = ranks[o:o + n].reshape(hr, wr).astype(np.int64)
+            lm["part_prune_rank"] = lims[lo + nparts * n:lo + 2 * nparts * n].reshape(
+                nparts, hr, wr).astype(np.int64)
+    for d in recs:
+        py, px = unpack_positions(d["parts"][:nparts])
+        pp = tuple((int(y), int(x)) for y, x in zip(py, px))
+        score = float(d["score"])
+        hyp = Hypothesis(level=int(d["level"]), root=(int(d["ry"]), int(d["rx"])), parts=pp,
+                         score=score)
+        detections.append(Detection(hyp, model_id=model_id, score=score, tau=tau))
     detections.sort(key=lambda d: (d.hypothesis.level, d.hypothesis.root))
     stats.wall_time = time.perf_counter() - start
     return detections, stats

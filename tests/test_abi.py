@@ -50,6 +50,9 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
         "dpm_place_range": ("rx", "ry", "E2", "E2in"),
         "dpm_prune_job": ("out_off", "offs0", "thr0", "R", "Hp", "ry0", "rx1", "scale", "radius",
                           "block0"),
+        "dpm_prune_asm": ("rank_off", "lim_off", "root_off", "root_pitch", "hist_off", "block0",
+                          "bias", "part_R", "ay", "ax"),
+        "dpm_cover_job": ("lim_off", "hr", "y0", "oy", "radius", "hist_off", "block0", "pad"),
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dpm_b200.h"', "int main(){"]
     for st, fs in fields.items():
@@ -66,7 +69,8 @@ def test_struct_layout_against_compiled_offsets(tmp_path):
     dts = {"dpm_proj_job": _lib.PROJ_JOB, "dpm_corr_job": _lib.CORR_JOB,
            "dpm_place_job": _lib.PLACE_JOB, "dpm_asm_job": _lib.ASM_JOB,
            "dpm_detection": _lib.DETECTION, "dpm_place_range": _lib.PLACE_RANGE,
-           "dpm_prune_job": _lib.PRUNE_JOB, "dpm_smap_desc": _lib.SMAP_DESC}
+           "dpm_prune_job": _lib.PRUNE_JOB, "dpm_smap_desc": _lib.SMAP_DESC,
+           "dpm_prune_asm": _lib.PRUNE_ASM, "dpm_cover_job": _lib.COVER_JOB}
     for st, fs in fields.items():
         assert int(out[st]) == dts[st].itemsize, st
         for f in fs:
