@@ -21,10 +21,26 @@ $(LIB): $(OBJS)
 	@mkdir -p $(dir $(LIB))
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
+# Checked build: device-side bounds checks (DPM_CHECK) compiled in; load it
+# with DPM_LIB=paper_1707_03268_b200/lib/libdpm_b200_checked.so
+CHK_DIR   := build/objc
+CHK_LIB   := paper_1707_03268_b200/lib/libdpm_b200_checked.so
+CHK_OBJS  := $(patsubst $(SRC_DIR)/%.cu,$(CHK_DIR)/%.o,$(SRCS))
+
+$(CHK_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
+	@mkdir -p $(CHK_DIR)
+	$(NVCC) $(NVFLAGS) -DDPM_CHECKED -c $< -o $@
+
+$(CHK_LIB): $(CHK_OBJS)
+	@mkdir -p $(dir $(CHK_LIB))
+	$(NVCC) $(ARCH) -shared -o $@ $(CHK_OBJS)
+
+checked: $(CHK_LIB)
+
 ptxas: EXTRA := -Xptxas -v
 ptxas: clean all
 
 clean:
-	rm -rf $(OBJ_DIR) $(LIB)
+	rm -rf $(OBJ_DIR) $(LIB) $(CHK_DIR) $(CHK_LIB)
 
-.PHONY: all clean ptxas
+.PHONY: all clean ptxas checked

@@ -43,6 +43,27 @@ const char* last_error();
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Bounds checks of the checked build (make checked -> libdpm_b200_checked.so,
+// -DDPM_CHECKED): shared- and global-memory indices of the hot kernels are
+// asserted; a violation prints the site and traps.  compute-sanitizer is
+// closed on this GPU pool, so the parity suite run against the checked
+// library stands in for memcheck (profiles/r2_checked_build.txt).  The
+// product build compiles the checks away.
+#ifdef DPM_CHECKED
+#define DPM_CHECK(cond, what)                                                              \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("DPM_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                           \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define DPM_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 // Row pitch (floats) of a response map S of width w: rows are padded to 16
 // bytes, so band / row copies can move whole 16-byte chunks and a map can be
 // described to the TMA unit (strides must be multiples of 16 B).

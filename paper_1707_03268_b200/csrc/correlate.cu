@@ -106,6 +106,7 @@ __device__ __forceinline__ void stage_p(float* dst, const CorrArgs& a, const dpm
     const int gy = y0 + row;
     const float* srow = pbase + r * plane + (int64_t)gy * job.pitch;
     float* drow = dst + (r * TROWS + row) * TPITCH;
+    DPM_CHECK(tcols <= TPITCH && r < K2_RCH, "P tile row fits its buffer");
     for (int col = lane; col < tcols; col += 32) {
       const int gx = x0 + col;
       const bool ok = gy < job.H && gx < job.W;
@@ -144,6 +145,7 @@ __device__ __forceinline__ void chunk_fma(unsigned long long (&acc)[K2_MP][NF / 
   for (int j = 0; j < w; ++j) {
     for (int r = 0; r < nr; ++r) {
       const float* pc = pw + r * TROWS * TPITCH + j;
+      DPM_CHECK(wy * MP + COL <= TROWS && lane + j < TPITCH, "compute reads inside the P tile");
       float col[COL];
 #pragma unroll
       for (int q = 0; q < COL; ++q) col[q] = pc[q * TPITCH];

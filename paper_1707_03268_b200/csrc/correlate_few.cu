@@ -87,6 +87,7 @@ corr_few_kernel(const FewArgs a) {
       const int ij = e / nr, r = e - ij * nr;
       const float* src = a.G + jb.g_off + ((int64_t)ij * jb.R + rc + r) * jb.nf_pad;
       const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sg + e * NF);
+      DPM_CHECK((e + 1) * NF <= a.gbuf, "core chunk fits its buffer");
       if constexpr (NF % 4 == 0) {
 #pragma unroll
         for (int q = 0; q < NF / 4; ++q)
@@ -110,6 +111,8 @@ corr_few_kernel(const FewArgs a) {
       const int gy = y0 + row;
       const float* srow = pbase + r * plane + (int64_t)gy * jb.pitch;
       float* drow = sp + (r * a.prow + row) * TPITCH;
+      DPM_CHECK(row < a.prow && (r * a.prow + row + 1) * TPITCH <= a.pbuf && tcols <= TPITCH,
+                "P chunk fits its buffer");
       for (int col = lane; col < tcols; col += 32) {
         const int gx = x0 + col;
         const bool ok = gy < jb.H && gx < jb.W;
@@ -150,6 +153,9 @@ corr_few_kernel(const FewArgs a) {
     const int nr = min(FEW_RCH, R - rc);
     const float* sp = sP0 + buf * a.pbuf + (wy * MP + i0) * TPITCH + lane;
     const float* sg = sG0 + buf * a.gbuf + i0 * w * nr * NF;
+    DPM_CHECK(((nr - 1) * a.prow + wy * MP + i0 + COL) * TPITCH <= a.pbuf && w <= a.w_max &&
+                  (min(FH, i0 + KS) * w * nr) * NF <= a.gbuf,
+              "compute reads stay inside the staged chunk");
     for (int j = 0; j < w; ++j) {
       for (int r = 0; r < nr; ++r) {
         const float* pc = sp + r * a.prow * TPITCH + j;

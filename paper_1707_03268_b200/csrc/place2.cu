@@ -340,6 +340,11 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
   auto screen = [&](int r, float& m1, float& m2, bool& full) {
     const float* row = band + r * COLS_PITCH;
     const float* s0 = row + c0 + cstep * xc;  // dx = 0
+    DPM_CHECK(r >= 0 && r < BAND2, "x pass: band row");
+    DPM_CHECK(c0 + cstep * xc - R1 >= 0 && c0 + cstep * xc + R1 < COLS_PITCH &&
+                  (!PACKED || (c0 + cstep * xc + xd.d0 >= 0 &&
+                               c0 + cstep * xc + xd.d0 + 2 * R1 < COLS_PITCH)),
+              "x pass: band column");
     if constexpr (PACKED) scr_packed<R1>(s0 + xd.d0, pp, s0[xd.ds] + pr[0], mask, m1, m2);
     else scr_strided<R1, 1>(s0, pr, mask, m1, m2);
     full = false;
@@ -350,10 +355,12 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
     const bool rare = live && (full || m1 < NONE_BELOW || m2 >= m1 - E2);
     const uint32_t bal = __ballot_sync(0xffffffffu, rare);
     if (bal != 0u) {
+      DPM_CHECK(it < 32, "x pass: at most 32 row iterations per warp");
       iters |= 1u << it;
       if (lane == 0) rmask[it] = bal;
     }
     if (live) {  // certified: the screen maximum, its code names the winner
+      DPM_CHECK(r >= 0 && r < BAND2 && xc >= 0 && xc < PT_W, "x pass: x word");
       x32[r * PT_W + xc] = m1;
       cmaxv = fmaxf(cmaxv, m1);
     }
@@ -417,6 +424,8 @@ __device__ __forceinline__ void y_group(const float* __restrict__ x32, const flo
     if (!root_of(k, iyr, ixr)) continue;
     const int cy = scale * (aj.ry0 + ty0 + iyr) + ay;
     const float* xcol = x32 + (cy - yb0) * PT_W + ixr;
+    DPM_CHECK(cy - yb0 - R1 >= 0 && cy - yb0 + R1 < BAND2 && ixr >= 0 && ixr < PT_W,
+              "y pass: x words of the inner window");
     float m1 = -INFINITY, m2 = -INFINITY;
     scr_strided<R1, PT_W>(xcol, pr, mask, m1, m2);
     const float lo = m1 - E2;
@@ -438,6 +447,8 @@ __device__ __forceinline__ void y_group(const float* __restrict__ x32, const flo
         const int dx = c == xd.c2r1 ? xd.ds : xd.d0 + c;
         const int cx = scale * (aj.rx0 + tx0 + ixr) + ax;
         stk = 1 | ((dy + 64) << 3) | ((dx + 64) << 10);
+        DPM_CHECK(cy + dy >= 0 && cy + dy < pjs->Hp && cx + dx >= 0 && cx + dx < pjs->Wp,
+                  "y pass: winner inside the map");
         sv[g] = __ldg(smap + (int64_t)(cy + dy) * pitch + cx + dx);
       }
     }
@@ -624,6 +635,8 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
     const int nrows = pj.scale * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
     const int xb0 = pj.scale * rx_lo + pj.ax - jr.rx;
     const int nbox = (nrows + TMA_BH - 1) / TMA_BH;
+    DPM_CHECK(nbox * TMA_BH <= BAND2 && xb0 - (xb0 & ~3) + pj.scale * (PT_W - 1) + 1 + 2 * jr.rx <= COLS_PITCH,
+              "band boxes fit the band buffer");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(band_bar),
                  "r"((uint32_t)nbox * TMA_BOX_BYTES)
@@ -683,6 +696,7 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
       const float sent = enc_code(OUT_SENTINEL, CODE_NONE);
       for (int i = tid; i < n_out * PT_W; i += THREADS) {
         const int k = i / PT_W, l = i - k * PT_W;
+        DPM_CHECK((k < r_lo ? k : r_hi + (k - r_lo)) < BAND2, "rows outside the map");
         x32[(k < r_lo ? k : r_hi + (k - r_lo)) * PT_W + l] = sent;
       }
       const int rpw = PT_W >> lpr_log;

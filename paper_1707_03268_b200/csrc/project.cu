@@ -31,6 +31,7 @@ project_kernel(const float* __restrict__ X, float* __restrict__ P, const float* 
   const int64_t cell0 = (int64_t)(blockIdx.x - job.block0) * K1_CELLS;
   const int ncell = (int)min((int64_t)K1_CELLS, ncells_level - cell0);
   const int t = threadIdx.x;
+  DPM_CHECK(ncell > 0 && ncell <= K1_CELLS, "CTA cells inside its level");
 
   for (int i = t; i < L * Rp; i += blockDim.x) {
     const int l = i / Rp, r = i % Rp;

@@ -180,6 +180,7 @@ prune_cover_kernel(const uint8_t* __restrict__ lim, const dpm_cover_job* __restr
   int m = 0;
   for (int iy = iy0; iy <= iy1; ++iy)
     for (int ix = ix0; ix <= ix1; ++ix) m = max(m, (int)lim[j.lim_off + (int64_t)iy * j.wr + ix]);
+  DPM_CHECK(m < 256, "cover histogram bin");
   if (m > 0) atomicAdd(hist + j.hist_off + m, 1u);
 }
 }  // namespace dpm
