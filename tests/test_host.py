@@ -140,3 +140,22 @@ def test_factor_fixtures_match_generators():
         T = synth.workload(cfg).bank.stacked()
         assert hashlib.sha256(np.ascontiguousarray(T).tobytes()).hexdigest() == str(fx["digest"])
         assert fx["G"].shape == (T.shape[0], R) and fx["C"].shape == (32, R)
+
+
+def test_segment_strips_cover_every_output_row_once():
+    """Small pyramids split their tcgen05 part strips into row segments
+    (engine._segment_strips); every output row of every strip is covered by
+    exactly one segment, and a batch with enough strips stays whole."""
+    from paper_1707_03268_b200.engine import _segment_strips
+    rng = np.random.default_rng(5)
+    strips = [(j, 0, int(sx), int(ho)) for j, (sx, ho) in
+              enumerate(zip(rng.integers(0, 4, 40), rng.integers(1, 200, 40)))]
+    segs = _segment_strips(strips, sms=148)
+    assert len(segs) > len(strips)
+    for j, _, sx, ho in strips:
+        rows = sorted(r for sj, y0, ssx, n, h in segs if sj == j and ssx == sx
+                      for r in range(y0, y0 + n))
+        assert rows == list(range(ho))
+        assert all(h == ho for sj, _, _, _, h in segs if sj == j)
+    whole = _segment_strips(strips, sms=10)
+    assert [(j, y0, sx, n) for j, y0, sx, n, _ in whole] == [(j, 0, sx, ho) for j, _, sx, ho in strips]
