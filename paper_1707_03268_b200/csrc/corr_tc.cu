@@ -39,6 +39,19 @@
 
 namespace dpm {
 
+// A strip is a 128-column band of one job's output rows, walked top to
+// bottom.  tile.pad > 0 makes it a segment: output rows [ty, ty + pad) (the
+// planner splits the tall strips of small pyramids this way so that every SM
+// gets work); pad == 0 is the whole strip.  Input rows staged for a segment:
+// [ty, min(ty + pad + fh - 1, H)).
+__device__ __forceinline__ int seg_out_rows(const dpm_corr_tile& st, int ho) {
+  return st.pad > 0 ? st.pad : ho;
+}
+__device__ __forceinline__ int seg_in_rows(const dpm_corr_tile& st, int H, int fh) {
+  return st.pad > 0 ? min(st.ty + st.pad + fh - 1, H) - st.ty : H;
+}
+
+
 #ifdef DPM_TC_PROBE
 // MMA-warp wait cycles (debug builds only, tools/tc_probe.py): accumulator
 // free, input rows staged, output rows, total loop cycles
@@ -158,6 +171,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
         const dpm_corr_job job = a.jobs[a.strips[st].job];
         const int ho = job.H - FH + 1;
+        DPM_CHECK(a.strips[st].pad == 0, "stacked-row strips are never segmented");
         int qready = 0;  // rows of this strip known to be staged
         int y = 0;
         for (; y < ho; y += KS, ++row_glob) {
@@ -221,8 +235,10 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       uint32_t qs = 0, qph = 0;    // ring slot / phase of the strip's input row 0
       uint32_t acc = 0, aph = 0;   // accumulator index / phase of the current output row
       for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
-        const dpm_corr_job job = a.jobs[a.strips[st].job];
-        const int ho = job.H - FH + 1;
+        const dpm_corr_tile strip = a.strips[st];
+        const dpm_corr_job job = a.jobs[strip.job];
+        const int ho = seg_out_rows(strip, job.H - FH + 1);  // this segment's output rows
+        const int hs = seg_in_rows(strip, job.H, FH);        // and staged input rows
         for (int y = 0; y < ho; ++y) {
           uint32_t sl[FH], ph[FH];  // slots / phases of input rows y .. y+FH-1
           sl[0] = qs;
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
           if (FH == 1) { if (++qs == ring) { qs = 0; qph ^= 1; } }
           if (++acc == TC_MAX_ACC) { acc = 0; aph ^= 1; }
         }
-        for (int rr = ho; rr < job.H; ++rr)  // rows never first of an output row
+        for (int rr = ho; rr < hs; ++rr)  // rows never first of an output row
           if (++qs == ring) { qs = 0; qph ^= 1; }
       }
 #ifdef DPM_TC_PROBE
@@ -300,6 +316,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
     for (int st = blockIdx.x; st < a.nstrips; st += gridDim.x) {
       const dpm_corr_job job = a.jobs[a.strips[st].job];
       const int ho = job.H - a.h + 1;
+      DPM_CHECK(a.strips[st].pad == 0, "generic-shape strips are never segmented");
       if (a.tc_off != nullptr) {
         const int64_t off = a.tc_off[a.strips[st].job];
         if (off != b_res) {
@@ -378,13 +395,14 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       const int64_t plane = (int64_t)job.H * job.pitch;
       const float* pbase = a.P + job.p_off + (int64_t)job.chan_off * plane;
       const int nelem = nq * tcols;
-      for (int q = pw; q < job.H; q += TC_PRODUCERS) {
+      const int hs = seg_in_rows(strip, job.H, FH > 0 ? FH : a.h);  // rows staged for the strip
+      for (int q = pw; q < hs; q += TC_PRODUCERS) {
         const uint32_t qg = q_glob + q;
         const uint32_t slot = qg % a.ring;
         mbar_wait(empty + slot, ((qg / a.ring) & 1) ^ 1);
         float4* hi = reinterpret_cast<float4*>(sA + slot * slot_bytes);
         float4* lo = hi + nelem;
-        const float* prow = pbase + (int64_t)q * job.pitch;
+        const float* prow = pbase + (int64_t)(strip.ty + q) * job.pitch;
         if constexpr (BF) {
           // R == 8: lane handles positions c = lane + 32k; hi as two tf32 quads,
           // lo as 8 bf16 (16 B) per position, one zero position past the row
@@ -454,7 +472,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         __syncwarp();
         if (lane == 0) mbar_arrive(full + slot);
       }
-      q_glob += job.H;
+      q_glob += hs;
     }
   } else {
     // =================== epilogue ===================
@@ -535,6 +553,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       const dpm_corr_tile strip = a.strips[st];
       const dpm_corr_job job = a.jobs[strip.job];
       const int ho = job.H - a.h + 1, wo = job.W - a.w + 1;
+      const int nout = seg_out_rows(strip, ho), hs = seg_in_rows(strip, job.H, a.h);
       const int x = strip.tx * TC_M + quarter * 32 + lane;
       float vmax[LOC], vmin[LOC];  // this warp's chunks only (chunk c -> local c / SPLIT)
 #pragma unroll
@@ -544,13 +563,13 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
       const bool xin = x < wo;
       // N is a compile-time constant for the fixed DPM shapes (N == NMAX)
       const int N = FH > 0 ? NMAX : a.N;
-      for (int y = 0; y < ho; ++y, ++row_glob) {
+      for (int y = 0; y < nout; ++y, ++row_glob) {
         const uint32_t b = row_glob & (TC_MAX_ACC - 1);
         mbar_wait(tfull + b, (row_glob / TC_MAX_ACC) & 1);
         tc_fence_after();
         if constexpr (FH > 0) release(1);  // input row y: no later output row reads it
         const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * (uint32_t)a.acc_cols;
-        float* dst = a.S + job.s_off + (int64_t)y * wp + x;
+        float* dst = a.S + job.s_off + (int64_t)(strip.ty + y) * wp + x;
         // CW filters at a time: hi-half columns [fc, fc+CW) and lo-half [N+fc, ...)
 #pragma unroll
         for (int fc = 0; fc < NMAX; fc += CW) {
@@ -582,7 +601,7 @@ __global__ void __launch_bounds__(32 * (1 + TC_PRODUCERS + EPI), 1) corr_tc_kern
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + b);
       }
-      if constexpr (FH > 0) release(job.H - ho);  // rows never first of an output row
+      if constexpr (FH > 0) release(hs - nout);  // rows never first of an output row
       if (a.ranges != nullptr && job.range_idx >= 0) {
 #pragma unroll
         for (int li = 0; li < LOC; ++li) {

@@ -14,6 +14,7 @@ HBM layout (per image, images stacked):
   S arena : response maps, one block [nf][Ho][Wo] per (level, filter group)
 """
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -310,8 +311,15 @@ class Plan:
         for fl, strips in sorted(tc_classes.items()):
             fd = self.filters[fl[0]]
             if _tc_compiled(fd.h, fd.w, fd.R):
+                # the one-row part kernel (6 x 6, more than 8 filters; tc_stack in
+                # corr_tc.cu) walks segments too, the stacked-row kernel whole strips
+                if fd.w == 6 and len(fl) > 8:
+                    strips = _segment_strips(strips, _sm_count())
                 strips = _snake_order(strips, key=lambda t: t[3], ctas=_sm_count())
-                arr = np.array([(j, 0, sx, 0) for j, _, sx, _ in strips], dtype=_lib.CORR_TILE)
+                arr = np.array([(j, y0, sx, n if n < ho_full else 0)
+                                for j, y0, sx, n, ho_full in
+                                ((t[0], t[1], t[2], t[3], t[4] if len(t) > 4 else t[3])
+                                 for t in strips)], dtype=_lib.CORR_TILE)
                 self._tc_classes.append((f"k2_tcgen05_{fd.h}x{fd.w}_nf{len(fl)}", fd.h, fd.w,
                                          fd.R, len(fl), self.tc_core_off[fl], arr, None))
             else:
@@ -814,6 +822,29 @@ def plan_signature(L, levels, n_images, Rtot, filters, apps_key, opts=()):
 def _spitch(w):
     """Row pitch (floats) of a response map of width w (s_pitch in csrc)."""
     return (w + 3) & ~3
+
+
+def _segment_strips(strips, sms, per_sm=2, min_rows=16):
+    """Split the tcgen05 part strips (job, 0, sx, ho) of a small pyramid into
+    row segments (job, y0, sx, rows, ho) so that the persistent grid (one CTA
+    per SM) gets about ``per_sm`` items per SM: a single 640x480 or 1920x1080
+    pyramid has only ~60-250 strips, each walked top to bottom by one CTA.  A
+    segment re-stages its filter's h - 1 halo rows; segments are at least
+    ``min_rows`` output rows.  Batches with enough strips are left whole (the
+    kernel reads rows = 0 as the whole strip).  Off under DPM_TC_PAIR=1 (the
+    CTA-pair kernel walks whole strips only)."""
+    if (len(strips) >= per_sm * sms or os.environ.get("DPM_TC_PAIR") == "1"
+            or os.environ.get("DPM_TC_SEGMENT") == "0"):
+        return [(j, 0, sx, ho, ho) for j, _, sx, ho in strips]
+    total = sum(t[3] for t in strips)
+    seg = max(min_rows, -(-total // (per_sm * sms)))
+    out = []
+    for j, _, sx, ho in strips:
+        n = -(-ho // seg)
+        step = -(-ho // n)
+        for y0 in range(0, ho, step):
+            out.append((j, y0, sx, min(step, ho - y0), ho))
+    return out
 
 
 def _snake_order(items, key, ctas=148):
