@@ -22,11 +22,14 @@
 // kernel and this one is opt-in (DPM_TC_PAIR=1); the maps are bit-identical
 // either way (tests/test_gpu_parity.py).
 //
-// Row split.  CTA r's ring position k holds input row k + r (rows past the
-// level are zero), so tap row i of output pair (2p, 2p + 1) is ring position
-// 2p + i in BOTH CTAs: one descriptor addresses both.  Each CTA stages every
-// row of the strip once, like the one-CTA kernel, and consumes H positions
-// per strip.
+// Row split.  The strip's ho output rows are halved: CTA r computes output
+// rows r*np .. r*np + np - 1 (np = ceil(ho / 2)), and its ring position k
+// holds input row k + r*np (rows past the level are zero), so tap row i of
+// output pair p (rows p and np + p) is ring position p + i in BOTH CTAs: one
+// descriptor addresses both.  Each CTA stages np + h - 1 rows per strip, so
+// the pair stages each row about once (an earlier split -- CTA r taking rows
+// 2p + r -- made BOTH CTAs stage every row of the strip, twice the staging of
+// the one-CTA kernel).
 //
 // Synchronisation (rank 0 = leader issues every MMA):
 //   full[s]   leader's barrier, 2 arrivals: each CTA's producer after staging
@@ -201,7 +204,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const dpm_corr_job job = a.jobs[a.strips[st].job];
         const int ho = job.H - FH + 1, np = (ho + 1) >> 1;
         for (int p = 0; p < np; ++p) {
-          uint32_t sl[FH], ph[FH];  // slots / phases of positions 2p .. 2p + FH - 1
+          uint32_t sl[FH], ph[FH];  // slots / phases of positions p .. p + FH - 1
           sl[0] = qs;
           ph[0] = qph;
 #pragma unroll
@@ -213,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           mbar_wait(tempty + acc, aph ^ 1);
 #pragma unroll
           for (int i = 0; i < FH; ++i)
-            if (p == 0 || i >= FH - 2) mbar_wait(full + sl[i], ph[i]);
+            if (p == 0 || i == FH - 1) mbar_wait(full + sl[i], ph[i]);
           tc_fence_after();
           const uint32_t d = tmem_base + acc * (uint32_t)a.acc_cols;
           uint64_t bB = dB0, bB2 = dB20;
@@ -238,11 +241,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             commit_pair(tfull + acc);
           }
           __syncwarp();
-          qs = sl[2];
-          qph = ph[2];
+          qs = sl[1];
+          qph = ph[1];
           if (++acc == TC_MAX_ACC) { acc = 0; aph ^= 1; }
         }
-        for (int rr = 2 * np; rr < job.H; ++rr)  // positions no pair starts at
+        for (int rr = np; rr < np + FH - 1; ++rr)  // positions no pair starts at
           if (++qs == ring) { qs = 0; qph ^= 1; }
       }
     }
@@ -258,11 +261,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int x0 = strip.tx * TC_M;
       const int64_t plane = (int64_t)job.H * job.pitch;
       const float* pbase = a.P + job.p_off + (int64_t)job.chan_off * plane;
-      for (int k = pw; k < job.H; k += PRODUCERS) {
+      const int np = (job.H - FH + 2) >> 1;  // output rows per CTA: ceil(ho / 2)
+      for (int k = pw; k < np + FH - 1; k += PRODUCERS) {
         const uint32_t qg = q_glob + k;
         const uint32_t slot = qg % ring;
         mbar_wait(empty + slot, ((qg / ring) & 1) ^ 1);
-        const int q = k + (int)rank;
+        const int q = k + (int)rank * np;
         float4* hi = reinterpret_cast<float4*>(sA + slot * SLOT_BYTES);
         uint4* lo16 = reinterpret_cast<uint4*>(sA + slot * SLOT_BYTES + HI_BYTES);
         const float* prow = pbase + (int64_t)q * job.pitch;
@@ -299,11 +303,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           else mbar_arrive_at(full + slot, 0);
         }
       }
-      q_glob += job.H;
+      q_glob += np + FH - 1;
     }
   } else {
     // =================== epilogue (both CTAs) ===================
-    // output row 2p + rank of pair p from this CTA's TMEM (lanes = positions)
+    // output row p + rank * np of pair p from this CTA's TMEM (lanes = positions)
     constexpr int CW = 8;                               // TMEM columns per chunk
     constexpr int LOC = ((N / CW + 1) / 2) * CW;        // filters per warp
     const int quarter = warp & 3;
@@ -332,8 +336,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const uint32_t b = row_glob & (TC_MAX_ACC - 1);
         mbar_wait(tfull + b, (row_glob / TC_MAX_ACC) & 1);
         tc_fence_after();
-        release(2);  // positions 2p, 2p + 1: no later pair reads them
-        const int y = 2 * p + (int)rank;
+        release(1);  // position p: no later pair reads it
+        const int y = p + (int)rank * np;
         if (y < ho) {
           const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * (uint32_t)a.acc_cols;
           float* dst = a.S + job.s_off + (int64_t)y * wp + x;
@@ -364,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           else mbar_arrive_relaxed_at(tempty + b, 0);
         }
       }
-      release(job.H - 2 * np);  // positions no pair starts at
+      release(FH - 1);  // positions no pair starts at
       if (a.ranges != nullptr && job.range_idx >= 0) {
 #pragma unroll
         for (int li = 0; li < LOC; ++li) {
