@@ -39,17 +39,6 @@
 
 namespace dpm {
 
-// A strip is a 128-column band of one job's output rows, walked top to
-// bottom.  tile.pad > 0 makes it a segment: output rows [ty, ty + pad) (the
-// planner splits the tall strips of small pyramids this way so that every SM
-// gets work); pad == 0 is the whole strip.  Input rows staged for a segment:
-// [ty, min(ty + pad + fh - 1, H)).
-__device__ __forceinline__ int seg_out_rows(const dpm_corr_tile& st, int ho) {
-  return st.pad > 0 ? st.pad : ho;
-}
-__device__ __forceinline__ int seg_in_rows(const dpm_corr_tile& st, int H, int fh) {
-  return st.pad > 0 ? min(st.ty + st.pad + fh - 1, H) - st.ty : H;
-}
 
 
 #ifdef DPM_TC_PROBE
@@ -683,12 +672,14 @@ static int tc_ring(int h, int w, int R, int nf) {
   return ring;
 }
 
-// CTA-pair kernel for the part shape (corr_tc2.cu), opt-in with
-// DPM_TC_PAIR=1: bit-identical maps, but not faster (DESIGN.md section 3,
-// "K2 on CTA pairs")
-static bool tc_pairs() {
+// CTA-pair kernel for the part shape (corr_tc2.cu, "K2
+// on CTA pairs"): by default for launches of at least 4 strips per SM;
+// DPM_TC_PAIR=0 always selects the one-CTA kernel (bit-identical maps),
+// DPM_TC_PAIR=1 pairs whatever the strip count (tests; the strips must be
+// whole: DPM_TC_SEGMENT=0 for small pyramids)
+static int tc_pairs_mode() {
   const char* e = getenv("DPM_TC_PAIR");
-  return e && e[0] == '1';
+  return e && e[0] == '0' ? 0 : e && e[0] == '1' ? 1 : 2;
 }
 
 extern "C" int dpm_correlate_tc_stack(int h, int w, int R, int nf) { return tc_stack(h, w, R, nf); }
@@ -748,8 +739,12 @@ static int tc_launch(const float* P, const float* Gtc, const int64_t* tc_off, fl
     a.acc_cols = 16 * ks;
     a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
     fn = w == 11 ? corr_tc_kernel<8, 6, 11, 4, 6> : corr_tc_kernel<8, 6, 6, 4, 6>;
-  } else if (h == 6 && w == 6 && R == 8 && tc_pairs()) {
-    return launch_tc_pair(a, as_stream(stream));  // DPM part filters: cta_group::2 pairs
+  } else if (h == 6 && w == 6 && R == 8 &&
+             (tc_pairs_mode() == 1 || (tc_pairs_mode() == 2 && nstrips >= 4 * sms))) {
+    // DPM part filters: cta_group::2 pairs, on whole strips only.  The planner
+    // (engine._segment_strips) splits strips only below 2 strips per SM, which
+    // leaves fewer than 4 per SM, so segmented lists never reach this kernel.
+    return launch_tc_pair(a, as_stream(stream));
   } else if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps (12 measured slower)
     fn = N <= 16 ? corr_tc_kernel<16, 6, 6, 8>
        : N <= 32 ? corr_tc_kernel<32, 6, 6, 8>

@@ -262,6 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int64_t plane = (int64_t)job.H * job.pitch;
       const float* pbase = a.P + job.p_off + (int64_t)job.chan_off * plane;
       const int np = (job.H - FH + 2) >> 1;  // output rows per CTA: ceil(ho / 2)
+      DPM_CHECK(strip.pad == 0, "CTA-pair strips are never segmented");
       for (int k = pw; k < np + FH - 1; k += PRODUCERS) {
         const uint32_t qg = q_glob + k;
         const uint32_t slot = qg % ring;
@@ -324,7 +325,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int st = cluster; st < a.nstrips; st += nclusters) {
       const dpm_corr_tile strip = a.strips[st];
       const dpm_corr_job job = a.jobs[strip.job];
-      const int ho = job.H - FH + 1, wo = job.W - FW + 1, np = (ho + 1) >> 1;
+      const int ho = job.H - FH + 1, wo = job.W - FW + 1;
+      const int np = (ho + 1) >> 1;
       const int x = strip.tx * TC_M + quarter * 32 + lane;
       float vmax[LOC], vmin[LOC];
 #pragma unroll
@@ -341,22 +343,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (y < ho) {
           const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * (uint32_t)a.acc_cols;
           float* dst = a.S + job.s_off + (int64_t)y * wp + x;
+          // all of this warp's chunks in flight, then one wait
+          constexpr int NCH = LOC / CW;
+          float vh[NCH][CW], vl[NCH][CW];
 #pragma unroll
-          for (int fc = 0; fc < N; fc += CW) {
-            if ((fc / CW) % 2 == half) {
-              float vh[CW], vl[CW];
-              tmem_ld8(taddr + fc, vh);
-              tmem_ld8(taddr + N + fc, vl);
-              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int c = 0; c < NCH; ++c) {
+            const int fc = (2 * c + half) * CW;
+            if (fc < N) {
+              tmem_ld8(taddr + fc, vh[c]);
+              tmem_ld8(taddr + N + fc, vl[c]);
+            }
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-              for (int k = 0; k < CW; ++k) {
-                const int f = fc + k, li = (fc / CW / 2) * CW + k;
-                if (f < job.nf && xin) {
-                  const float sv = vh[k] + vl[k];
-                  dst[(int64_t)f * plane] = sv;
-                  vmax[li] = fmaxf(vmax[li], sv);
-                  vmin[li] = fminf(vmin[li], sv);
-                }
+          for (int c = 0; c < NCH; ++c) {
+            const int fc = (2 * c + half) * CW;
+#pragma unroll
+            for (int k = 0; k < CW; ++k) {
+              const int f = fc + k, li = c * CW + k;
+              if (fc < N && f < job.nf && xin) {
+                const float sv = vh[c][k] + vl[c][k];
+                dst[(int64_t)f * plane] = sv;
+                vmax[li] = fmaxf(vmax[li], sv);
+                vmin[li] = fminf(vmin[li], sv);
               }
             }
           }

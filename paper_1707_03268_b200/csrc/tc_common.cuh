@@ -179,4 +179,16 @@ size_t tc16_core_floats();
 size_t tc16_smem(int* ring_out);
 int launch_tc16(TcArgs a, cudaStream_t stream);
 
+// A strip is a 128-column band of one job's output rows, walked top to
+// bottom.  tile.pad > 0 makes it a segment: output rows [ty, ty + pad) (the
+// planner splits the tall strips of small pyramids this way so that every SM
+// gets work); pad == 0 is the whole strip.  Input rows staged for a segment:
+// [ty, min(ty + pad + fh - 1, H)).
+__device__ __forceinline__ int seg_out_rows(const dpm_corr_tile& st, int ho) {
+  return st.pad > 0 ? st.pad : ho;
+}
+__device__ __forceinline__ int seg_in_rows(const dpm_corr_tile& st, int H, int fh) {
+  return st.pad > 0 ? min(st.ty + st.pad + fh - 1, H) - st.ty : H;
+}
+
 }  // namespace dpm

@@ -831,10 +831,8 @@ def _segment_strips(strips, sms, per_sm=2, min_rows=16):
     pyramid has only ~60-250 strips, each walked top to bottom by one CTA.  A
     segment re-stages its filter's h - 1 halo rows; segments are at least
     ``min_rows`` output rows.  Batches with enough strips are left whole (the
-    kernel reads rows = 0 as the whole strip).  Off under DPM_TC_PAIR=1 (the
-    CTA-pair kernel walks whole strips only)."""
-    if (len(strips) >= per_sm * sms or os.environ.get("DPM_TC_PAIR") == "1"
-            or os.environ.get("DPM_TC_SEGMENT") == "0"):
+    kernels read rows = 0 as the whole strip); DPM_TC_SEGMENT=0 turns it off."""
+    if len(strips) >= per_sm * sms or os.environ.get("DPM_TC_SEGMENT") == "0":
         return [(j, 0, sx, ho, ho) for j, _, sx, ho in strips]
     total = sum(t[3] for t in strips)
     seg = max(min_rows, -(-total // (per_sm * sms)))

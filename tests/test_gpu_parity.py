@@ -563,7 +563,7 @@ def test_tensor_core_multi_group_launch_matches_oracle(shape, generic, name):
 
 def test_part_correlation_cta_pairs_bit_identical_to_one_cta_kernel(monkeypatch):
     """The part shape (6 x 6 taps, R = 8) on CTA pairs (cta_group::2, M =
-    256, corr_tc2.cu, opt-in with DPM_TC_PAIR=1): the same MMAs in the same
+    256, corr_tc2.cu; forced with DPM_TC_PAIR=1): the same MMAs in the same
     order as the one-CTA kernel, so the maps are bit-identical -- odd and
     even output heights, one-row levels, 16..64 filters, more strips than
     SM pairs."""
@@ -576,6 +576,7 @@ def test_part_correlation_cta_pairs_bit_identical_to_one_cta_kernel(monkeypatch)
         cores = [rng.normal(0, 0.05, (6, 6, 8)).astype(np.float32) for _ in range(nf)]
         data = [rng.random((H, W, 32)).astype(np.float32) for H, W in levels]
         maps = []
+        monkeypatch.setenv("DPM_TC_SEGMENT", "0")  # the pair kernel walks whole strips
         for pair in ("1", "0"):
             monkeypatch.setenv("DPM_TC_PAIR", pair)
             plan = Plan(32, levels, C, [FilterDef(c) for c in cores],
