@@ -673,7 +673,7 @@ static int tc_ring(int h, int w, int R, int nf) {
 }
 
 // CTA-pair kernel for the part shape (corr_tc2.cu, "K2
-// on CTA pairs"): by default for launches of at least 4 strips per SM;
+// on CTA pairs"): by default for launches of at least 2 strips per SM;
 // DPM_TC_PAIR=0 always selects the one-CTA kernel (bit-identical maps),
 // DPM_TC_PAIR=1 pairs whatever the strip count (tests; the strips must be
 // whole: DPM_TC_SEGMENT=0 for small pyramids)
@@ -740,10 +740,10 @@ static int tc_launch(const float* P, const float* Gtc, const int64_t* tc_off, fl
     a.nacc = 512 / a.acc_cols > TC_MAX_ACC ? TC_MAX_ACC : 512 / a.acc_cols;
     fn = w == 11 ? corr_tc_kernel<8, 6, 11, 4, 6> : corr_tc_kernel<8, 6, 6, 4, 6>;
   } else if (h == 6 && w == 6 && R == 8 &&
-             (tc_pairs_mode() == 1 || (tc_pairs_mode() == 2 && nstrips >= 4 * sms))) {
+             (tc_pairs_mode() == 1 || (tc_pairs_mode() == 2 && nstrips >= 2 * sms))) {
     // DPM part filters: cta_group::2 pairs, on whole strips only.  The planner
-    // (engine._segment_strips) splits strips only below 2 strips per SM, which
-    // leaves fewer than 4 per SM, so segmented lists never reach this kernel.
+    // (engine._segment_strips) splits strips only below 2 strips per SM and
+    // keeps the segments below 2 per SM, so segmented lists never reach it.
     return launch_tc_pair(a, as_stream(stream));
   } else if (h == 6 && w == 6 && R == 8) {  // DPM part filters: 8 epilogue warps (12 measured slower)
     fn = N <= 16 ? corr_tc_kernel<16, 6, 6, 8>

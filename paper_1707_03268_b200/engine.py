@@ -836,6 +836,10 @@ def _segment_strips(strips, sms, per_sm=2, min_rows=16):
         return [(j, 0, sx, ho, ho) for j, _, sx, ho in strips]
     total = sum(t[3] for t in strips)
     seg = max(min_rows, -(-total // (per_sm * sms)))
+    # fewer than per_sm * sms segments: the C side pairs CTAs (corr_tc2.cu) only
+    # for launches of at least 2 strips per SM, which must be whole strips
+    while sum(-(-ho // seg) for _, _, _, ho in strips) >= per_sm * sms:
+        seg += max(1, seg // 16)
     out = []
     for j, _, sx, ho in strips:
         n = -(-ho // seg)
