@@ -355,17 +355,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (xin && job.nf >= N) {  // every filter of the padded group is real: no predicates
 #pragma unroll
-          for (int c = 0; c < NCH; ++c) {
-            const int fc = (2 * c + half) * CW;
+            for (int c = 0; c < NCH; ++c) {
+              const int fc = (2 * c + half) * CW;
+              if (fc >= N) continue;
+              float* d = dst + (int64_t)fc * plane;
 #pragma unroll
-            for (int k = 0; k < CW; ++k) {
-              const int f = fc + k, li = c * CW + k;
-              if (fc < N && f < job.nf && xin) {
+              for (int k = 0; k < CW; ++k, d += plane) {
+                const int li = c * CW + k;
                 const float sv = vh[c][k] + vl[c][k];
-                dst[(int64_t)f * plane] = sv;
+                *d = sv;
                 vmax[li] = fmaxf(vmax[li], sv);
                 vmin[li] = fminf(vmin[li], sv);
+              }
+            }
+          } else if (xin) {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+              const int fc = (2 * c + half) * CW;
+#pragma unroll
+              for (int k = 0; k < CW; ++k) {
+                const int f = fc + k, li = c * CW + k;
+                if (fc < N && f < job.nf) {
+                  const float sv = vh[c][k] + vl[c][k];
+                  dst[(int64_t)f * plane] = sv;
+                  vmax[li] = fmaxf(vmax[li], sv);
+                  vmin[li] = fminf(vmin[li], sv);
+                }
               }
             }
           }
