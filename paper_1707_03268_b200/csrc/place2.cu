@@ -32,10 +32,9 @@
 // whose dx the y pass recovers by the same exact scan from global memory),
 // so the x loop stores its screen maximum as is.
 //
-// Structure.  CTA = 12 warps, 32 x 48 root tile of one (image, component,
-// root level), two CTAs per SM (80 registers: 24 warps per SM measured
-// faster than 16 warps at 128 registers -- 7.77 against 8.05 ms -- and than
-// 32 at 64, which spills).  Per part:
+// Structure.  CTA = 8 warps, 32 x 32 root tile of one (image, component,
+// root level), three CTAs per SM (24 warps, 85 registers; 64 KB of shared
+// memory each).  Per part:
 //   wait for the part's S band (TMA boxes, NaN outside the map, mbarrier),
 //   x pass over the band rows (lane = centre column), per-warp column maxima,
 //   one CTA barrier (x words complete, band buffer free, the next part's job
@@ -43,11 +42,19 @@
 //   y pass for the thread's 4 roots: screen the x words of the column; the
 //   winner's exact FP64 value from its S value in global memory (L2
 //   resident: the TMA just streamed it), so the y pass never reads the band
-//   and the next band lands underneath it.
-// x words are double-buffered by part parity and job records / tables
-// triple-buffered, so one barrier per part orders everything.  Warp 0 copies
-// the next part's job record (cp.async) and builds its penalty tables (FP32
-// screen values, exact FP64 penalties) during the x pass.
+//   and the next band lands underneath it,
+//   a second barrier before the next part's x pass overwrites the x words.
+// Job records / tables are triple-buffered; warp 0 copies the next part's
+// job record (cp.async) and builds its penalty tables (FP32 screen values,
+// exact FP64 penalties) during the x pass.
+// Geometry, measured at config 4 (7.77 -> 7.47 ms came from screening work;
+// these are the same kernel at other shapes): 12 warps x 48 rows, two CTAs
+// per SM, x words double-buffered (one barrier per part): 7.47 ms; the same
+// with one x buffer: 7.76; 8 warps x 32 rows at two CTAs per SM (128
+// registers): 8.14; 8 warps x 32 rows, one x buffer, THREE CTAs per SM:
+// 7.28 ms (the default).  More independent CTAs per SM hide the per-part
+// barrier better than the second barrier costs.  DPM_K3_THREADS / _TH /
+// _XBUF / _MINB rebuild the others.
 #include <math.h>
 
 #include "place_common.cuh"
@@ -55,9 +62,22 @@
 namespace dpm {
 namespace k3v2 {
 
-constexpr int THREADS = 384;
+#ifndef DPM_K3_THREADS
+#define DPM_K3_THREADS 256
+#endif
+#ifndef DPM_K3_TH
+#define DPM_K3_TH 32
+#endif
+#ifndef DPM_K3_XBUF
+#define DPM_K3_XBUF 1
+#endif
+#ifndef DPM_K3_MINB
+#define DPM_K3_MINB 3
+#endif
+constexpr int THREADS = DPM_K3_THREADS;  // tile geometry: see "Shape" above (A/B macros)
+constexpr int XBUF = DPM_K3_XBUF;         // x-word buffers (2: one barrier per part)
 constexpr int WARPS = THREADS / 32;
-constexpr int TH = 48;                      // root rows per tile (32 columns)
+constexpr int TH = DPM_K3_TH;               // root rows per tile (32 columns)
 constexpr int RPT = TH * PT_W / THREADS;    // roots per thread
 static_assert(RPT * THREADS == TH * PT_W, "whole roots per thread");
 constexpr int BAND2 = (2 * (TH - 1) + 1 + 2 * RCAP + TMA_BH - 1) / TMA_BH * TMA_BH;  // 128 band rows
@@ -80,9 +100,9 @@ struct PartTab {
 
 struct __align__(128) Smem {
   float s[BAND2 * COLS_PITCH];     // S band (TMA, NaN outside the map)
-  float x32[2][BAND2 * PT_W];      // x words by part parity
+  float x32[XBUF][BAND2 * PT_W];   // x words by part parity
   double tot[RPT][THREADS];        // running totals of the roots, summed in part order
-  float cm[2][WARPS][PT_W];        // per-warp column maxima of the x words
+  float cm[XBUF][WARPS][PT_W];     // per-warp column maxima of the x words
   uint32_t rmask[WARPS][32];       // x pass: lane masks of the rows to rescan exactly
   PartTab tab[3];                  // tables of part q at slot q % 3
   alignas(16) JobRange jr[3];
@@ -552,7 +572,7 @@ __device__ __forceinline__ void build_tab(PartTab& tb, const dpm_place_job& pj, 
   }
 }
 
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, DPM_K3_MINB)
 place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ smaps,
               const dpm_place_job* __restrict__ pjobs, const dpm_asm_job* __restrict__ ajobs,
               int najobs, const dpm_place_range* __restrict__ prep, double* __restrict__ total,
@@ -661,7 +681,8 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
   double* const placedb = aj.placed_off >= 0 ? placed + aj.placed_off : nullptr;
   const int xsub = lane >> lpr_log, xc = lane & (lpr - 1);
   for (int p = 0; p < aj.nparts; ++p) {
-    const int slot = p % 3, buf = p & 1;
+    const int slot = p % 3, buf = XBUF == 2 ? p & 1 : 0;
+    if (XBUF == 1 && p > 0) __syncthreads();  // y(p-1) done with the single x-word buffer
     const dpm_place_job& pj = sh.pj[slot];
     const JobRange& jr = sh.jr[slot];
     const PartTab& tb = sh.tab[slot];
