@@ -592,6 +592,67 @@ def test_part_correlation_cta_pairs_bit_identical_to_one_cta_kernel(monkeypatch)
                                               err_msg=f"nf {nf} level {levels[k]} filter {f}")
 
 
+def test_part_strip_segments_bit_identical_to_whole_strips(monkeypatch):
+    """Row segments of the tcgen05 part strips (engine._segment_strips, used
+    when a launch has fewer than 2 strips per SM) compute the same rows with
+    the same MMAs as whole strips: bit-identical maps, at odd heights and one
+    strip taller than the segment size; the segmented plan really splits."""
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    rng = np.random.default_rng(21)
+    levels = [(90, 300), (7, 140), (41, 261), (130, 40)]
+    nf = 24
+    C = rng.normal(size=(32, 8)).astype(np.float32)
+    cores = [rng.normal(0, 0.05, (6, 6, 8)).astype(np.float32) for _ in range(nf)]
+    data = [rng.random((H, W, 32)).astype(np.float32) for H, W in levels]
+    maps, nseg = [], []
+    for seg in ("0", "1"):
+        monkeypatch.setenv("DPM_TC_SEGMENT", seg)
+        plan = Plan(32, levels, C, [FilterDef(c) for c in cores],
+                    apps=[(k, f) for k in range(len(levels)) for f in range(nf)], outputs=(),
+                    tensor_cores=True)
+        nseg.append(sum(len(st) for *_, st, _ in plan._tc_classes))
+        plan.load_levels(0, data)
+        plan.run(stages=("project", "correlate"))
+        maps.append([[plan.map(0, k, f).cpu().numpy().copy() for f in range(nf)]
+                     for k in range(len(levels))])
+    assert nseg[1] > nseg[0]
+    for k in range(len(levels)):
+        for f in range(nf):
+            np.testing.assert_array_equal(maps[0][k][f], maps[1][k][f],
+                                          err_msg=f"level {levels[k]} filter {f}")
+
+
+def test_few_filter_kernel_deterministic_and_matches_oracle():
+    """The few-filter K2 (correlate_few.cu: filter rows split across warps,
+    partial sums added in a fixed order) gives bit-identical maps run to run,
+    and matches the float64 oracle at 1e-5 for 15 x 15, 11 x 15 and 5 x 8
+    groups of 2-8 filters at R = 32 (several rank chunks)."""
+    from paper_1707_03268_b200.engine import FilterDef, Plan
+
+    rng = np.random.default_rng(22)
+    levels = [(70, 90), (23, 17), (16, 160)]
+    shapes = [(15, 15), (15, 15), (11, 15), (11, 15), (5, 8), (5, 8), (5, 8), (5, 8), (5, 8)]
+    C = rng.normal(size=(32, 32)).astype(np.float32)
+    cores = [rng.normal(0, 0.05, (h, w, 32)).astype(np.float32) for h, w in shapes]
+    data = [rng.random((H, W, 32)).astype(np.float32) for H, W in levels]
+    runs = []
+    for _ in range(2):
+        plan = Plan(32, levels, C, [FilterDef(c) for c in cores],
+                    apps=[(k, f) for k in range(len(levels)) for f in range(len(cores))],
+                    outputs=(), tensor_cores=False)
+        plan.load_levels(0, data)
+        plan.run(stages=("project", "correlate"))
+        runs.append({(k, f): plan.map(0, k, f).cpu().numpy().copy()
+                     for k in range(len(levels)) for f in range(len(cores))})
+    for key, m in runs[0].items():
+        np.testing.assert_array_equal(m, runs[1][key], err_msg=f"run to run {key}")
+        k, f = key
+        filt = np.einsum("ijr,cr->ijc", cores[f].astype(np.float64), C.astype(np.float64))
+        ref = O.correlate3_full(data[k].astype(np.float64), filt)
+        assert_map_close(m, ref, f"level {levels[k]} filter {shapes[f]}")
+
+
 def test_score_batch_pipelined_matches_full_run():
     """The chunk-pipelined public call returns exactly the detections of one
     full-batch run (same records as a set)."""
