@@ -47,18 +47,24 @@ def main():
     evals = sum((pyr.levels[k][0] - bank.filters[f].shape[0] + 1) *
                 (pyr.levels[k][1] - bank.filters[f].shape[1] + 1) for k, f in apps)
 
+    # (name, C, filters, R, tensor cores): R = 8 both ways, so the decomposed-vs-dense
+    # ratio is also quoted FFMA against FFMA (R = 32 and dense run FFMA either way)
     variants = []
     for R in (8, 32):
         fx = np.load(os.path.join(REPO, "paper_1707_03268_b200", "data", f"factors_cfg5_R{R}.npz"))
         cores = cores_from_stacked(bank, fx["G"])
-        variants.append((f"decomposed R={R}", fx["C"], [FilterDef(c) for c in cores], R))
+        variants.append((f"decomposed R={R}", fx["C"], [FilterDef(c) for c in cores], R, True))
+        if R == 8:
+            variants.append(("decomposed R=8, FFMA only", fx["C"], [FilterDef(c) for c in cores],
+                             R, False))
     dense = [FilterDef(np.ascontiguousarray(f, dtype=np.float32)) for f in bank.filters]
-    variants.append(("dense 32-channel (C = I)", np.eye(32, dtype=np.float32), dense, 32))
+    variants.append(("dense 32-channel (C = I)", np.eye(32, dtype=np.float32), dense, 32, True))
 
     levels = [synth.hog_pyramid(5, img, pyr) for img in range(args.images)]
     out = []
-    for name, C, filters, R in variants:
-        plan = Plan(32, pyr.levels, C, filters, apps=apps, n_images=args.images, outputs=())
+    for name, C, filters, R, tc in variants:
+        plan = Plan(32, pyr.levels, C, filters, apps=apps, n_images=args.images, outputs=(),
+                    tensor_cores=tc)
         for img in range(args.images):
             plan.load_levels(img, levels[img])
         for _ in range(args.warmup):
