@@ -53,8 +53,10 @@
 // with one x buffer: 7.76; 8 warps x 32 rows at two CTAs per SM (128
 // registers): 8.14; 8 warps x 32 rows, one x buffer, THREE CTAs per SM:
 // 7.28 ms (the default).  More independent CTAs per SM hide the per-part
-// barrier better than the second barrier costs.  DPM_K3_THREADS / _TH /
-// _XBUF / _MINB rebuild the others.
+// barrier better than the second barrier costs: with the column maxima kept
+// as one shared atomic-max row per part (instead of per-warp rows), two x
+// buffers also fit three CTAs per SM (75.5 KB) and measured the same 7.28 ms.
+// DPM_K3_THREADS / _TH / _XBUF / _MINB rebuild the others.
 #include <math.h>
 
 #include "place_common.cuh"
@@ -76,6 +78,7 @@ namespace k3v2 {
 #endif
 constexpr int THREADS = DPM_K3_THREADS;  // tile geometry: see "Shape" above (A/B macros)
 constexpr int XBUF = DPM_K3_XBUF;         // x-word buffers (2: one barrier per part)
+constexpr int RMASK = 16;                 // x-pass row iterations per warp and part (<= 12 here)
 constexpr int WARPS = THREADS / 32;
 constexpr int TH = DPM_K3_TH;               // root rows per tile (32 columns)
 constexpr int RPT = TH * PT_W / THREADS;    // roots per thread
@@ -102,8 +105,8 @@ struct __align__(128) Smem {
   float s[BAND2 * COLS_PITCH];     // S band (TMA, NaN outside the map)
   float x32[XBUF][BAND2 * PT_W];   // x words by part parity
   double tot[RPT][THREADS];        // running totals of the roots, summed in part order
-  float cm[XBUF][WARPS][PT_W];     // per-warp column maxima of the x words
-  uint32_t rmask[WARPS][32];       // x pass: lane masks of the rows to rescan exactly
+  uint32_t cmk[3][PT_W];           // column maxima of the x words (float_key), part q at q % 3
+  uint32_t rmask[WARPS][RMASK];    // x pass: lane masks of the rows to rescan exactly
   PartTab tab[3];                  // tables of part q at slot q % 3
   alignas(16) JobRange jr[3];
   alignas(16) dpm_place_job pj[3];
@@ -375,9 +378,9 @@ __device__ __forceinline__ void x_pass(float* __restrict__ x32, const float* __r
     const bool rare = live && (full || m1 < NONE_BELOW || m2 >= m1 - E2);
     const uint32_t bal = __ballot_sync(0xffffffffu, rare);
     if (bal != 0u) {
-      DPM_CHECK(it < 32, "x pass: at most 32 row iterations per warp");
+      DPM_CHECK(it < RMASK, "x pass: at most RMASK row iterations per warp");
       iters |= 1u << it;
-      if (lane == 0) rmask[it] = bal;
+      if (lane == 0) rmask[it] = bal;  // it < RMASK (checked above)
     }
     if (live) {  // certified: the screen maximum, its code names the winner
       DPM_CHECK(r >= 0 && r < BAND2 && xc >= 0 && xc < PT_W, "x pass: x word");
@@ -592,6 +595,7 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(band_bar));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (tid < 3 * PT_W) (&sh.cmk[0][0])[tid] = 0u;  // float_key(-inf) > 0: every value beats it
   __syncthreads();
   const dpm_asm_job& aj = sh.aj;
   const int hr = aj.ry1 - aj.ry0 + 1, wr = aj.rx1 - aj.rx0 + 1;
@@ -683,6 +687,9 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
   for (int p = 0; p < aj.nparts; ++p) {
     const int slot = p % 3, buf = XBUF == 2 ? p & 1 : 0;
     if (XBUF == 1 && p > 0) __syncthreads();  // y(p-1) done with the single x-word buffer
+    // column maxima of part p+1 go to slot (p+1) % 3, last read by y(p-2), which
+    // every warp finished before the barrier after x(p-1)
+    if (warp == 0) sh.cmk[(p + 1) % 3][lane] = 0u;
     const dpm_place_job& pj = sh.pj[slot];
     const JobRange& jr = sh.jr[slot];
     const PartTab& tb = sh.tab[slot];
@@ -755,7 +762,7 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1)
         if (o >= lpr) cmaxv = fmaxf(cmaxv, __shfl_xor_sync(0xffffffffu, cmaxv, o));
-      if (xsub == 0) sh.cm[buf][warp][xc] = cmaxv;
+      if (xsub == 0) atomicMax(&sh.cmk[slot][xc], float_key(cmaxv));
     }
     if (warp == 0 && have_next) finish_job(p + 1);
     __syncthreads();  // x(p) done: x words visible, band buffer free, tables of p+1 built
@@ -783,11 +790,7 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
     // the column maximum of this thread's roots (every root of a thread has
     // the column tid & (lpr - 1))
     float cmax = -INFINITY;
-    if (ry > R1MAX) {
-      const int col = tid & (lpr - 1);
-#pragma unroll
-      for (int w = 0; w < WARPS; ++w) cmax = fmaxf(cmax, sh.cm[buf][w][col]);
-    }
+    if (ry > R1MAX) cmax = key_float(sh.cmk[slot][tid & (lpr - 1)]);
 #define DPM_YARGS x32, sm, pitch, &pj, tb, xd, rx, ry, yb0, ty0, tx0, mask, root_of, aj, p, hr, wr, tot, posb, placedb, cmax
     if (ry > R1MAX) {
       y_pass<R1MAX, true>(DPM_YARGS);
