@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DPM_ABI_VERSION 3
+#define DPM_ABI_VERSION 4
 #define DPM_MAX_PARTS 16
 
 typedef enum {
@@ -255,8 +255,9 @@ typedef struct {
   int32_t part_job0;  /* first dpm_place_job of this assembly                 */
   int32_t nparts;
   int32_t image, level, component;
-  int32_t block0;     /* first CTA; set by dpm_assemble_prepare               */
-  int32_t pad;
+  int32_t block0;     /* first CTA of the specialised K3 kernel (its tiles)   */
+  int32_t block1;     /* first CTA of the generic K3 kernel (the others);     */
+                      /*   both set by dpm_assemble_prepare                   */
   double bias;
 } dpm_asm_job;
 
@@ -266,12 +267,16 @@ typedef struct {
   uint32_t parts[DPM_MAX_PARTS]; /* (int16 y) << 16 | (uint16)(int16 x) */
 } dpm_detection;
 
-/* Validates both tables (host memory), fills block0 of the assembly jobs and
- * returns the CTA count to pass to dpm_assemble.  One job's outputs
- * (nparts x hr x wr) must stay below 2^31 elements (32-bit offsets inside a
- * job); larger rectangles are split by the caller. */
+/* Validates both tables (host memory), numbers the root tiles of the
+ * assembly jobs (block0 / block1) and returns the total CTA count to pass to
+ * dpm_assemble; *nfast (if not NULL) receives how many of them run on the
+ * specialised kernel (tiles at least 17 roots wide of jobs whose parts are
+ * all at scale 2 with radius < 0 or 7 <= radius <= 16; see place2.cu), the
+ * rest run on the generic one.  One job's outputs (nparts x hr x wr) must
+ * stay below 2^31 elements (32-bit offsets inside a job); larger rectangles
+ * are split by the caller. */
 int64_t dpm_assemble_prepare(dpm_asm_job* jobs_host, int njobs, const dpm_place_job* pjobs_host,
-                             int npjobs);
+                             int npjobs, int64_t* nfast);
 
 /* K3 prologue, once per run after K2: per placement job, the radius on each
  * axis (the job's radius, or r* from its map range when radius < 0), the
@@ -310,7 +315,8 @@ int dpm_smap_encode(const float* S, const dpm_smap_desc* descs_host, int n, void
  * Detections require the positions output. */
 int dpm_assemble(const float* S, const void* smaps, const dpm_place_job* pjobs,
                  const dpm_asm_job* ajobs,
-                 int najobs, int64_t nblocks, const dpm_place_range* prep, double* total,
+                 int najobs, int64_t nfast, int64_t nblocks, const dpm_place_range* prep,
+                 double* total,
                  uint32_t* pos, double* placed, double tau, dpm_detection* dets, int max_dets,
                  int* det_count, void* stream);
 

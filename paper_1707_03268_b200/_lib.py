@@ -18,7 +18,7 @@ __all__ = ["lib", "check", "PROJ_JOB", "CORR_JOB", "CORR_TILE", "PLACE_JOB", "AS
 LIB_PATH = os.environ.get("DPM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                                                    "libdpm_b200.so")
 MAX_PARTS = 16
-ABI_VERSION = 3  # DPM_ABI_VERSION of include/dpm_b200.h
+ABI_VERSION = 4  # DPM_ABI_VERSION of include/dpm_b200.h
 
 DPM_OK, DPM_ERR_ARG, DPM_ERR_UNSUPPORTED, DPM_ERR_CUDA, DPM_ERR_NUMERIC = 0, -1, -2, -3, -4
 
@@ -41,7 +41,7 @@ ASM_JOB = np.dtype([("root_off", "<i8"), ("total_off", "<i8"), ("pos_off", "<i8"
                     ("placed_off", "<i8"), ("root_pitch", "<i4"), ("ry0", "<i4"),
                     ("ry1", "<i4"), ("rx0", "<i4"), ("rx1", "<i4"), ("part_job0", "<i4"),
                     ("nparts", "<i4"), ("image", "<i4"), ("level", "<i4"),
-                    ("component", "<i4"), ("block0", "<i4"), ("pad", "<i4"),
+                    ("component", "<i4"), ("block0", "<i4"), ("block1", "<i4"),
                     ("bias", "<f8")], align=True)
 DETECTION = np.dtype([("image", "<i4"), ("level", "<i4"), ("component", "<i4"), ("ry", "<i4"),
                       ("rx", "<i4"), ("nparts", "<i4"), ("score", "<f8"),
@@ -109,9 +109,9 @@ _SIGNATURES = {
     "dpm_correlate_tc_core_floats": (ctypes.c_size_t, [_i32, _i32, _i32, _i32]),
     "dpm_correlate_tc_stack": (_i32, [_i32, _i32, _i32, _i32]),
     "dpm_place_prepare": (_i64, [_vp, _i32]),
-    "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32]),
+    "dpm_assemble_prepare": (_i64, [_vp, _i32, _vp, _i32, _vp]),
     "dpm_place_ranges": (_i32, [_vp, _i32, _vp, _vp, _vp]),
-    "dpm_assemble": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32,
+    "dpm_assemble": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _vp, _dbl, _vp, _i32,
                             _vp, _vp]),
     "dpm_smap_encode": (_i32, [_vp, _vp, _i32, _vp]),
     "dpm_gdt_x_prepare": (_i64, [_vp, _i32]),

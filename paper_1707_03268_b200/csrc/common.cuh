@@ -92,21 +92,27 @@ __device__ __forceinline__ int find_job(const Job* jobs, int njobs, int64_t b) {
 
 // The same as a 32-ary search by a whole warp (every lane calls it with the
 // same b): each round one load per lane and a ballot narrow the range 32-fold,
-// so a 15k-job table costs three dependent loads instead of fourteen.
-template <typename Job>
-__device__ __forceinline__ int find_job_warp(const Job* jobs, int njobs, int64_t b) {
+// so a 15k-job table costs three dependent loads instead of fourteen.  `key`
+// picks the start field (block0 by default); zero-size jobs share their
+// successor's start and are skipped (the owner is the LAST job starting <= b).
+template <typename Job, typename Key>
+__device__ __forceinline__ int find_job_warp(const Job* jobs, int njobs, int64_t b, Key key) {
   const int lane = threadIdx.x & 31;
-  int lo = 0, n = njobs;  // jobs[lo].block0 <= b; the owner lies in [lo, lo + n)
+  int lo = 0, n = njobs;  // key(jobs[lo]) <= b; the owner lies in [lo, lo + n)
   while (n > 1) {
     const int step = (n + 31) >> 5;
     const int idx = lo + lane * step;
-    const bool le = idx < lo + n && jobs[idx].block0 <= b;
+    const bool le = idx < lo + n && key(jobs[idx]) <= b;
     const unsigned m = __ballot_sync(0xffffffffu, le);  // lane 0 is always set
     const int k = 31 - __clz(m);
     lo += k * step;
     n = min(step, n - k * step);
   }
   return lo;
+}
+template <typename Job>
+__device__ __forceinline__ int find_job_warp(const Job* jobs, int njobs, int64_t b) {
+  return find_job_warp(jobs, njobs, b, [](const Job& j) { return j.block0; });
 }
 
 }  // namespace dpm

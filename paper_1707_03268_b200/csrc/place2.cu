@@ -58,6 +58,7 @@
 // buffers also fit three CTAs per SM (75.5 KB) and measured the same 7.28 ms.
 // DPM_K3_THREADS / _TH / _XBUF / _MINB rebuild the others.
 #include <math.h>
+#include <stdlib.h>
 
 #include "place_common.cuh"
 
@@ -575,21 +576,65 @@ __device__ __forceinline__ void build_tab(PartTab& tb, const dpm_place_job& pj, 
   }
 }
 
+// Bias, totals and tau compaction of a tile's roots (part positions read back
+// from `pos`); root k of the thread at (iyr, ixr) when live.
+__device__ __forceinline__ void emit_root(const dpm_asm_job& aj, bool live, int iy, int ix, int wr,
+                                          double t0, double* __restrict__ total,
+                                          const uint32_t* __restrict__ pos, double tau,
+                                          dpm_detection* __restrict__ dets, int max_dets,
+                                          int* __restrict__ det_count, int lane, int hr) {
+  const double t = __dadd_rn(t0, aj.bias);
+  if (live && aj.total_off >= 0) total[aj.total_off + (int64_t)iy * wr + ix] = t;
+  if (dets == nullptr) return;
+  const bool hit = live && t >= tau;
+  const unsigned bal = __ballot_sync(0xffffffffu, hit);
+  if (bal == 0u) return;
+  const int leader = __ffs(bal) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(det_count, __popc(bal));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!hit) return;
+  const int slot = base + __popc(bal & ((1u << lane) - 1u));
+  if (slot >= max_dets) return;
+  dpm_detection d;
+  d.image = aj.image;
+  d.level = aj.level;
+  d.component = aj.component;
+  d.ry = aj.ry0 + iy;
+  d.rx = aj.rx0 + ix;
+  d.nparts = aj.nparts;
+  d.score = t;
+  for (int q = 0; q < DPM_MAX_PARTS; ++q)
+    d.parts[q] = (q < aj.nparts && aj.pos_off >= 0)
+                     ? pos[aj.pos_off + ((int64_t)q * hr + iy) * wr + ix]
+                     : 0u;
+  dets[slot] = d;
+}
+
 __global__ void __launch_bounds__(THREADS, DPM_K3_MINB)
 place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ smaps,
               const dpm_place_job* __restrict__ pjobs, const dpm_asm_job* __restrict__ ajobs,
               int najobs, const dpm_place_range* __restrict__ prep, double* __restrict__ total,
               uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
-              dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
+              dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count,
+              int fast_on) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem& sh = *reinterpret_cast<Smem*>(smem_raw);
-  const int jid = find_job_warp(ajobs, najobs, blockIdx.x);
+  const int jid = find_job_warp(ajobs, najobs, blockIdx.x,
+                                [](const dpm_asm_job& j) { return j.block1; });
   int tid_, lane_, warp_;
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_));
   asm volatile("and.b32 %0, %1, 31;" : "=r"(lane_) : "r"(tid_));
   asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp_) : "r"(tid_));
   const int tid = tid_, lane = lane_, warp = __shfl_sync(0xffffffffu, warp_, 0);
   const uint32_t band_bar = pl_smem(&sh.band_bar);
+  if (warp == 0) {  // this CTA's tile among the job's generic ones (block1 numbering)
+    const dpm_asm_job& g = ajobs[jid];
+    const int w = g.rx1 - g.rx0 + 1, nt = (w + PT_W - 1) / PT_W;
+    const int fc = fast_on ? k3_fast_cols_warp(g, pjobs, w, lane) : 0;
+    const int t = (int)blockIdx.x - g.block1;
+    if (lane == 0) sh.rmask[0][0] = fc > 0 ? (t << 16) | (nt - 1) : ((t / nt) << 16) | (t % nt);
+  }
   if (tid == 0) {
     sh.aj = ajobs[jid];
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(band_bar));
@@ -599,9 +644,7 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
   __syncthreads();
   const dpm_asm_job& aj = sh.aj;
   const int hr = aj.ry1 - aj.ry0 + 1, wr = aj.rx1 - aj.rx0 + 1;
-  const int ntx = (wr + PT_W - 1) / PT_W;
-  const int tile = blockIdx.x - aj.block0;
-  const int ty0 = (tile / ntx) * TH, tx0 = (tile % ntx) * PT_W;
+  const int ty0 = (int)(sh.rmask[0][0] >> 16) * TH, tx0 = (int)(sh.rmask[0][0] & 0xffffu) * PT_W;
   const int wt = min(PT_W, wr - tx0), h_tile = min(TH, hr - ty0);
   const int lpr_log = wt > 16 ? 5 : wt > 8 ? 4 : wt > 4 ? 3 : wt > 2 ? 2 : wt > 1 ? 1 : 0;
   const int lpr = 1 << lpr_log;
@@ -839,22 +882,454 @@ place2_kernel(const float* __restrict__ S, const unsigned char* __restrict__ sma
   }
 }
 
+// Specialised kernel for the bulk tiles (fast_tile): scale 2, both radii in
+// (R1MAX, RCAP], full-width tiles (lane = root column, one band row per warp
+// iteration).  Same algorithm, bounds and results as place2_kernel -- the
+// generic kernel's instantiation <R1MAX, PACKED, OUTER, FULLW> of the x pass
+// and <R1MAX, OUTER> of the y pass -- with the per-part geometry computed
+// once per CTA by warp 0 (PartHdr) instead of by every warp, per-thread root
+// offsets advanced by compile-time strides, and no radius / scale / lane
+// packing dispatch, so the part loop carries far fewer live values.
+struct PartHdr {
+  const float* sm;    // S + s_off of the part's map
+  int r_lo, r_hi;     // band rows inside the map: [r_lo, r_hi)
+  int n_out;          // band rows outside the map
+  int c0;             // shared column of lane 0's dx = 0
+  int d0, ds;         // packed screen: first pair's dx, the single candidate's dx
+  int reach;          // band columns the tile's windows reach
+  int rx, ry;
+  int pitch, Wp;
+  int cyb, cxb;       // window centre of root (ty0, tx0) in map rows / columns
+  int soff0;          // its S offset, cyb * pitch + cxb
+  int xb0, yb0, nbox; // TMA band boxes: first column (16-byte aligned), row, count
+  int map, map_z;     // TMA descriptor index, map index in its group
+  int ok;             // both radii in (R1MAX, RCAP]: staged two-phase path
+};
+
+// A part of a fast tile whose r* falls outside (R1MAX, RCAP]: every root of
+// the thread by direct global loads (exact, the reference's order).  Out of
+// line so the hot loop's register allocation does not carry it.
+__device__ __noinline__ void fast_unstaged(const dpm_place_job& pj, const PartHdr& h,
+                                           double* tot, int warp, int lane, int h_tile, int o0,
+                                           int wr, uint32_t* posb, double* placedb) {
+  for (int k = 0; k < RPT; ++k) {
+    const int iyr = warp + WARPS * k;
+    if (iyr >= h_tile) continue;
+    const int cy = h.cyb + 2 * iyr, cx = h.cxb + 2 * lane;
+    double best;
+    int bdy, bdx;
+    place_unstaged(h.sm, pj, cy, cx, h.rx, h.ry, best, bdy, bdx);
+    tot[k * THREADS] = __dadd_rn(tot[k * THREADS], best);
+    const int o = o0 + WARPS * k * wr;
+    if (posb) posb[o] = pack_pos(cy + bdy, cx + bdx);
+    if (placedb) placedb[o] = best;
+  }
+}
+
+// y-pass roots of a fast tile that need an exact scan (near tie, failed
+// outer bound, or an x row resolved exactly), resolved after the hot loop and
+// out of line, in the reference's order, exactly as the generic kernel's
+// y_group phase 2 does (state and screening threshold of each root passed in).
+static_assert(RPT == 4, "fast_rare_roots takes four roots");
+__device__ __noinline__ void fast_rare_roots(uint32_t rare, int st0, int st1, int st2, int st3,
+                                             float sv0, float sv1, float sv2, float sv3,
+                                             const float* x32, const PartHdr& h,
+                                             const PartTab& tb, double* tot, int warp, int lane,
+                                             int o0, int wr, uint32_t* posb, double* placedb,
+                                             uint32_t mask) {
+  const int ry = h.ry, rx = h.rx, pitch = h.pitch;
+  XDec xd;
+  xd.d0 = h.d0;
+  xd.ds = h.ds;
+  xd.c2r1 = 2 * R1MAX;
+  while (rare) {
+    const int k = __ffs(rare) - 1;
+    rare &= rare - 1;
+    const int st = k == 0 ? st0 : k == 1 ? st1 : k == 2 ? st2 : st3;
+    const float thr = k == 0 ? sv0 : k == 1 ? sv1 : k == 2 ? sv2 : sv3;
+    int state = st & 7;
+    int dy = ((st >> 3) & 127) - 64, dx = ((st >> 10) & 127) - 64;
+    const int iyr = warp + WARPS * k;
+    const int cy = h.cyb + 2 * iyr, cx = h.cxb + 2 * lane;
+    const int so = cy * pitch + cx;
+    if (state == 5) {
+      dx = x_exact_global(h.sm + so + dy * pitch, cx, h.Wp, rx, tb.px);
+    } else {
+      const float* xcol = x32 + (2 * iyr + ry) * PT_W + lane;
+      const int q = y_exact(xcol, h.sm, pitch, cy, cx, state == 2 ? -R1MAX : -ry,
+                            state == 2 ? R1MAX : ry, h.Wp, &tb, xd, rx,
+                            state == 2 ? thr : -INFINITY, mask, R1MAX,
+                            state == 2 ? dy : 1000, state == 2 ? dx : 1000);
+      if (q < 0) {
+        state = 4;
+      } else {
+        dy = (q & 255) - 64;
+        dx = (q >> 8) - 64;
+      }
+    }
+    double best = -INFINITY;
+    if (state == 4) {
+      dy = -ry;
+      dx = -rx;
+    } else {
+      const float s = __ldg(h.sm + so + dy * pitch + dx);
+      best = __dadd_rn(__dadd_rn((double)s, -tb.px[dx + 16]), -tb.py[dy + 16]);
+    }
+    tot[k * THREADS] = __dadd_rn(tot[k * THREADS], best);
+    const int o = o0 + WARPS * k * wr;
+    if (posb) posb[o] = pack_pos(cy + dy, cx + dx);
+    if (placedb) placedb[o] = best;
+  }
+}
+
+struct __align__(128) SmemF {
+  float s[BAND2 * COLS_PITCH];
+  float x32[XBUF][BAND2 * PT_W];
+  double tot[RPT][THREADS];
+  uint32_t cmk[3][PT_W];           // column maxima (float_key), part q at q % 3
+  uint32_t rmask[WARPS][RMASK];
+  PartTab tab[3];
+  PartHdr hdr[3];
+  alignas(16) JobRange jr[3];
+  alignas(16) dpm_place_job pj[3];
+  dpm_asm_job aj;
+  alignas(8) uint64_t band_bar;
+  int tile;  // (tile row << 16) | tile column
+};
+
+__device__ __forceinline__ void fast_tile_run(
+    const float* __restrict__ S, const unsigned char* __restrict__ smaps,
+    const dpm_place_job* __restrict__ pjobs, const dpm_asm_job* __restrict__ ajobs, int najobs,
+    const dpm_place_range* __restrict__ prep, double* __restrict__ total,
+    uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
+    dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count, int jid) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  SmemF& sh = *reinterpret_cast<SmemF*>(smem_raw);
+  int tid_, lane_, warp_;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid_));
+  asm volatile("and.b32 %0, %1, 31;" : "=r"(lane_) : "r"(tid_));
+  asm volatile("shr.u32 %0, %1, 5;" : "=r"(warp_) : "r"(tid_));
+  const int tid = tid_, lane = lane_, warp = __shfl_sync(0xffffffffu, warp_, 0);
+  const uint32_t band_bar = pl_smem(&sh.band_bar);
+  if (warp == 0) {  // this CTA's tile among the job's fast ones (block0 numbering)
+    const dpm_asm_job& g = ajobs[jid];
+    const int fc = k3_fast_cols_warp(g, pjobs, g.rx1 - g.rx0 + 1, lane);
+    const int t = (int)blockIdx.x - g.block0;
+    if (lane == 0) sh.tile = ((t / fc) << 16) | (t % fc);
+  }
+  if (tid == 0) {
+    sh.aj = ajobs[jid];
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(band_bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 3 * PT_W) (&sh.cmk[0][0])[tid] = 0u;
+  __syncthreads();
+  const dpm_asm_job& aj = sh.aj;
+  const int hr = aj.ry1 - aj.ry0 + 1, wr = aj.rx1 - aj.rx0 + 1;
+  const int ty0 = (sh.tile >> 16) * TH, tx0 = (sh.tile & 0xffff) * PT_W;
+  const int wt = min(PT_W, wr - tx0), h_tile = min(TH, hr - ty0);
+  const int ry_lo = aj.ry0 + ty0, ry_hi = ry_lo + h_tile - 1, rx_lo = aj.rx0 + tx0;
+  const bool lane_live = lane < wt;
+  const uint32_t mask = ~15u | ((uint32_t)najobs >> 31);  // see place2_kernel
+
+  // root k of this thread: row warp + WARPS k, column lane
+  double* const tot = &sh.tot[0][tid];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int iyr = warp + WARPS * k;
+    double t = 0.0;
+    if (aj.root_off >= 0 && lane_live && iyr < h_tile)
+      t = (double)__ldg(S + aj.root_off + (int64_t)(ry_lo + iyr) * aj.root_pitch + rx_lo + lane);
+    tot[k * THREADS] = t;
+  }
+
+  auto fetch_job = [&](int q) {  // warp 0
+    const int slot = q % 3;
+    if (lane < (int)(sizeof(dpm_place_job) / 8)) {
+      const uint32_t sa = pl_smem(reinterpret_cast<unsigned char*>(&sh.pj[slot]) + 8 * lane);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                   "l"(reinterpret_cast<const unsigned char*>(pjobs + aj.part_job0 + q) + 8 * lane));
+    } else if (lane == 31) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(pl_smem(&sh.jr[slot])),
+                   "l"(prep + aj.part_job0 + q));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto finish_job = [&](int q) {  // warp 0: tables and the part's geometry
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncwarp();
+    const int slot = q % 3;
+    const dpm_place_job& pj = sh.pj[slot];
+    const JobRange& jr = sh.jr[slot];
+    build_tab(sh.tab[slot], pj, jr, lane);
+    if (lane == 0) {
+      PartHdr& h = sh.hdr[slot];
+      const int yb0 = 2 * ry_lo + pj.ay - jr.ry;
+      const int nrows = 2 * (ry_hi - ry_lo) + 1 + 2 * jr.ry;
+      const int xb0 = 2 * rx_lo + pj.ax - jr.rx;
+      h.sm = S + pj.s_off;
+      h.r_lo = min(max(0, -yb0), nrows);
+      h.r_hi = max(min(nrows, pj.Hp - yb0), h.r_lo);
+      h.n_out = h.r_lo + (nrows - h.r_hi);
+      h.c0 = (xb0 & 3) + jr.rx;
+      const int s = h.c0 & 1;  // packed pairs start on an even shared column
+      h.d0 = -R1MAX + s;
+      h.ds = s ? -R1MAX : R1MAX;
+      h.reach = 2 * (wt - 1) + 1 + 2 * jr.rx;
+      h.rx = jr.rx;
+      h.ry = jr.ry;
+      h.pitch = s_pitch(pj.Wp);
+      h.Wp = pj.Wp;
+      h.cyb = 2 * ry_lo + pj.ay;
+      h.cxb = 2 * rx_lo + pj.ax;
+      h.soff0 = h.cyb * h.pitch + h.cxb;
+      h.xb0 = xb0 & ~3;
+      h.yb0 = yb0;
+      h.nbox = (nrows + TMA_BH - 1) / TMA_BH;
+      h.map = pj.smap;
+      h.map_z = pj.smap_z;
+      h.ok = jr.rx > R1MAX && jr.rx <= RCAP && jr.ry > R1MAX && jr.ry <= RCAP;
+    }
+  };
+  auto issue_band = [&](int q) {  // thread 0; the buffer's last readers passed a barrier
+    const PartHdr& h = sh.hdr[q % 3];
+    if (tid != 0 || !h.ok) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(band_bar),
+                 "r"((uint32_t)h.nbox * TMA_BOX_BYTES)
+                 : "memory");
+    const void* map = smaps + (int64_t)h.map * DPM_SMAP_BYTES;
+    const uint32_t dst = pl_smem(sh.s);
+    for (int k = 0; k < h.nbox; ++k)
+      tma_band_box(dst + (uint32_t)k * TMA_BOX_BYTES, map, h.xb0, h.yb0 + k * TMA_BH, h.map_z,
+                   band_bar);
+  };
+
+  uint32_t bands = 0;
+  if (warp == 0) {
+    fetch_job(0);
+    finish_job(0);
+  }
+  __syncthreads();
+  issue_band(0);
+  uint32_t* const posb = aj.pos_off >= 0 ? pos + aj.pos_off : nullptr;
+  double* const placedb = aj.placed_off >= 0 ? placed + aj.placed_off : nullptr;
+  const int obase = (ty0 + warp) * wr + tx0 + lane;  // output offset of root 0 in part 0
+  const float sent = enc_code(OUT_SENTINEL, CODE_NONE);
+  for (int p = 0; p < aj.nparts; ++p) {
+    const int slot = p % 3, buf = XBUF == 2 ? p & 1 : 0;
+    if (XBUF == 1 && p > 0) __syncthreads();  // y(p-1) done with the single x-word buffer
+    if (warp == 0) sh.cmk[(p + 1) % 3][lane] = 0u;  // slot of part p+1 (see place2_kernel)
+    const PartTab& tb = sh.tab[slot];
+    const PartHdr& h = sh.hdr[slot];
+    const bool have_next = p + 1 < aj.nparts;
+    if (warp == 0 && have_next) fetch_job(p + 1);
+    float* x32 = sh.x32[buf];
+    const bool staged = h.ok;
+    float cmaxv = -INFINITY;
+    if (staged) pl_mbar_wait(band_bar, bands++ & 1);
+    if (staged && h.n_out > 0) {  // rows outside the map: no candidate (reference: (-inf, -r))
+      const int r_lo = h.r_lo, r_hi = h.r_hi, n_out = h.n_out;
+      for (int i = tid; i < n_out * PT_W; i += THREADS) {
+        const int k = i >> 5, l = i & 31;
+        x32[(k < r_lo ? k : r_hi + (k - r_lo)) * PT_W + l] = sent;
+      }
+      cmaxv = sent;
+    }
+    // ---- x pass: band rows r_lo + warp, + WARPS, ...; lane = centre column
+    if (staged) {
+      const float E2 = tb.E2x, outx = tb.out_x, e2o = tb.E2o;
+      unsigned long long pp[R1MAX];
+      const float* tp = ((h.d0 + 16) & 1) ? tb.npx1 + h.d0 + 17 : tb.npx + h.d0 + 16;
+#pragma unroll
+      for (int k = 0; k < R1MAX; ++k) pp[k] = *reinterpret_cast<const unsigned long long*>(tp + 2 * k);
+      const float pr0 = tb.npx[h.ds + 16];
+      const int r_hi = h.r_hi, d0 = h.d0, ds = h.ds;
+      const float* s0row = sh.s + h.c0 + 2 * lane;         // dx = 0 of lane's centre, row 0
+      const float* mrow = sh.s + (h.c0 - h.rx) + lane;     // band column 0 + lane
+      const bool b1 = lane + 32 < h.reach, b2 = lane + 64 < h.reach;
+      uint32_t iters = 0;
+      int it = 0;
+      const int rb0 = h.r_lo + warp;
+      for (int r = rb0; r < r_hi; r += WARPS, ++it) {
+        const float* s0 = s0row + r * COLS_PITCH;
+        float m1, m2;
+        scr_packed<R1MAX>(s0 + d0, pp, s0[ds] + pr0, mask, m1, m2);
+        const float* mr_ = mrow + r * COLS_PITCH;
+        const float l = fmaxf(mr_[0], fmaxf(b1 ? mr_[32] : -INFINITY, b2 ? mr_[64] : -INFINITY));
+        float mr;
+        asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mr) : "f"(l));
+        const bool rare =
+            lane_live && (mr + outx + e2o >= m1 - E2 || m1 < NONE_BELOW || m2 >= m1 - E2);
+        const uint32_t bal = __ballot_sync(0xffffffffu, rare);
+        if (bal != 0u) {
+          iters |= 1u << it;
+          if (lane == 0) sh.rmask[warp][it] = bal;  // it < RMASK
+        }
+        if (lane_live) {
+          x32[r * PT_W + lane] = m1;
+          cmaxv = fmaxf(cmaxv, m1);
+        }
+      }
+      if (iters != 0u) {
+        __syncwarp();
+        while (iters != 0u) {
+          const int i = __ffs(iters) - 1;
+          iters &= iters - 1;
+          if (!((sh.rmask[warp][i] >> lane) & 1u)) continue;
+          const int r = rb0 + i * WARPS;
+          const float* s0 = s0row + r * COLS_PITCH;
+          const int xi = x_exact_band(s0, -h.rx, h.rx, tb.px);
+          const float v = s0[xi];
+          const float word = v == v ? enc_code(v + tb.npx[xi + 16], CODE_RARE)
+                                    : enc_code(OUT_SENTINEL, CODE_NONE);
+          x32[r * PT_W + lane] = word;
+          cmaxv = fmaxf(cmaxv, word);
+        }
+      }
+    }
+    if (staged) atomicMax(&sh.cmk[slot][lane], float_key(cmaxv));
+    if (warp == 0 && have_next) finish_job(p + 1);
+    __syncthreads();  // x(p) done: x words visible, band buffer free, part p+1 ready
+    if (have_next) issue_band(p + 1);
+    if (!staged) {  // r* outside (R1MAX, RCAP]: the exact per-root path (rare)
+      if (lane_live)
+        fast_unstaged(sh.pj[slot], h, tot, warp, lane, h_tile, p * hr * wr + obase, wr, posb,
+                      placedb);
+      continue;
+    }
+    // ---- y pass: roots (warp + WARPS k, lane)
+    {
+      const float cmax = key_float(sh.cmk[slot][lane]);
+      const float E2 = tb.E2y, bound = cmax + tb.out_y + tb.E2o;
+      float pr[2 * R1MAX + 1];
+#pragma unroll
+      for (int d = -R1MAX; d <= R1MAX; ++d) pr[d + R1MAX] = tb.npy[d + 16];
+      const int ry = h.ry, rx = h.rx, pitch = h.pitch, d0 = h.d0, ds = h.ds;
+      const float* smap = h.sm;
+      const float* xcol0 = x32 + (2 * warp + ry) * PT_W + lane;
+      const int soff0 = h.soff0 + 2 * warp * pitch + 2 * lane;
+      int st[RPT];
+      float sv[RPT];
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        st[k] = 0;
+        sv[k] = 0.f;
+        if (!lane_live || warp + WARPS * k >= h_tile) continue;
+        const float* xcol = xcol0 + 2 * WARPS * k * PT_W;
+        float m1, m2;
+        scr_strided<R1MAX, PT_W>(xcol, pr, mask, m1, m2);
+        const float lo = m1 - E2;
+        if (bound >= lo) {
+          st[k] = 3;
+        } else if (m1 < NONE_BELOW) {
+          st[k] = 4;
+        } else if (m2 >= lo) {
+          st[k] = 2 | ((code_of(m1) - R1MAX + 64) << 3) | ((code_of(m2) - R1MAX + 64) << 10);
+          sv[k] = lo;
+        } else {
+          const int dy = code_of(m1) - R1MAX;
+          const int c = code_of(xcol[dy * PT_W]);
+          if (c == CODE_RARE) {
+            st[k] = 5 | ((dy + 64) << 3);
+          } else {
+            const int dx = c == 2 * R1MAX ? ds : d0 + c;
+            st[k] = 1 | ((dy + 64) << 3) | ((dx + 64) << 10);
+            sv[k] = __ldg(smap + soff0 + 2 * WARPS * k * pitch + dy * pitch + dx);
+          }
+        }
+      }
+      const int o0 = p * hr * wr + obase;
+      uint32_t rare = 0;  // roots whose winner needs an exact scan (~1%), after the loop
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        const int state = st[k] & 7;
+        if (state == 0) continue;
+        if (state != 1 && state != 4) {
+          rare |= 1u << k;
+          continue;
+        }
+        int dy = ((st[k] >> 3) & 127) - 64, dx = ((st[k] >> 10) & 127) - 64;
+        double best = -INFINITY;
+        if (state == 4) {  // no candidate: the reference's (-inf, first dy, first row's dx)
+          dy = -ry;
+          dx = -rx;
+        } else {
+          best = __dadd_rn(__dadd_rn((double)sv[k], -tb.px[dx + 16]), -tb.py[dy + 16]);
+        }
+        tot[k * THREADS] = __dadd_rn(tot[k * THREADS], best);
+        const int o = o0 + WARPS * k * wr;
+        if (posb) posb[o] = pack_pos(h.cyb + 2 * (warp + WARPS * k) + dy, h.cxb + 2 * lane + dx);
+        if (placedb) placedb[o] = best;
+      }
+      if (rare)
+        fast_rare_roots(rare, st[0], st[1], st[2], st[3], sv[0], sv[1], sv[2], sv[3], x32, h, tb,
+                        tot, warp, lane, o0, wr, posb, placedb, mask);
+    }
+  }
+
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int iyr = warp + WARPS * k;
+    emit_root(aj, lane_live && iyr < h_tile, ty0 + iyr, tx0 + lane, wr, tot[k * THREADS], total,
+              pos, tau, dets, max_dets, det_count, lane, hr);
+  }
+}
+
+
+// The specialised path and the generic one as two kernels over disjoint tile
+// lists (block0 / block1 numbering of dpm_assemble_prepare); one kernel
+// calling both paths allocates registers for their union and spills ~2 KB.
+__global__ void __launch_bounds__(THREADS, DPM_K3_MINB)
+place2f_kernel(const float* __restrict__ S, const unsigned char* __restrict__ smaps,
+               const dpm_place_job* __restrict__ pjobs, const dpm_asm_job* __restrict__ ajobs,
+               int najobs, const dpm_place_range* __restrict__ prep, double* __restrict__ total,
+               uint32_t* __restrict__ pos, double* __restrict__ placed, double tau,
+               dpm_detection* __restrict__ dets, int max_dets, int* __restrict__ det_count) {
+  const int jid = find_job_warp(ajobs, najobs, blockIdx.x);
+  fast_tile_run(S, smaps, pjobs, ajobs, najobs, prep, total, pos, placed, tau, dets, max_dets,
+                det_count, jid);
+}
+
 }  // namespace k3v2
 
 int k3v2_tile_rows() { return k3v2::TH; }
 
 // launched by dpm_assemble (placement.cu)
+// DPM_K3F=0 keeps every tile on the generic kernel (A/B of the specialised
+// one); read by dpm_assemble_prepare's tile numbering and by the launch
+bool k3_fast_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DPM_K3F");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+// launched by dpm_assemble (placement.cu): the specialised kernel over its
+// nfast tiles, the generic kernel over the other ngeneric
 int launch_place2(const float* S, const void* smaps, const dpm_place_job* pjobs,
-                  const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
+                  const dpm_asm_job* ajobs, int najobs, int64_t nfast, int64_t ngeneric,
                   const dpm_place_range* prep, double* total, uint32_t* pos, double* placed,
                   double tau, dpm_detection* dets, int max_dets, int* det_count, cudaStream_t st) {
-  const size_t smem = sizeof(k3v2::Smem);
-  DPM_CUDA(cudaFuncSetAttribute(k3v2::place2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
-  k3v2::place2_kernel<<<(unsigned)nblocks, k3v2::THREADS, smem, st>>>(
-      S, static_cast<const unsigned char*>(smaps), pjobs, ajobs, najobs, prep, total, pos, placed,
-      tau, dets, max_dets, det_count);
-  DPM_LAUNCHED("place2_kernel");
+  const unsigned char* sm = static_cast<const unsigned char*>(smaps);
+  if (nfast > 0) {
+    const size_t smf = sizeof(k3v2::SmemF);
+    DPM_CUDA(cudaFuncSetAttribute(k3v2::place2f_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf));
+    k3v2::place2f_kernel<<<(unsigned)nfast, k3v2::THREADS, smf, st>>>(
+        S, sm, pjobs, ajobs, najobs, prep, total, pos, placed, tau, dets, max_dets, det_count);
+    DPM_LAUNCHED("place2f_kernel");
+  }
+  if (ngeneric > 0) {
+    const size_t smem = sizeof(k3v2::Smem);
+    DPM_CUDA(cudaFuncSetAttribute(k3v2::place2_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k3v2::place2_kernel<<<(unsigned)ngeneric, k3v2::THREADS, smem, st>>>(
+        S, sm, pjobs, ajobs, najobs, prep, total, pos, placed, tau, dets, max_dets, det_count,
+        k3_fast_enabled() ? 1 : 0);
+    DPM_LAUNCHED("place2_kernel");
+  }
   return DPM_OK;
 }
 

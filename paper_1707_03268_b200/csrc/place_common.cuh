@@ -141,10 +141,39 @@ __device__ __forceinline__ void pl_mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 
-// the two-phase K3/K4 kernel (place2.cu) and its tile height in root rows
+// Tiles of the specialised K3 kernel (place2.cu): the leading tile columns
+// at least FAST_MINW roots wide of a job whose parts are all at scale 2 with
+// radius < 0 (r* from the device's map ranges; a part whose r* falls outside
+// (6, RCAP] takes the kernel's exact per-root path) or 7 <= radius <= RCAP.
+// Host (dpm_assemble_prepare) and device (tile numbering) evaluate the same
+// rule.  Returns the number of such tile columns.
+constexpr int FAST_MINW = 17;
+constexpr int FAST_R1 = 6;  // inner screen radius of the two-phase kernel
+__host__ __device__ inline bool k3_fast_part(const dpm_place_job& pj) {
+  return pj.scale == 2 && (pj.radius < 0 || (pj.radius > FAST_R1 && pj.radius <= RCAP));
+}
+bool k3_fast_enabled();  // DPM_K3F=0 turns the specialised kernel off (place2.cu)
+__host__ inline int k3_fast_cols(const dpm_asm_job& j, const dpm_place_job* pjobs, int wr) {
+  if (j.nparts <= 0 || !k3_fast_enabled()) return 0;
+  for (int q = 0; q < j.nparts; ++q)
+    if (!k3_fast_part(pjobs[j.part_job0 + q])) return 0;
+  const int ntx = (wr + PT_W - 1) / PT_W;
+  return wr - PT_W * (ntx - 1) >= FAST_MINW ? ntx : ntx - 1;
+}
+// the same on the device, by a whole warp (lane q tests part q)
+__device__ __forceinline__ int k3_fast_cols_warp(const dpm_asm_job& j, const dpm_place_job* pjobs,
+                                                 int wr, int lane) {
+  if (j.nparts <= 0) return 0;
+  const bool ok = lane >= j.nparts || k3_fast_part(pjobs[j.part_job0 + lane]);
+  if (!__all_sync(0xffffffffu, ok)) return 0;
+  const int ntx = (wr + PT_W - 1) / PT_W;
+  return wr - PT_W * (ntx - 1) >= FAST_MINW ? ntx : ntx - 1;
+}
+
+// the two-phase K3/K4 kernels (place2.cu) and their tile height in root rows
 int k3v2_tile_rows();
 int launch_place2(const float* S, const void* smaps, const dpm_place_job* pjobs,
-                  const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
+                  const dpm_asm_job* ajobs, int najobs, int64_t nfast, int64_t ngeneric,
                   const dpm_place_range* prep, double* total, uint32_t* pos, double* placed,
                   double tau, dpm_detection* dets, int max_dets, int* det_count, cudaStream_t st);
 

@@ -577,12 +577,11 @@ static bool k3_use_v1() {
 }
 
 extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_place_job* pjobs,
-                                        int npjobs) {
+                                        int npjobs, int64_t* nfast) {
   if (njobs < 0 || (njobs > 0 && !jobs) || npjobs < 0 || (npjobs > 0 && !pjobs)) {
     set_error("dpm_assemble_prepare: bad job tables");
     return DPM_ERR_ARG;
   }
-  int64_t b = 0;
   for (int i = 0; i < njobs; ++i) {
     const dpm_asm_job& j = jobs[i];
     if (j.ry1 < j.ry0 || j.rx1 < j.rx0 || j.nparts < 0 || j.nparts > DPM_MAX_PARTS ||
@@ -599,21 +598,39 @@ extern "C" int64_t dpm_assemble_prepare(dpm_asm_job* jobs, int njobs, const dpm_
         return DPM_ERR_ARG;
       }
     }
-    jobs[i].block0 = (int32_t)b;
     const int64_t hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
     if ((int64_t)(j.nparts > 0 ? j.nparts : 1) * hr * wr > INT32_MAX) {  // 32-bit output offsets
       set_error("dpm_assemble_prepare: job %d: %d parts x %lld x %lld roots exceed 2^31 outputs", i,
                 j.nparts, (long long)hr, (long long)wr);
       return DPM_ERR_ARG;
     }
-    const int th = k3_use_v1() ? PT_H : k3v2_tile_rows();
-    b += ((hr + th - 1) / th) * ((wr + PT_W - 1) / PT_W);
   }
-  if (b > INT32_MAX) {
+  // tiles: the specialised kernel's (leading tile columns of eligible jobs)
+  // numbered by block0 over [0, nf), the generic kernel's by block1 over
+  // [0, ng); the round-1 kernel (DPM_K3=v1) numbers every tile by block0
+  const bool v1 = k3_use_v1();
+  const int th = v1 ? PT_H : k3v2_tile_rows();
+  int64_t nf = 0, ng = 0;
+  for (int i = 0; i < njobs; ++i) {
+    const dpm_asm_job& j = jobs[i];
+    const int hr = j.ry1 - j.ry0 + 1, wr = j.rx1 - j.rx0 + 1;
+    const int64_t nty = (hr + th - 1) / th, ntx = (wr + PT_W - 1) / PT_W;
+    const int fc = v1 ? 0 : k3_fast_cols(j, pjobs, wr);
+    jobs[i].block0 = (int32_t)(v1 ? ng : nf);
+    jobs[i].block1 = (int32_t)ng;
+    if (v1) {
+      ng += nty * ntx;
+    } else {
+      nf += nty * fc;
+      ng += nty * (ntx - fc);
+    }
+  }
+  if (nf + ng > INT32_MAX) {
     set_error("dpm_assemble_prepare: too many CTAs");
     return DPM_ERR_ARG;
   }
-  return b;
+  if (nfast) *nfast = nf;
+  return nf + ng;
 }
 
 extern "C" int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uint32_t* ranges,
@@ -628,7 +645,7 @@ extern "C" int dpm_place_ranges(const dpm_place_job* pjobs, int njobs, const uin
 }
 
 extern "C" int dpm_assemble(const float* S, const void* smaps, const dpm_place_job* pjobs,
-                            const dpm_asm_job* ajobs, int najobs, int64_t nblocks,
+                            const dpm_asm_job* ajobs, int najobs, int64_t nfast, int64_t nblocks,
                             const dpm_place_range* prep, double* total, uint32_t* pos,
                             double* placed, double tau, dpm_detection* dets, int max_dets,
                             int* det_count, void* stream) {
@@ -636,11 +653,13 @@ extern "C" int dpm_assemble(const float* S, const void* smaps, const dpm_place_j
   DPM_REQUIRE((reinterpret_cast<uintptr_t>(smaps) & 63) == 0,
               "dpm_assemble: tensor maps must be 64-byte aligned");
   DPM_REQUIRE(!dets || (det_count && pos), "dpm_assemble: detections need a counter and positions");
-  DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX, "dpm_assemble: nblocks");
+  DPM_REQUIRE(nblocks >= 0 && nblocks <= INT32_MAX && nfast >= 0 && nfast <= nblocks,
+              "dpm_assemble: nfast / nblocks");
   if (najobs == 0 || nblocks == 0) return DPM_OK;
   if (!k3_use_v1())
-    return launch_place2(S, smaps, pjobs, ajobs, najobs, nblocks, prep, total, pos, placed, tau,
-                         dets, max_dets, det_count, as_stream(stream));
+    return launch_place2(S, smaps, pjobs, ajobs, najobs, nfast, nblocks - nfast, prep, total, pos,
+                         placed, tau, dets, max_dets, det_count, as_stream(stream));
+  DPM_REQUIRE(nfast == 0, "dpm_assemble: the round-1 kernel has no specialised tiles");
   const size_t smem = sizeof(PlaceSmem);
   DPM_CUDA(cudaFuncSetAttribute(place_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));

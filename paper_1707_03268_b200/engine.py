@@ -17,6 +17,8 @@ HBM layout (per image, images stacked):
 import os
 from dataclasses import dataclass, field
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -577,10 +579,11 @@ class Plan:
             tb["prefix"].append((h, len(sub), upload_table(sub, dev)))
         in_chunk = np.isin(self._asm_jobs["image"], list(imgs))
         aj = np.ascontiguousarray(self._asm_jobs[in_chunk & ~self._asm_gdt])
+        nfast = ctypes.c_int64(0)
         blocks = _lib.check(lib.dpm_assemble_prepare(
-            _lib.table_ptr(aj), len(aj), _lib.table_ptr(self._place_jobs), len(self._place_jobs)),
-            "assembly")
-        tb["asm"] = (upload_table(aj, dev), len(aj), blocks)
+            _lib.table_ptr(aj), len(aj), _lib.table_ptr(self._place_jobs), len(self._place_jobs),
+            ctypes.byref(nfast)), "assembly")
+        tb["asm"] = (upload_table(aj, dev), len(aj), (nfast.value, blocks))
         # lower-envelope GDT: x-pass table (the chunk's placement jobs) and the
         # y-pass/assembly table (indexing the full placement table)
         gj = np.ascontiguousarray(self._asm_jobs[in_chunk & self._asm_gdt])
@@ -690,9 +693,9 @@ class Plan:
             _lib.check(lib.dpm_place_ranges(ptr(self.place_jobs_d), len(self._place_jobs),
                                             ptr(self.ranges), ptr(self.prep), s), "place ranges")
             mark("k3k4_place_assemble")
-            aj_d, naj, nblk = tb["asm"]
+            aj_d, naj, (nfast, nblk) = tb["asm"]
             _lib.check(lib.dpm_assemble(
-                ptr(self.S), ptr(self.smaps), ptr(self.place_jobs_d), ptr(aj_d), naj, nblk,
+                ptr(self.S), ptr(self.smaps), ptr(self.place_jobs_d), ptr(aj_d), naj, nfast, nblk,
                 ptr(self.prep),
                 ptr(self.totals) if self.total_size else None,
                 ptr(self.positions) if self.pos_size else None,

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 11
     for n in names:
         assert hasattr(lib, n), n
-    assert lib.dpm_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.dpm_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_struct_sizes_match_header_comments():
@@ -95,16 +95,51 @@ def test_prepare_validates_and_numbers_blocks():
     aj = np.zeros(1, dtype=_lib.ASM_JOB)
     aj["ry1"], aj["rx1"], aj["nparts"] = 3, 3, 1
     with pytest.raises(Exception, match="x-pass columns"):
-        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1))
+        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1, None))
     aj["rx1"] = 4
-    assert lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1) == 1
+    assert lib.dpm_assemble_prepare(_lib.table_ptr(aj), 1, _lib.table_ptr(pj), 1, None) == 1
     # one job's outputs must fit 32-bit offsets (nparts x hr x wr < 2^31)
     big_pj = np.repeat(pj, 8)
     big_pj["wr"] = 50000
     big = aj.copy()
     big["ry1"], big["rx1"], big["nparts"] = 6000 - 1, 50000 - 1, 8
     with pytest.raises(Exception, match="exceed 2\\^31"):
-        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(big), 1, _lib.table_ptr(big_pj), 8))
+        _lib.check(lib.dpm_assemble_prepare(_lib.table_ptr(big), 1, _lib.table_ptr(big_pj), 8, None))
+
+
+def test_assemble_prepare_splits_tiles_between_the_two_k3_kernels():
+    """Tiles >= 17 roots wide of jobs whose parts are all at scale 2 with an
+    unbounded (or 7..16) radius go to the specialised kernel (block0
+    numbering), the others to the generic kernel (block1 numbering)."""
+    lib = _lib.lib()
+    pj = np.zeros(3, dtype=_lib.PLACE_JOB)
+    pj["Hp"], pj["Wp"], pj["range_idx"] = 500, 500, 0
+    pj["cdxx"], pj["cdyy"] = 0.01, 0.01
+    pj["scale"], pj["radius"] = 2, -1
+    pj["rx0"], pj["wr"] = 0, 40
+    pj["wr"][2] = 20
+    pj["scale"][1] = 1          # job 1: a scale-1 part -> generic only
+    aj = np.zeros(3, dtype=_lib.ASM_JOB)
+    aj["ry1"] = 99              # 100 root rows: r tile rows (r = ceil(100 / tile height))
+    aj["rx1"] = (39, 39, 19)    # 40 columns: a full column and an 8-wide one; 20: one fast column
+    aj["part_job0"], aj["nparts"] = (0, 1, 2), 1
+    # tile rows of a 100-row job, from a job that is generic whatever the kernel geometry
+    one = aj[1:2].copy()
+    one["rx1"], one["part_job0"] = 0, 0
+    pj1 = pj[1:2].copy()
+    pj1["wr"] = 1
+    r = lib.dpm_assemble_prepare(_lib.table_ptr(one), 1, _lib.table_ptr(pj1), 1, None)
+    assert r >= 2
+    nfast = ctypes.c_int64(-1)
+    total = lib.dpm_assemble_prepare(_lib.table_ptr(aj), 3, _lib.table_ptr(pj), 3,
+                                     ctypes.byref(nfast))
+    assert (nfast.value, total) == (r + 0 + r, 2 * r + 2 * r + r)
+    assert list(aj["block0"]) == [0, r, r]
+    assert list(aj["block1"]) == [0, r, 3 * r]
+    pj["radius"][0] = 5         # a fixed radius inside the inner screen -> generic
+    assert lib.dpm_assemble_prepare(_lib.table_ptr(aj), 3, _lib.table_ptr(pj), 3,
+                                    ctypes.byref(nfast)) == 5 * r
+    assert nfast.value == r and list(aj["block1"]) == [0, 2 * r, 4 * r]
 
 
 def test_tile_shapes():
