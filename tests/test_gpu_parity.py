@@ -319,7 +319,7 @@ def _shared(cfg, R):
     return fx["C"], fx["G"]
 
 
-def _pyramid_parity(cfg, R, sel_levels=None, comps=None, images=(0,), n_images=1):
+def _pyramid_parity(cfg, R, sel_levels=None, comps=None, images=(0,), n_images=1, feat_scale=1.0):
     wl = synth.workload(cfg)
     C, G = _shared(cfg, R)
     bank, pyr = wl.bank, wl.pyramid
@@ -327,7 +327,7 @@ def _pyramid_parity(cfg, R, sel_levels=None, comps=None, images=(0,), n_images=1
     sc = PyramidScorer(bank, C, G, pyr, n_images=n_images, components=comp_list)
     levels = {}
     for img in range(n_images):
-        lv = synth.hog_pyramid(cfg, img, pyr)
+        lv = [np.float32(feat_scale) * x for x in synth.hog_pyramid(cfg, img, pyr)]
         levels[img] = lv
         sc.load_image(img, lv)
     sc.run()
@@ -457,6 +457,18 @@ def test_config4_full_image_every_level_and_component():
     run on the GPU's own maps (ties <= 1e-4), and against the float64 oracle
     only at ties (zero errors)."""
     worst = _pyramid_parity(4, 8, sel_levels=None, images=(0,), n_images=1)
+    assert worst <= 1e-5
+
+
+@pytest.mark.parametrize("feat_scale", [8.0, 0.05])
+def test_config4_specialised_k3_radius_fallback(feat_scale):
+    """The specialised K3 kernel takes every wide scale-2 tile of an unbounded
+    (GDT) placement, but its staged path needs r* in (6, 16]: features scaled
+    by 8 (map ranges x8, r* ~ 28) or by 0.05 (r* ~ 3) send its parts to the
+    exact per-root fallback (fast_unstaged).  Values to 1e-5 of the float64
+    oracle and argmaxes exact against the oracle on the GPU's own maps, on the
+    two widest root levels."""
+    worst = _pyramid_parity(4, 8, sel_levels=(0, 1), comps=(0, 1), feat_scale=feat_scale)
     assert worst <= 1e-5
 
 
