@@ -504,9 +504,12 @@ def _rooflines(plan, n, kernel_ms, stream, traffic_ok):
     k34_ms = sum(k34_parts.values())
     k34_traffic = [traffic.get(k) for k in ("gdt_x_kernel", "gdt_y_kernel")
                    if "k3x_gdt_rows" in kernel_ms]
-    if "k3k4_place_assemble" in kernel_ms:  # the two-phase kernel, or the round-1 one (DPM_K3=v1)
-        k34_traffic.append(traffic.get("place_assemble_kernel" if os.environ.get("DPM_K3") == "v1"
-                                       else "k3v2::place2_kernel"))
+    if "k3k4_place_assemble" in kernel_ms:  # the two-phase kernels, or the round-1 one (DPM_K3=v1)
+        if os.environ.get("DPM_K3") == "v1":
+            k34_traffic.append(traffic.get("place_assemble_kernel"))
+        else:  # the specialised bulk-tile kernel and the generic one
+            k34_traffic.extend(traffic.get(k) for k in ("k3v2::place2f_kernel", "k3v2::place2_kernel")
+                               if k in traffic or k == "k3v2::place2_kernel")
     k34_traffic = (sum(k34_traffic) if k34_traffic and None not in k34_traffic else None)
     k1_bytes = n * plan.k1_bytes()
     k1_ms = kernel_ms.get("k1_project", 0.0)
@@ -527,9 +530,10 @@ def _rooflines(plan, n, kernel_ms, stream, traffic_ok):
                          "note": "peak = per-launch roofline mix: tcgen05 launches vs the "
                                  "tf32 rate / 2.5, FFMA launches vs the FP32 FFMA rate",
                          "ffma_probe_tflops": probe_tflops,
-                         "traffic": (traffic["corr_tc_kernel"] + traffic["corr_kernel"]
-                                     if "corr_tc_kernel" in traffic and "corr_kernel" in traffic
-                                     else None)},
+                         "traffic": (sum(v for k, v in traffic.items()
+                                         if k.endswith(("corr_tc_kernel", "corr_tc2_kernel",
+                                                        "corr_kernel", "corr_few_kernel")))
+                                     if "corr_tc_kernel" in traffic else None)},
         "k1_project": {"bound": "hbm", "achieved": gbs(k1_bytes, k1_ms), "peak": hbm,
                        "unit": "GB/s", "frac": gbs(k1_bytes, k1_ms) / hbm,
                        "algorithmic_bytes_per_launch": k1_bytes,
