@@ -36,7 +36,8 @@
 // root level), three CTAs per SM (24 warps, 85 registers; 64 KB of shared
 // memory each).  Per part:
 //   wait for the part's S band (TMA boxes, NaN outside the map, mbarrier),
-//   x pass over the band rows (lane = centre column), per-warp column maxima,
+//   x pass over the band rows (lane = centre column), column maxima (shared
+//   atomic max),
 //   one CTA barrier (x words complete, band buffer free, the next part's job
 //   record and tables visible) -> thread 0 issues the next part's band,
 //   y pass for the thread's 4 roots: screen the x words of the column; the
@@ -57,6 +58,15 @@
 // as one shared atomic-max row per part (instead of per-warp rows), two x
 // buffers also fit three CTAs per SM (75.5 KB) and measured the same 7.28 ms.
 // DPM_K3_THREADS / _TH / _XBUF / _MINB rebuild the others.
+//
+// Two kernels over disjoint tile lists (dpm_assemble_prepare numbers them):
+// place2f_kernel, one compile-time instantiation of the above for the bulk
+// tiles (at least 17 roots wide, every part at scale 2 with r* in (6, 16]:
+// 95% of config 4's roots; per-part geometry computed once by warp 0, rare
+// roots resolved out of line), and place2_kernel, the generic form (any
+// width, scale, radius) for the rest.  With both at three CTAs per SM the
+// pair took K3 from 7.27 to 6.99 ms at config 4; at two 12-warp CTAs per SM
+// the specialised kernel had lost (57% against 66% issue).
 #include <math.h>
 #include <stdlib.h>
 
