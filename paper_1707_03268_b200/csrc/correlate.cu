@@ -166,6 +166,50 @@ __device__ __forceinline__ void chunk_fma(unsigned long long (&acc)[K2_MP][NF / 
   }
 }
 
+// chunk_fma with compile-time strides (filter width FW, a full K2_RCH-rank
+// chunk, core stride NFP, two row warps): every LDS of a (j, r) step is the
+// step's base register plus an immediate.  With runtime strides the loop
+// spends ~31 IMADs per 192 FFMA2 on addresses, and IMAD issues to the same
+// FMA-heavy pipe as FFMA2 (ncu: fmaheavy 78% busy, math-pipe throttle the top
+// stall at config 5, R = 32).  Same fma order as chunk_fma.
+template <int FH, int NF, int FW, int NFP>
+__device__ __forceinline__ void chunk_fma_fixed(unsigned long long (&acc)[K2_MP][NF / 2],
+                                                const float* sP, const float* sG, int wy, int wf,
+                                                int lane) {
+  constexpr int MP = K2_MP;
+  constexpr int COL = MP + FH - 1;
+  constexpr int NP = NF / 2;
+  constexpr int NR = K2_RCH;
+  constexpr int TROWS = 2 * MP + FH - 1;
+  constexpr int TPITCH = 32 + FW - 1;
+  constexpr int GI = FW * NR * NFP;  // core stride of a filter row
+  const float* pw = sP + (wy * MP) * TPITCH + lane;
+  const float* gw = sG + wf * NF;
+#pragma unroll 1
+  for (int j = 0; j < FW; ++j) {
+    const float* pj = pw + j;
+    const float* gj = gw + j * (NR * NFP);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      float col[COL];
+#pragma unroll
+      for (int q = 0; q < COL; ++q) col[q] = pj[r * TROWS * TPITCH + q * TPITCH];
+#pragma unroll
+      for (int i = 0; i < FH; ++i) {
+        float g[NF];
+        load_g<NF>(g, gj + r * NFP + i * GI);
+        unsigned long long g2[NP];
+#pragma unroll
+        for (int f = 0; f < NP; ++f) g2[f] = pack2(g[2 * f], g[2 * f + 1]);
+#pragma unroll
+        for (int p = 0; p < MP; ++p)
+#pragma unroll
+          for (int f = 0; f < NP; ++f) ffma2(acc[p][f], col[p + i], g2[f]);
+      }
+    }
+  }
+}
+
 // epilogue: coalesced stores (lane = x), optional per-map range fold
 template <int FH, int NF>
 __device__ __forceinline__ void tile_epilogue(unsigned long long (&acc)[K2_MP][NF / 2],
@@ -221,7 +265,7 @@ __device__ __forceinline__ void stage_g_async(float* sG, const CorrArgs& a,
 // Rank-chunk pipeline for R > K2_RCH: a step is (tile, rank chunk); the P and
 // core chunks of step s+1 are copied (cp.async) while step s computes, into
 // the other half of double buffers; accumulators live across a tile's chunks.
-template <int FH, int NF>
+template <int FH, int NF, int FW = 0, int NFP = 0>
 __device__ __forceinline__ void corr_chunked(const CorrArgs& a, float* smem, int PBUF, int GBUF,
                                              int TY, int TROWS, int TPITCH) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -260,8 +304,18 @@ __device__ __forceinline__ void corr_chunked(const CorrArgs& a, float* smem, int
     }
     __syncthreads();  // step s resident for every warp
     const int nr = min(K2_RCH, job.R - rc);
-    chunk_fma<FH, NF>(acc, smem + buf * PBUF, sG0 + buf * GBUF, wy, wf, lane, nr, job.w,
-                      job.nf_pad, TROWS, TPITCH);
+    if constexpr (FW > 0) {
+      if (nr == K2_RCH && job.w == FW && job.nf_pad == NFP) {
+        DPM_CHECK(TPITCH == 32 + FW - 1 && TROWS == 2 * K2_MP + FH - 1, "fixed strides");
+        chunk_fma_fixed<FH, NF, FW, NFP>(acc, smem + buf * PBUF, sG0 + buf * GBUF, wy, wf, lane);
+      } else {
+        chunk_fma<FH, NF>(acc, smem + buf * PBUF, sG0 + buf * GBUF, wy, wf, lane, nr, job.w,
+                          job.nf_pad, TROWS, TPITCH);
+      }
+    } else {
+      chunk_fma<FH, NF>(acc, smem + buf * PBUF, sG0 + buf * GBUF, wy, wf, lane, nr, job.w,
+                        job.nf_pad, TROWS, TPITCH);
+    }
     if (nrc == 0 || nt != t)  // last chunk of this tile
       tile_epilogue<FH, NF>(acc, a, job, tile.tx * 32, tile.ty * TY, wy, wf, lane);
     t = nt;
@@ -271,7 +325,7 @@ __device__ __forceinline__ void corr_chunked(const CorrArgs& a, float* smem, int
   asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-template <int FH, int NF>
+template <int FH, int NF, int FW = 0, int NFP = 0>
 __global__ void __launch_bounds__(32 * K2_MAX_WARPS)
 corr_kernel(const CorrArgs a) {
   constexpr int MP = K2_MP;
@@ -284,7 +338,7 @@ corr_kernel(const CorrArgs a) {
   const int PBUF = (K2_RCH * TROWS * TPITCH + 3) & ~3;
   if (a.R_max > K2_RCH) {  // several rank chunks per tile: chunk pipeline
     const int GBUF = (FH * a.w_max * K2_RCH * ((a.nf_max + 7) & ~7) + 3) & ~3;
-    corr_chunked<FH, NF>(a, smem, PBUF, GBUF, TY, TROWS, TPITCH);
+    corr_chunked<FH, NF, FW, NFP>(a, smem, PBUF, GBUF, TY, TROWS, TPITCH);
     return;
   }
   // P double buffer [2][RCH][TROWS][TPITCH] at smem, core [FH][w][RCH][nf_pad] after it
@@ -421,6 +475,15 @@ static bool few_enabled() {
   return on;
 }
 
+// DPM_K2FIXED=0 keeps the runtime-stride inner loop for R > 8 (A/B)
+static bool fixed_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DPM_K2FIXED");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int FH>
 static corr_fn by_nf(int nfk) {
   switch (nfk) {
@@ -505,6 +568,11 @@ extern "C" int dpm_correlate(const float* P, const float* G, float* S, const dpm
   DPM_REQUIRE(smem <= 227 * 1024, "dpm_correlate: h=%d w=%d nf=%d needs %zu B shared memory",
               h, w_max, nf, smem);
   corr_fn fn = kernel_for(h, s.nf_kernel);
+  // R > 8 with 6x6 filters in groups of 16 / 48: compile-time strides (chunk_fma_fixed)
+  if (R > K2_RCH && h == 6 && w_max == 6 && s.nf_kernel == 8 && s.nwy == 2 && fixed_enabled()) {
+    if (nfp == 48) fn = corr_kernel<6, 8, 6, 48>;
+    else if (nfp == 16) fn = corr_kernel<6, 8, 6, 16>;
+  }
   DPM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   const int threads = 32 * s.nwf * s.nwy;
