@@ -60,20 +60,68 @@ __device__ __forceinline__ void f_ffma2(unsigned long long& acc, float a, unsign
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(f_pack2(a, a)), "l"(b));
 }
 
-template <int FH, int NF>
+// One staged chunk of a warp's filter-row slice (NKS rows starting at the
+// warp's i0): every shared-memory address is a per-j base plus an immediate
+// (compile-time tile pitch TP, plane stride PROW * TP, core layout
+// [j][r][i][NF]); full chunks unroll the ranks.  Same fma order as before
+// (j, r, i), so the sums are unchanged bit for bit.
+template <int NKS, int MP, int NF, int FH, int TP, int PROW>
+__device__ __forceinline__ void few_chunk(unsigned long long (&acc)[MP][NF / 2], const float* sp,
+                                          const float* sg, int w, int nr) {
+  constexpr int NP = NF / 2, COL = MP + NKS - 1, PLANE = PROW * TP;
+  const bool full = nr == FEW_RCH;
+#pragma unroll 1
+  for (int j = 0; j < w; ++j) {
+    const float* pj = sp + j;
+    const float* gj = sg + j * nr * FH * NF;
+#pragma unroll
+    for (int r = 0; r < FEW_RCH; ++r) {
+      if (!full && r >= nr) break;
+      float col[COL];
+#pragma unroll
+      for (int q = 0; q < COL; ++q) col[q] = pj[r * PLANE + q * TP];
+#pragma unroll
+      for (int i = 0; i < NKS; ++i) {
+        unsigned long long g2[NP];
+        const float* gp = gj + (r * FH + i) * NF;
+        if constexpr (NF % 4 == 0) {
+#pragma unroll
+          for (int f = 0; f < NP; f += 2) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(gp + 2 * f);
+            g2[f] = v.x;
+            g2[f + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int f = 0; f < NP; ++f) g2[f] = *reinterpret_cast<const unsigned long long*>(gp + 2 * f);
+        }
+#pragma unroll
+        for (int p = 0; p < MP; ++p)
+#pragma unroll
+          for (int f = 0; f < NP; ++f) f_ffma2(acc[p][f], col[p + i], g2[f]);
+      }
+    }
+  }
+}
+
+template <int FH, int NF, int TP>
 __global__ void __launch_bounds__(64 * few_split(FH, NF))
 corr_few_kernel(const FewArgs a) {
   constexpr int SK = few_split(FH, NF), KS = few_ks(FH, NF);
-  constexpr int MP = FEW_MP, NP = NF / 2, COL = MP + KS - 1;
+  constexpr int KS_LAST = FH - (SK - 1) * KS;  // rows of the last slice
+  static_assert(KS_LAST >= 1 && KS_LAST <= KS, "every filter-row slice is non-empty");
+  constexpr int MP = FEW_MP, NP = NF / 2;
   constexpr int NT = 64 * SK;
+  constexpr int PROW = FEW_TY + SK * KS - 1;   // P rows per plane (= a.prow)
+  constexpr int TPITCH = TP;                   // P tile pitch (>= 32 + w - 1)
   extern __shared__ __align__(16) float smem[];
-  float* const sP0 = smem;                      // [2][RCH][prow][TPITCH]
-  float* const sG0 = smem + 2 * a.pbuf;         // [2][FH][w][RCH][NF]
+  float* const sP0 = smem;                      // [2][RCH][PROW][TP]
+  float* const sG0 = smem + 2 * a.pbuf;         // [2][w][RCH][FH][NF]
   float* const sX = sG0 + 2 * a.gbuf;           // [SK-1][2][MP][NF][32] partial sums
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wy = warp & 1, wk = warp >> 1;     // row block, filter-row slice
   const int i0 = wk * KS;                       // first filter row of this warp
-  const int TPITCH = 32 + a.w_max - 1;
+  DPM_CHECK(a.prow == PROW && 32 + a.w_max - 1 <= TP, "compile-time tile geometry");
 
   // stage the P and core chunk (ranks rc .. rc + nr) of tile t into buffer b
   auto issue = [&](int t, int rc, int b) {
@@ -85,9 +133,11 @@ corr_few_kernel(const FewArgs a) {
     const int rows = FH * jb.w * nr;
     for (int e = threadIdx.x; e < rows; e += NT) {
       const int ij = e / nr, r = e - ij * nr;
+      const int i = ij / jb.w, j = ij - i * jb.w;
       const float* src = a.G + jb.g_off + ((int64_t)ij * jb.R + rc + r) * jb.nf_pad;
-      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sg + e * NF);
-      DPM_CHECK((e + 1) * NF <= a.gbuf, "core chunk fits its buffer");
+      const int d = (j * nr + r) * FH + i;  // smem layout [j][r][i][NF]
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sg + d * NF);
+      DPM_CHECK((d + 1) * NF <= a.gbuf, "core chunk fits its buffer");
       if constexpr (NF % 4 == 0) {
 #pragma unroll
         for (int q = 0; q < NF / 4; ++q)
@@ -152,31 +202,14 @@ corr_few_kernel(const FewArgs a) {
     __syncthreads();  // step s resident
     const int nr = min(FEW_RCH, R - rc);
     const float* sp = sP0 + buf * a.pbuf + (wy * MP + i0) * TPITCH + lane;
-    const float* sg = sG0 + buf * a.gbuf + i0 * w * nr * NF;
-    DPM_CHECK(((nr - 1) * a.prow + wy * MP + i0 + COL) * TPITCH <= a.pbuf && w <= a.w_max &&
-                  (min(FH, i0 + KS) * w * nr) * NF <= a.gbuf,
+    const float* sg = sG0 + buf * a.gbuf + i0 * NF;
+    DPM_CHECK(((nr - 1) * PROW + wy * MP + i0 + MP + KS - 1) * TPITCH <= a.pbuf && w <= a.w_max &&
+                  (w * nr * FH) * NF <= a.gbuf,
               "compute reads stay inside the staged chunk");
-    for (int j = 0; j < w; ++j) {
-      for (int r = 0; r < nr; ++r) {
-        const float* pc = sp + r * a.prow * TPITCH + j;
-        float col[COL];
-#pragma unroll
-        for (int q = 0; q < COL; ++q) col[q] = pc[q * TPITCH];
-        const float* gp = sg + (j * nr + r) * NF;
-#pragma unroll
-        for (int i = 0; i < KS; ++i) {
-          if (i0 + i >= FH) break;  // the last slice may be short (warp-uniform)
-          unsigned long long g2[NP];
-#pragma unroll
-          for (int f = 0; f < NP; ++f)
-            g2[f] = *reinterpret_cast<const unsigned long long*>(gp + i * w * nr * NF + 2 * f);
-#pragma unroll
-          for (int p = 0; p < MP; ++p)
-#pragma unroll
-            for (int f = 0; f < NP; ++f) f_ffma2(acc[p][f], col[p + i], g2[f]);
-        }
-      }
-    }
+    if (wk == SK - 1)
+      few_chunk<KS_LAST, MP, NF, FH, TPITCH, PROW>(acc, sp, sg, w, nr);
+    else
+      few_chunk<KS, MP, NF, FH, TPITCH, PROW>(acc, sp, sg, w, nr);
     if (nt != t) {  // last chunk of the tile: sum the filter-row slices, store
       if constexpr (SK > 1) {
         if (wk > 0) {
@@ -249,25 +282,33 @@ corr_few_kernel(const FewArgs a) {
 
 typedef void (*few_fn)(const FewArgs);
 
-template <int FH>
+// compile-time tile pitch: 40 floats for filters up to 9 wide, 48 up to 17
+template <int FH, int TP>
 static few_fn few_by_nf(int nf) {
-  if (nf <= 2) return corr_few_kernel<FH, 2>;
-  if (nf <= 4) return corr_few_kernel<FH, 4>;
-  if (nf <= 6) return corr_few_kernel<FH, 6>;
-  return corr_few_kernel<FH, 8>;
+  if (nf <= 2) return corr_few_kernel<FH, 2, TP>;
+  if (nf <= 4) return corr_few_kernel<FH, 4, TP>;
+  if (nf <= 6) return corr_few_kernel<FH, 6, TP>;
+  return corr_few_kernel<FH, 8, TP>;
 }
 
-static few_fn few_kernel_for(int h, int nf) {
+template <int FH>
+static few_fn few_by_w(int nf, int tp) {
+  return tp == 40 ? few_by_nf<FH, 40>(nf) : few_by_nf<FH, 48>(nf);
+}
+
+static int few_pitch(int w_max) { return w_max <= 9 ? 40 : w_max <= 17 ? 48 : 0; }
+
+static few_fn few_kernel_for(int h, int nf, int tp) {
   switch (h) {
-    case 2: return few_by_nf<2>(nf);
-    case 3: return few_by_nf<3>(nf);
-    case 4: return few_by_nf<4>(nf);
-    case 5: return few_by_nf<5>(nf);
-    case 6: return few_by_nf<6>(nf);
-    case 7: return few_by_nf<7>(nf);
-    case 8: return few_by_nf<8>(nf);
-    case 11: return few_by_nf<11>(nf);
-    case 15: return few_by_nf<15>(nf);
+    case 2: return few_by_w<2>(nf, tp);
+    case 3: return few_by_w<3>(nf, tp);
+    case 4: return few_by_w<4>(nf, tp);
+    case 5: return few_by_w<5>(nf, tp);
+    case 6: return few_by_w<6>(nf, tp);
+    case 7: return few_by_w<7>(nf, tp);
+    case 8: return few_by_w<8>(nf, tp);
+    case 11: return few_by_w<11>(nf, tp);
+    case 15: return few_by_w<15>(nf, tp);
     default: return nullptr;
   }
 }
@@ -279,13 +320,13 @@ static int nf_kernel(int nf) { return nf <= 2 ? 2 : nf <= 4 ? 4 : nf <= 6 ? 6 : 
 int launch_corr_few(const float* P, const float* G, float* S, const dpm_corr_job* jobs,
                     const dpm_corr_tile* tiles, int ntiles, int h, int nf, int w_max,
                     uint32_t* ranges, cudaStream_t st) {
-  few_fn fn = nf >= 1 && nf <= 8 ? few_kernel_for(h, nf) : nullptr;
+  const int tpitch = few_pitch(w_max);
+  few_fn fn = nf >= 1 && nf <= 8 && tpitch > 0 ? few_kernel_for(h, nf, tpitch) : nullptr;
   if (fn == nullptr) return DPM_ERR_UNSUPPORTED;
   const int nfk = nf_kernel(nf);
   const int sk = few_split(h, nfk), ks = few_ks(h, nfk);
   FewArgs a{P, G, S, jobs, tiles, ntiles, w_max, ranges, 0, 0, 0};
   a.prow = FEW_TY + sk * ks - 1;  // rows the last filter-row slice may touch
-  const int tpitch = 32 + w_max - 1;
   a.pbuf = (FEW_RCH * a.prow * tpitch + 3) & ~3;
   a.gbuf = (h * w_max * FEW_RCH * nfk + 3) & ~3;
   const size_t xbuf = (size_t)(sk - 1) * 2 * FEW_MP * nfk * 32;
