@@ -293,6 +293,24 @@ class Plan:
         self.n_ranges = nslots
         self._corr_jobs = np.array(jobs, dtype=_lib.CORR_JOB) if jobs else np.zeros(0, _lib.CORR_JOB)
         self._corr_job_image = np.array(job_image, dtype=np.int64)
+        # A class of > 8 filters with fewer tiles than SMs (e.g. config 5's 16-filter
+        # part groups at the small levels where only two components fit) is a
+        # latency-bound launch of its own: its tiles join the largest > 8-filter
+        # class of the same filter height, whose 32 x 16 tiles and per-job cores
+        # serve any nf up to its own (the extra filter warps of those few tiles idle).
+        for h in sorted({h for h, _ in classes}):
+            big = [(len(c["tiles"]), nf) for (hh, nf), c in classes.items() if hh == h and nf > 8]
+            if len(big) < 2:
+                continue
+            target = classes[(h, max(big)[1])]
+            tnf = max(big)[1]
+            for n, nf in big:
+                c = classes[(h, nf)]
+                if c is not target and nf < tnf and n < _sm_count():
+                    target["tiles"].extend(c["tiles"])
+                    target["w_max"] = max(target["w_max"], c["w_max"])
+                    target["R"] = max(target["R"], c["R"])
+                    del classes[(h, nf)]
         self._classes = []
         for (h, nf), cls in sorted(classes.items()):
             # tiles sorted by core so persistent CTAs keep it resident
