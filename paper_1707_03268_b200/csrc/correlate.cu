@@ -201,10 +201,19 @@ __device__ __forceinline__ void chunk_fma_fixed(unsigned long long (&acc)[K2_MP]
         unsigned long long g2[NP];
 #pragma unroll
         for (int f = 0; f < NP; ++f) g2[f] = pack2(g[2 * f], g[2 * f + 1]);
+#ifdef DPM_K2_POUTER
 #pragma unroll
         for (int p = 0; p < MP; ++p)
 #pragma unroll
           for (int f = 0; f < NP; ++f) ffma2(acc[p][f], col[p + i], g2[f]);
+#else
+        // filter pair outer: consecutive FFMA2 reuse the 64-bit core pair (operand
+        // reuse cache) and read only the scalar P value and the accumulator
+#pragma unroll
+        for (int f = 0; f < NP; ++f)
+#pragma unroll
+          for (int p = 0; p < MP; ++p) ffma2(acc[p][f], col[p + i], g2[f]);
+#endif
       }
     }
   }
