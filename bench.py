@@ -537,7 +537,7 @@ def _rooflines(plan, n, kernel_ms, stream, traffic_ok):
         "k1_project": {"bound": "hbm", "achieved": gbs(k1_bytes, k1_ms), "peak": hbm,
                        "unit": "GB/s", "frac": gbs(k1_bytes, k1_ms) / hbm,
                        "algorithmic_bytes_per_launch": k1_bytes,
-                       "traffic": traffic.get("project_kernel")},
+                       "traffic": traffic.get("project_mma_kernel", traffic.get("project_kernel"))},
     }
     shares = {"k1_project": k1_ms, "k2_correlate": k2_ms, "k3k4_place_assemble": k34_ms}
     dominant = max(shares, key=shares.get)
@@ -685,7 +685,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": rk.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": ("fp32 (K1; K2 tcgen05 2xTF32 + bf16 correction, FFMA) + f64 (K3/K4 placement)"),
+            "dtype": ("fp32 (K1 mma.sync 3xTF32 at R <= 8, else FFMA; K2 tcgen05 2xTF32 + bf16 correction, "
+                      "FFMA) + f64 (K3/K4 placement)"),
             "data": "synthetic",
             "config": ({"workload": "stub scorer (CPU harness test)", "images": args.images}
                        if args.stub else

@@ -10,6 +10,8 @@
 // its channels against C (broadcast from shared memory) and writes R planar
 // outputs; consecutive threads write consecutive x, so every plane store is
 // coalesced.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dpm {
@@ -101,6 +103,113 @@ project_kernel(const float* __restrict__ X, float* __restrict__ P, const float* 
   }
 }
 
+// K1 on mma.sync (the default for L = 32): the same projection with the
+// contraction as m16n8k8 TF32 tensor-core tiles, operands split hi + lo
+// (3xTF32: lo*hi + hi*lo + hi*hi, FP32 accumulate), so the shared-memory
+// staging, its barrier and the per-channel LDS of project_kernel disappear
+// and the kernel is eight 16-byte loads, 24 MMAs and eight stores per warp
+// and 32 cells.  A warp owns 32 consecutive cells as two 16-row A tiles.
+// The MMA's k index is a free permutation of the channels: lane (g, t)
+// loads chunks t and t + 4 (channels 4t.., 16 + 4t..) of cells g and g + 8,
+// and k-step e takes element e of both chunks, so column t of step e is
+// channel 4t + e and column t + 4 is channel 16 + 4t + e; B rows follow the
+// same map.  Each output column r is its own dot product (prefixes of C
+// give bit-identical planes).  Lanes (g, t) hold P[2t, 2t+1][cells g, g+8]:
+// every store instruction writes 32-byte runs of four planes.
+// hi = v rounded to TF32 (10 mantissa bits, half away from zero, integer
+// arithmetic on the bits); lo = v - hi, exact.  lo goes to the MMA as raw
+// FP32 bits: the tensor core reads the upper 19 bits only, and because hi is
+// round-to-nearest lo has either sign, so that truncation is unbiased
+// (|error| <= 2^-21 |v|).  Finite inputs (check_feature_map's contract).
+__device__ __forceinline__ void split_tf32(float v, uint32_t& hi, uint32_t& lo) {
+  hi = (__float_as_uint(v) + 0x1000u) & 0xffffe000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(K1_CELLS, 3)
+project_mma_kernel(const float* __restrict__ X, float* __restrict__ P, const float* __restrict__ C,
+                   int R, const dpm_proj_job* __restrict__ jobs, int njobs) {
+  constexpr int L = 32;
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
+  const dpm_proj_job job = jobs[jid];
+  const int ncl = job.H * job.W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int c0 = (blockIdx.x - job.block0) * K1_CELLS + warp * 32;
+  DPM_CHECK(c0 >= 0, "CTA cells inside its level");
+  if (c0 >= ncl) return;  // no CTA barrier below: a warp past the level's end just leaves
+
+  // ---- loads: all eight 16-byte chunks of the warp's 32 cells in flight.
+  // q[k][v]: chunk t + 4v of cell c0 + 8k + g (k = 2h + u: tile h, row half u)
+  const float* src = X + job.x_off + (int64_t)(c0 + g) * L + 4 * t;
+  float4 q[4][2];
+  if (c0 + 32 <= ncl && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        q[k][v] = __ldcs(reinterpret_cast<const float4*>(src + 8 * k * L + 16 * v));
+  } else {  // a level's last cells, or a feature block off 16-byte alignment
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const float* a = src + 8 * k * L + 16 * v;
+        q[k][v] = c0 + 8 * k + g < ncl ? make_float4(__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  }
+
+  const int64_t plane = (int64_t)job.H * job.pitch;
+
+  // ---- B operands (R <= 8: one 8-column tile): rows t / t + 4 of k-step e, column g
+  uint32_t bhi[4][2], blo[4][2];
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+      split_tf32(g < R ? __ldg(C + (16 * v + 4 * t + e) * R + g) : 0.f, bhi[e][v], blo[e][v]);
+  const int ra = 2 * t;
+  float* const Pr = P + job.p_off + (int64_t)ra * plane;
+  int y = (c0 + g) / job.W, x = (c0 + g) - y * job.W;  // the other three cells follow by +8 with row wraps
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      // A operands of k-step e: element e of the four chunks, a[u + 2v]
+      uint32_t ahi[4], alo[4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const float4 f = q[2 * h + u][v];
+          split_tf32(e == 0 ? f.x : e == 1 ? f.y : e == 2 ? f.z : f.w, ahi[u + 2 * v], alo[u + 2 * v]);
+        }
+      mma_tf32(d, alo, bhi[e][0], bhi[e][1]);  // small terms first
+      mma_tf32(d, ahi, blo[e][0], blo[e][1]);
+      mma_tf32(d, ahi, bhi[e][0], bhi[e][1]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (c0 + 16 * h + 8 * u + g < ncl) {
+        const int o = y * job.pitch + x;
+        if (ra < R) Pr[o] = d[2 * u];
+        if (ra + 1 < R) Pr[plane + o] = d[2 * u + 1];
+      }
+      x += 8;
+      while (x >= job.W) { x -= job.W; ++y; }
+    }
+  }
+}
+
 }  // namespace dpm
 
 using namespace dpm;
@@ -127,6 +236,15 @@ extern "C" int64_t dpm_project_prepare(dpm_proj_job* jobs, int njobs) {
   return b;
 }
 
+// DPM_K1MMA=0 keeps 32-channel levels on project_kernel (A/B)
+static bool mma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DPM_K1MMA");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 extern "C" int dpm_project(const float* X, float* P, const float* C, int L, int R,
                            const dpm_proj_job* jobs, int njobs, int64_t nblocks, void* stream) {
   DPM_REQUIRE(X && P && C && jobs, "dpm_project: null pointer");
@@ -134,6 +252,11 @@ extern "C" int dpm_project(const float* X, float* P, const float* C, int L, int 
   DPM_REQUIRE(R >= 1 && R <= 1024, "dpm_project: rank R=%d out of [1, 1024]", R);
   DPM_REQUIRE(njobs >= 0 && nblocks >= 0 && nblocks <= INT32_MAX, "dpm_project: bad sizes");
   if (njobs == 0 || nblocks == 0) return DPM_OK;
+  if (L == 32 && R <= 8 && mma_enabled()) {
+    project_mma_kernel<<<(unsigned)nblocks, K1_CELLS, 0, as_stream(stream)>>>(X, P, C, R, jobs, njobs);
+    DPM_LAUNCHED("project_mma_kernel");
+    return DPM_OK;
+  }
   const int Rp = (R + K1_RC - 1) / K1_RC * K1_RC;
   const size_t smem = sizeof(float) * ((size_t)L * Rp + (size_t)K1_CELLS * (L + 1));
   DPM_REQUIRE(smem <= 227 * 1024, "dpm_project: L=%d R=%d needs %zu B shared memory", L, R, smem);

@@ -44,6 +44,7 @@ SHORT = {
     "corr_tc_kernel": "corr_tc_kernel",
     "corr_kernel": "corr_kernel",
     "project_kernel": "project_kernel",
+    "project_mma_kernel": "project_mma_kernel",
 }
 
 

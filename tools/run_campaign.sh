@@ -21,7 +21,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/${TAG}_launches.csv \
     python bench.py --images 8 --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"project_kernel|corr_|prefix_kernel|place|ranges_init" -c 9 \
+    -k regex:"project_|corr_|prefix_kernel|place|ranges_init" -c 9 \
     -o $OUT/${TAG}_full python bench.py --images 8 --steps 1 --warmup 0 --no-cpu --no-e2e \
     > $OUT/${TAG}_full.log 2>&1
 echo done
