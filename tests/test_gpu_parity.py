@@ -73,6 +73,68 @@ def test_cp_engine_edge_shapes_generic_and_chunked_kernels():
         assert_map_close(B.correlate3_cp(img, cp).scores, ref, f"{ishape}/{dims}/{rank}")
 
 
+def test_project_mma_kernel_ragged_levels_offsets_and_prefix_identity():
+    """K1 through the C ABI (dpm_project) on 32-channel levels at R <= 8 -- the
+    mma.sync kernel: levels whose cell count is not a multiple of 32 or 256,
+    widths below 8 (row wraps inside a lane's +8 stride), a feature block off
+    16-byte alignment (scalar-load path), R < 8, against the float64 oracle
+    (correlation.py:128); planes of a prefix of C are bit-identical."""
+    import torch
+
+    from paper_1707_03268_b200 import _lib
+    from paper_1707_03268_b200.device import upload_table
+
+    lib = _lib.lib()
+    rng = np.random.default_rng(11)
+    shapes = [(1, 1), (3, 5), (2, 16), (7, 33), (40, 37), (17, 256), (90, 160), (300, 3)]
+    for R in (8, 4, 1, 7):
+        for shift in (0, 1):  # float offset of the first level: 0, or off 16-byte alignment
+            C = rng.normal(size=(32, R)).astype(np.float32)
+            levels = [rng.random((h, w, 32), dtype=np.float32) * 0.4 for h, w in shapes]
+            x_off, p_off, jobs = shift, 0, []
+            for (h, w) in shapes:
+                pitch = (w + 3) // 4 * 4
+                jobs.append((x_off, p_off, h, w, pitch, 0))
+                x_off += h * w * 32 + (4 if shift == 0 else 0)
+                p_off += R * h * pitch
+            pj = np.array(jobs, dtype=_lib.PROJ_JOB)
+            nblk = _lib.check(lib.dpm_project_prepare(_lib.table_ptr(pj), len(pj)), "project")
+            X = torch.zeros(x_off + 8, dtype=torch.float32, device="cuda")
+            for j, lv in zip(jobs, levels):
+                X[j[0]:j[0] + lv.size] = torch.from_numpy(lv.ravel()).cuda()
+            P = torch.full((p_off,), float("nan"), dtype=torch.float32, device="cuda")
+            Cd = torch.from_numpy(C).cuda()
+            tab = upload_table(pj, "cuda")
+            st = torch.cuda.current_stream().cuda_stream
+            _lib.check(lib.dpm_project(X.data_ptr(), P.data_ptr(), Cd.data_ptr(), 32, R,
+                                       tab.data_ptr(), len(pj), nblk, st), "project")
+            out = P.cpu().numpy()
+            for j, lv in zip(jobs, levels):
+                _, po, h, w, pitch, _ = j
+                got = out[po:po + R * h * pitch].reshape(R, h, pitch)[:, :, :w]
+                ref = O.project(lv.astype(np.float64), C.astype(np.float64)).transpose(2, 0, 1)
+                assert_map_close(got, ref, f"K1 {h}x{w} R={R} shift={shift}", rtol=2e-6)
+            if R == 8 and shift == 0:  # prefix of the basis: the same planes, bit for bit
+                for k in (1, 5):
+                    Ck = torch.from_numpy(np.ascontiguousarray(C[:, :k])).cuda()
+                    jk, po = [], 0
+                    for (xo, _, h, w, pitch, _) in jobs:
+                        jk.append((xo, po, h, w, pitch, 0))
+                        po += k * h * pitch
+                    pk = np.array(jk, dtype=_lib.PROJ_JOB)
+                    nb = _lib.check(lib.dpm_project_prepare(_lib.table_ptr(pk), len(pk)), "project")
+                    Pk = torch.zeros(po, dtype=torch.float32, device="cuda")
+                    tk = upload_table(pk, "cuda")
+                    _lib.check(lib.dpm_project(X.data_ptr(), Pk.data_ptr(), Ck.data_ptr(), 32, k,
+                                               tk.data_ptr(), len(pk), nb, st), "project")
+                    outk = Pk.cpu().numpy()
+                    for j8, jk_ in zip(jobs, jk):
+                        h, w, pitch = j8[2], j8[3], j8[4]
+                        a = out[j8[1]:j8[1] + k * h * pitch].reshape(k, h, pitch)[:, :, :w]
+                        b = outk[jk_[1]:jk_[1] + k * h * pitch].reshape(k, h, pitch)[:, :, :w]
+                        assert np.array_equal(a, b), f"prefix {k} planes differ on {h}x{w}"
+
+
 def test_dense_many_filters_group_split():
     """More than 48 same-shape filters on one level: K2 splits the group."""
     rng = np.random.default_rng(5)
