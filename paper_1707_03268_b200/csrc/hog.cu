@@ -18,6 +18,8 @@
 // fixed order (no FMA contraction), the oracle emulates them bit for bit, so
 // orientation bins agree exactly; histograms and features are FP32 sums
 // compared at 1e-5.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dpm {
@@ -39,47 +41,101 @@ __constant__ float kHogV[9] = {0.0f,           0x1.5e3a88p-2f, 0x1.491b76p-1f,
 template <typename T>
 __device__ __forceinline__ float pix(const T* p) { return (float)*p; }
 
-// Box-filter resampling, one thread per output pixel (all channels).
-template <typename T>
-__global__ void __launch_bounds__(RS_THREADS)
-resample_kernel(const T* __restrict__ img, float* __restrict__ out,
-                const dpm_resample_job* __restrict__ jobs, int njobs) {
-  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
-  const dpm_resample_job j = jobs[jid];
-  const int64_t e = (int64_t)(blockIdx.x - j.block0) * RS_THREADS + threadIdx.x;
-  if (e >= (int64_t)j.Hs * j.Ws) return;
-  const int oy = (int)(e / j.Ws), ox = (int)(e - (int64_t)oy * j.Ws);
+// Box-filter resampling, one thread per output pixel (all channels).  CC > 0
+// fixes the channel count at compile time (unrolled, 32-bit pixel indices);
+// the float operations and their order are the same for every CC.
+template <typename T, int CC>
+__device__ __forceinline__ void resample_body(const T* __restrict__ img, float* __restrict__ out,
+                                              const dpm_resample_job& j, int blk) {
+  const int C = CC ? CC : j.C;
+  constexpr int CM = CC ? CC : 4;
+  const int e = blk * RS_THREADS + (int)threadIdx.x;  // Hs * Ws * C fits 31 bits (prepare)
+  if (e >= j.Hs * j.Ws) return;
+  const int oy = e / j.Ws, ox = e - oy * j.Ws;
   const float sy = __fdiv_rn((float)j.H, (float)j.Hs), sx = __fdiv_rn((float)j.W, (float)j.Ws);
   const float ay = __fmul_rn((float)oy, sy), by = __fmul_rn((float)(oy + 1), sy);
   const float ax = __fmul_rn((float)ox, sx), bx = __fmul_rn((float)(ox + 1), sx);
   const int iy0 = (int)floorf(ay), iy1 = min((int)ceilf(by), j.H);
   const int ix0 = (int)floorf(ax), ix1 = min((int)ceilf(bx), j.W);
   const T* base = img + j.img_off;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int iy = iy0; iy < iy1; ++iy) {
-    const float wy = __fsub_rn(fminf((float)(iy + 1), by), fmaxf((float)iy, ay));
-    float row[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int ix = ix0; ix < ix1; ++ix) {
-      const float wx = __fsub_rn(fminf((float)(ix + 1), bx), fmaxf((float)ix, ax));
-      const T* p = base + ((int64_t)iy * j.W + ix) * j.C;
-      for (int c = 0; c < j.C; ++c) row[c] = __fadd_rn(row[c], __fmul_rn(wx, pix(p + c)));
+  const int nx = ix1 - ix0;
+  float acc[CM];
+#pragma unroll
+  for (int c = 0; c < CM; ++c) acc[c] = 0.f;
+  if (nx <= 4) {  // every pyramid step (scale < 3): column weights once, not once per row
+    float wxs[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      wxs[k] = __fsub_rn(fminf((float)(ix0 + k + 1), bx), fmaxf((float)(ix0 + k), ax));
+    for (int iy = iy0; iy < iy1; ++iy) {
+      const float wy = __fsub_rn(fminf((float)(iy + 1), by), fmaxf((float)iy, ay));
+      float row[CM];
+#pragma unroll
+      for (int c = 0; c < CM; ++c) row[c] = 0.f;
+      const T* p = base + (iy * j.W + ix0) * C;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < nx) {
+#pragma unroll
+          for (int c = 0; c < CM; ++c)
+            if (c < C) row[c] = __fadd_rn(row[c], __fmul_rn(wxs[k], pix(p + k * C + c)));
+        }
+#pragma unroll
+      for (int c = 0; c < CM; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(wy, row[c]));
     }
-    for (int c = 0; c < j.C; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(wy, row[c]));
+  } else {
+    for (int iy = iy0; iy < iy1; ++iy) {
+      const float wy = __fsub_rn(fminf((float)(iy + 1), by), fmaxf((float)iy, ay));
+      float row[CM];
+#pragma unroll
+      for (int c = 0; c < CM; ++c) row[c] = 0.f;
+      for (int ix = ix0; ix < ix1; ++ix) {
+        const float wx = __fsub_rn(fminf((float)(ix + 1), bx), fmaxf((float)ix, ax));
+        const T* p = base + (iy * j.W + ix) * C;
+#pragma unroll
+        for (int c = 0; c < CM; ++c)
+          if (c < C) row[c] = __fadd_rn(row[c], __fmul_rn(wx, pix(p + c)));
+      }
+#pragma unroll
+      for (int c = 0; c < CM; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(wy, row[c]));
+    }
   }
   const float d = __fmul_rn(sy, sx);
-  float* o = out + j.out_off + e * j.C;
-  for (int c = 0; c < j.C; ++c) o[c] = __fdiv_rn(acc[c], d);
+  float* o = out + j.out_off + e * C;
+#pragma unroll
+  for (int c = 0; c < CM; ++c)
+    if (c < C) o[c] = __fdiv_rn(acc[c], d);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RS_THREADS)
+resample_kernel(const T* __restrict__ img, float* __restrict__ out,
+                const dpm_resample_job* __restrict__ jobs, int njobs) {
+  const int jid = find_job_warp(jobs, njobs, blockIdx.x);
+  const dpm_resample_job j = jobs[jid];
+  const int blk = blockIdx.x - j.block0;
+  if (j.C == 3) resample_body<T, 3>(img, out, j, blk);
+  else if (j.C == 1) resample_body<T, 1>(img, out, j, blk);
+  else resample_body<T, 0>(img, out, j, blk);
 }
 
 // Gradient magnitude and orientation bin (0..17) of resampled pixel (y, x).
-__device__ __forceinline__ void grad_bin(const float* __restrict__ R, int Hs, int Ws, int C, int y,
+template <int CC>
+__device__ __forceinline__ void grad_bin(const float* __restrict__ R, int Hs, int Ws, int Cj, int y,
                                          int x, float& v, int& bin) {
+  const int C = CC ? CC : Cj;  // CC > 0: compile-time channel count (unrolled)
   const int xr = min(x + 1, Ws - 1), xl = max(x - 1, 0);
   const int yd = min(y + 1, Hs - 1), yu = max(y - 1, 0);
+  const float* pr = R + (y * Ws + xr) * C;  // Hs * Ws * C fits 31 bits (prepare)
+  const float* pl = R + (y * Ws + xl) * C;
+  const float* pd = R + (yd * Ws + x) * C;
+  const float* pu = R + (yu * Ws + x) * C;
   float best = -1.f, bdx = 0.f, bdy = 0.f;
-  for (int c = 0; c < C; ++c) {
-    const float dx = __fsub_rn(R[((int64_t)y * Ws + xr) * C + c], R[((int64_t)y * Ws + xl) * C + c]);
-    const float dy = __fsub_rn(R[((int64_t)yd * Ws + x) * C + c], R[((int64_t)yu * Ws + x) * C + c]);
+#pragma unroll
+  for (int c = 0; c < (CC ? CC : 4); ++c) {
+    if (c >= C) break;
+    const float dx = __fsub_rn(pr[c], pl[c]);
+    const float dy = __fsub_rn(pd[c], pu[c]);
     const float m = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
     if (c == 0 || m > best) {
       best = m;
@@ -122,16 +178,22 @@ hog_cells_kernel(const float* __restrict__ R, float* __restrict__ hist,
   const int cy0 = (tile / ntx) * HOG_TC, cx0 = (tile % ntx) * HOG_TC;
   const int py0 = cy0 * HOG_SBIN - 2, px0 = cx0 * HOG_SBIN - 2;
   const float* Rl = R + j.r_off;
-  for (int e = threadIdx.x; e < HOG_TP * HOG_TP; e += HOG_THREADS) {
-    const int ry = e / HOG_TP, rx = e - ry * HOG_TP;
-    const int y = py0 + ry, x = px0 + rx;
-    float v = 0.f;
-    int b = 0;
-    // only pixels of whole cells contribute
-    if (y >= 0 && x >= 0 && y < Hc * HOG_SBIN && x < Wc * HOG_SBIN) grad_bin(Rl, j.Hs, j.Ws, j.C, y, x, v, b);
-    sv[e] = v;
-    sb[e] = (uint8_t)b;
-  }
+  auto stage = [&](auto cc) {
+    for (int e = threadIdx.x; e < HOG_TP * HOG_TP; e += HOG_THREADS) {
+      const int ry = e / HOG_TP, rx = e - ry * HOG_TP;
+      const int y = py0 + ry, x = px0 + rx;
+      float v = 0.f;
+      int b = 0;
+      // only pixels of whole cells contribute
+      if (y >= 0 && x >= 0 && y < Hc * HOG_SBIN && x < Wc * HOG_SBIN)
+        grad_bin<decltype(cc)::value>(Rl, j.Hs, j.Ws, j.C, y, x, v, b);
+      sv[e] = v;
+      sb[e] = (uint8_t)b;
+    }
+  };
+  if (j.C == 3) stage(std::integral_constant<int, 3>{});
+  else if (j.C == 1) stage(std::integral_constant<int, 1>{});
+  else stage(std::integral_constant<int, 0>{});
   float* h = sh + threadIdx.x * HOG_HPITCH;
 #pragma unroll
   for (int o = 0; o < 18; ++o) h[o] = 0.f;
@@ -140,18 +202,20 @@ hog_cells_kernel(const float* __restrict__ R, float* __restrict__ hist,
   if (cy >= Hc || cx >= Wc) return;
   // support: pixels 4c-2 .. 4c+5 on each axis (bilinear weights over cell centres)
   const int ly = (cy - cy0) * HOG_SBIN, lx = (cx - cx0) * HOG_SBIN;  // staged index of pixel 4c-2
+  // Bilinear weight of support pixel a (pixel 4c - 2 + a) towards cell c:
+  // ((p + 0.5) / 4 - 0.5 has fraction (2a + 1) / 8 below the cell centre and
+  // 1 - that above it; every step is exact in FP32, so these constants are
+  // the values the rounded intrinsics produce (oracle/hog_oracle.py).
+  constexpr float kW[2 * HOG_SBIN] = {0.125f, 0.375f, 0.625f, 0.875f, 0.875f, 0.625f, 0.375f, 0.125f};
+  const float* pv = sv + ly * HOG_TP + lx;
+  const uint8_t* pb = sb + ly * HOG_TP + lx;
+#pragma unroll
   for (int a = 0; a < 2 * HOG_SBIN; ++a) {
-    const int y = cy * HOG_SBIN - 2 + a;
-    const float yp = __fsub_rn(__fmul_rn((float)y + 0.5f, 0.25f), 0.5f);
-    const float fy = floorf(yp);
-    const float wy = (int)fy == cy ? __fsub_rn(1.f, __fsub_rn(yp, fy)) : __fsub_rn(yp, fy);
+#pragma unroll
     for (int b = 0; b < 2 * HOG_SBIN; ++b) {
-      const int x = cx * HOG_SBIN - 2 + b;
-      const float xp = __fsub_rn(__fmul_rn((float)x + 0.5f, 0.25f), 0.5f);
-      const float fx = floorf(xp);
-      const float wx = (int)fx == cx ? __fsub_rn(1.f, __fsub_rn(xp, fx)) : __fsub_rn(xp, fx);
-      const int si = (ly + a) * HOG_TP + lx + b;
-      h[sb[si]] = __fadd_rn(h[sb[si]], __fmul_rn(__fmul_rn(wy, wx), sv[si]));
+      const int si = a * HOG_TP + b;
+      float* hb = h + pb[si];
+      *hb = __fadd_rn(*hb, __fmul_rn(__fmul_rn(kW[a], kW[b]), pv[si]));
     }
   }
   float* g = hist + j.h_off + ((int64_t)cy * Wc + cx) * 20;  // 18 bins, E, pad
@@ -236,6 +300,7 @@ extern "C" int64_t dpm_resample_prepare(dpm_resample_job* jobs, int njobs) {
                     j.C >= 1 && j.C <= 4 && j.img_off >= 0 && j.out_off >= 0,
                 "dpm_resample_prepare: job %d resamples %dx%dx%d to %dx%d", i, j.H, j.W, j.C, j.Hs,
                 j.Ws);
+    DPM_REQUIRE((int64_t)j.H * j.W * j.C < INT32_MAX, "dpm_resample_prepare: job %d too large", i);
     j.block0 = (int32_t)b;
     b += ((int64_t)j.Hs * j.Ws + RS_THREADS - 1) / RS_THREADS;
   }
@@ -265,6 +330,7 @@ extern "C" int64_t dpm_hog_prepare(dpm_hog_job* jobs, int njobs) {
     DPM_REQUIRE(j.Hs >= HOG_SBIN && j.Ws >= HOG_SBIN && j.C >= 1 && j.C <= 4 && j.r_off >= 0 &&
                     j.x_off >= 0 && j.h_off >= 0 && j.x_off % 4 == 0,
                 "dpm_hog_prepare: job %d (%dx%dx%d)", i, j.Hs, j.Ws, j.C);
+    DPM_REQUIRE((int64_t)j.Hs * j.Ws * j.C < INT32_MAX, "dpm_hog_prepare: job %d too large", i);
     j.block0 = (int32_t)b;
     const int Hc = j.Hs / HOG_SBIN, Wc = j.Ws / HOG_SBIN;
     b += (int64_t)((Hc + HOG_TC - 1) / HOG_TC) * ((Wc + HOG_TC - 1) / HOG_TC);
