@@ -108,7 +108,8 @@ project_kernel(const float* __restrict__ X, float* __restrict__ P, const float* 
 // (3xTF32: lo*hi + hi*lo + hi*hi, FP32 accumulate), so the shared-memory
 // staging, its barrier and the per-channel LDS of project_kernel disappear
 // and the kernel is eight 16-byte loads, 24 MMAs and eight stores per warp
-// and 32 cells.  A warp owns 32 consecutive cells as two 16-row A tiles.
+// and 32 cells.  A warp owns 32 consecutive cells as two 16-row A tiles
+// (and K1_TPW such tiles one after the other, all loads issued up front).
 // The MMA's k index is a free permutation of the channels: lane (g, t)
 // loads chunks t and t + 4 (channels 4t.., 16 + 4t..) of cells g and g + 8,
 // and k-step e takes element e of both chunks, so column t of step e is
@@ -133,7 +134,19 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(K1_CELLS, 3)
+// Tiles (32 cells) per warp: a CTA still owns K1_CELLS cells, with
+// K1_CELLS / (32 K1_TPW) warps.  Two tiles per warp share the job lookup and
+// the B operands and keep 8 KB of loads per warp in flight.
+#ifndef DPM_K1_TPW
+#define DPM_K1_TPW 2
+#endif
+constexpr int K1_TPW = DPM_K1_TPW;
+constexpr int K1_MMA_THREADS = K1_CELLS / K1_TPW;
+
+#ifndef DPM_K1_CTAS
+#define DPM_K1_CTAS (K1_TPW == 1 ? 3 : 5)
+#endif
+__global__ void __launch_bounds__(K1_MMA_THREADS, DPM_K1_CTAS)
 project_mma_kernel(const float* __restrict__ X, float* __restrict__ P, const float* __restrict__ C,
                    int R, const dpm_proj_job* __restrict__ jobs, int njobs) {
   constexpr int L = 32;
@@ -142,29 +155,36 @@ project_mma_kernel(const float* __restrict__ X, float* __restrict__ P, const flo
   const int ncl = job.H * job.W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int c0 = (blockIdx.x - job.block0) * K1_CELLS + warp * 32;
-  DPM_CHECK(c0 >= 0, "CTA cells inside its level");
-  if (c0 >= ncl) return;  // no CTA barrier below: a warp past the level's end just leaves
+  const int cw = (blockIdx.x - job.block0) * K1_CELLS + warp * (32 * K1_TPW);
+  DPM_CHECK(cw >= 0, "CTA cells inside its level");
+  if (cw >= ncl) return;  // no CTA barrier below: a warp past the level's end just leaves
 
-  // ---- loads: all eight 16-byte chunks of the warp's 32 cells in flight.
-  // q[k][v]: chunk t + 4v of cell c0 + 8k + g (k = 2h + u: tile h, row half u)
-  const float* src = X + job.x_off + (int64_t)(c0 + g) * L + 4 * t;
-  float4 q[4][2];
-  if (c0 + 32 <= ncl && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+  // ---- loads: all eight 16-byte chunks of each of the warp's tiles in flight.
+  // q[i][k][v]: chunk t + 4v of cell cw + 32i + 8k + g (k = 2h + u: A tile h, row half u)
+  const float* src = X + job.x_off + (int64_t)(cw + g) * L + 4 * t;
+  const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  float4 q[K1_TPW][4][2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+  for (int i = 0; i < K1_TPW; ++i) {
+    const int c0 = cw + 32 * i;
+    const float* s = src + 32 * i * L;
+    if (c0 + 32 <= ncl && al16) {
 #pragma unroll
-      for (int v = 0; v < 2; ++v)
-        q[k][v] = __ldcs(reinterpret_cast<const float4*>(src + 8 * k * L + 16 * v));
-  } else {  // a level's last cells, or a feature block off 16-byte alignment
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+        for (int v = 0; v < 2; ++v)
+          q[i][k][v] = __ldcs(reinterpret_cast<const float4*>(s + 8 * k * L + 16 * v));
+    } else {  // a level's last cells, or a feature block off 16-byte alignment
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const float* a = src + 8 * k * L + 16 * v;
-        q[k][v] = c0 + 8 * k + g < ncl ? make_float4(__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const float* a = s + 8 * k * L + 16 * v;
+          q[i][k][v] = c0 + 8 * k + g < ncl
+                           ? make_float4(__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
   }
 
   const int64_t plane = (int64_t)job.H * job.pitch;
@@ -178,34 +198,38 @@ project_mma_kernel(const float* __restrict__ X, float* __restrict__ P, const flo
       split_tf32(g < R ? __ldg(C + (16 * v + 4 * t + e) * R + g) : 0.f, bhi[e][v], blo[e][v]);
   const int ra = 2 * t;
   float* const Pr = P + job.p_off + (int64_t)ra * plane;
-  int y = (c0 + g) / job.W, x = (c0 + g) - y * job.W;  // the other three cells follow by +8 with row wraps
+  int y = (cw + g) / job.W, x = (cw + g) - y * job.W;  // the other cells follow by +8 with row wraps
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float d[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < K1_TPW; ++i) {
+    if (cw + 32 * i >= ncl) break;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      // A operands of k-step e: element e of the four chunks, a[u + 2v]
-      uint32_t ahi[4], alo[4];
+    for (int h = 0; h < 2; ++h) {
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int e = 0; e < 4; ++e) {
+        // A operands of k-step e: element e of the four chunks, a[u + 2v]
+        uint32_t ahi[4], alo[4];
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const float4 f = q[2 * h + u][v];
-          split_tf32(e == 0 ? f.x : e == 1 ? f.y : e == 2 ? f.z : f.w, ahi[u + 2 * v], alo[u + 2 * v]);
-        }
-      mma_tf32(d, alo, bhi[e][0], bhi[e][1]);  // small terms first
-      mma_tf32(d, ahi, blo[e][0], blo[e][1]);
-      mma_tf32(d, ahi, bhi[e][0], bhi[e][1]);
-    }
+        for (int u = 0; u < 2; ++u)
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      if (c0 + 16 * h + 8 * u + g < ncl) {
-        const int o = y * job.pitch + x;
-        if (ra < R) Pr[o] = d[2 * u];
-        if (ra + 1 < R) Pr[plane + o] = d[2 * u + 1];
+          for (int v = 0; v < 2; ++v) {
+            const float4 f = q[i][2 * h + u][v];
+            split_tf32(e == 0 ? f.x : e == 1 ? f.y : e == 2 ? f.z : f.w, ahi[u + 2 * v], alo[u + 2 * v]);
+          }
+        mma_tf32(d, alo, bhi[e][0], bhi[e][1]);  // small terms first
+        mma_tf32(d, ahi, blo[e][0], blo[e][1]);
+        mma_tf32(d, ahi, bhi[e][0], bhi[e][1]);
       }
-      x += 8;
-      while (x >= job.W) { x -= job.W; ++y; }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (cw + 32 * i + 16 * h + 8 * u + g < ncl) {
+          const int o = y * job.pitch + x;
+          if (ra < R) Pr[o] = d[2 * u];
+          if (ra + 1 < R) Pr[plane + o] = d[2 * u + 1];
+        }
+        x += 8;
+        while (x >= job.W) { x -= job.W; ++y; }
+      }
     }
   }
 }
@@ -253,7 +277,7 @@ extern "C" int dpm_project(const float* X, float* P, const float* C, int L, int 
   DPM_REQUIRE(njobs >= 0 && nblocks >= 0 && nblocks <= INT32_MAX, "dpm_project: bad sizes");
   if (njobs == 0 || nblocks == 0) return DPM_OK;
   if (L == 32 && R <= 8 && mma_enabled()) {
-    project_mma_kernel<<<(unsigned)nblocks, K1_CELLS, 0, as_stream(stream)>>>(X, P, C, R, jobs, njobs);
+    project_mma_kernel<<<(unsigned)nblocks, K1_MMA_THREADS, 0, as_stream(stream)>>>(X, P, C, R, jobs, njobs);
     DPM_LAUNCHED("project_mma_kernel");
     return DPM_OK;
   }

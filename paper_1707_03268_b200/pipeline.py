@@ -143,7 +143,7 @@ class PyramidScorer:
                          init_ranges=(k == 0))
             return plan.detections()
 
-    def score_images(self, host_images, tau, stream=None, chunk_images=2):
+    def score_images(self, host_images, tau, stream=None, chunk_images=16):
         """Public end-to-end call from images: host images (n_images, H, W, C)
         uint8 or float32 in [0, 255] (pinned for async copies) in, detection
         records >= tau out.  The 32-channel HOG pyramid of every image is

@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--images", type=int, default=64)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--chunk", type=int, default=4)
+    ap.add_argument("--chunk", type=int, default=16)
     args = ap.parse_args()
 
     import torch
