@@ -65,7 +65,11 @@ int dpm_device_query(int device, int* sm_count, int* cc_major, int* cc_minor);
  * P[r][y][x] = sum_l X[y][x][l] * C[l][r]
  * Replaces the channel contraction of _term_stack (correlation.py:128) and,
  * with C = identity, the channel layout change feeding correlate3_full
- * (correlation.py:92-112).  One job per (image, level). */
+ * (correlation.py:92-112).  One job per (image, level).
+ * L = 32 with R <= 8 runs on mma.sync tensor-core tiles (3xTF32 split, FP32
+ * accumulation; within 2e-6 of max |P| of the float64 product, as the FFMA
+ * path is); every other shape on FP32 FFMA.  A prefix
+ * of C's columns gives bit-identical planes on either path. */
 typedef struct {
   int64_t x_off;  /* float offset of the level's X block [H][W][L]          */
   int64_t p_off;  /* float offset of the level's P block [R][H][pitch]      */
