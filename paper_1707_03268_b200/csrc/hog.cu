@@ -59,6 +59,7 @@ __device__ __forceinline__ void resample_body(const T* __restrict__ img, float* 
   const int ix0 = (int)floorf(ax), ix1 = min((int)ceilf(bx), j.W);
   const T* base = img + j.img_off;
   const int nx = ix1 - ix0;
+  DPM_CHECK(iy0 >= 0 && ix0 >= 0 && iy1 <= j.H && ix1 <= j.W && nx >= 1, "box support inside the source");
   float acc[CM];
 #pragma unroll
   for (int c = 0; c < CM; ++c) acc[c] = 0.f;

@@ -224,6 +224,7 @@ project_mma_kernel(const float* __restrict__ X, float* __restrict__ P, const flo
       for (int u = 0; u < 2; ++u) {
         if (cw + 32 * i + 16 * h + 8 * u + g < ncl) {
           const int o = y * job.pitch + x;
+          DPM_CHECK(y >= 0 && y < job.H && x >= 0 && x < job.W, "output cell inside its level");
           if (ra < R) Pr[o] = d[2 * u];
           if (ra + 1 < R) Pr[plane + o] = d[2 * u + 1];
         }
