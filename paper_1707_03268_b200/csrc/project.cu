@@ -251,6 +251,10 @@ extern "C" int64_t dpm_project_prepare(dpm_proj_job* jobs, int njobs) {
       set_error("dpm_project_prepare: job %d has H=%d W=%d pitch=%d", i, j.H, j.W, j.pitch);
       return DPM_ERR_ARG;
     }
+    if ((int64_t)j.H * j.pitch > INT32_MAX) {  // the kernels index a level's plane with 32 bits
+      set_error("dpm_project_prepare: job %d level %dx%d (pitch %d) too large", i, j.H, j.W, j.pitch);
+      return DPM_ERR_ARG;
+    }
     jobs[i].block0 = (int32_t)b;
     b += ((int64_t)j.H * j.W + K1_CELLS - 1) / K1_CELLS;
   }

@@ -86,6 +86,10 @@ def test_prepare_validates_and_numbers_blocks():
     jobs["pitch"][1] = 6  # not a multiple of 4
     with pytest.raises(Exception, match="pitch"):
         _lib.check(lib.dpm_project_prepare(_lib.table_ptr(jobs), 2))
+    jobs["pitch"][1] = 8
+    jobs["H"][0], jobs["W"][0], jobs["pitch"][0] = 70000, 70000, 70000  # plane past 2^31 floats
+    with pytest.raises(Exception, match="too large"):
+        _lib.check(lib.dpm_project_prepare(_lib.table_ptr(jobs), 2))
     pj = np.zeros(1, dtype=_lib.PLACE_JOB)
     pj["Hp"], pj["Wp"], pj["scale"], pj["radius"], pj["range_idx"], pj["wr"] = 5, 5, 1, -1, 0, 5
     with pytest.raises(Exception, match="c_dxx"):
